@@ -1,0 +1,311 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: one step = one full preconditioned FGMRES solve of a BASELINE
+workload (setup of the coefficients / line factors / multigrid levels + the solve), the
+paper's time-to-solution.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg4]
+
+Default workload: cfg4 (B:10), 4096^2 Shishkin mesh, eps = 1e-8, variable convection, seeded
+random f, Jacobi-weighted rtol 1e-8.  Prints ONE JSON line (rank 0).
+For N > 1 (torchrun) every rank solves its own replica (weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+import spp_inputs as si  # noqa: E402
+
+BASELINE = json.loads((ROOT / "BASELINE.json").read_text())
+METRIC = BASELINE["metric"]
+UNIT = "unknowns/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--n", type=int, default=None, help="override N (diagnostics only)")
+    ap.add_argument("--eps", type=float, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-all", action="store_true", help="print the per-class profile to stderr")
+    return ap.parse_args()
+
+
+def _workload(cfg):
+    return (f"{cfg.name}: -eps Lap u - c.grad u + r u = f, {cfg.N}x{cfg.N} Shishkin mesh "
+            f"(sigma=2, beta=1), eps={cfg.eps:g}, Jacobi-weighted rtol {cfg.tol:g}, fp64")
+
+
+# ---------------------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampled every 200 ms DURING the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(self.idx)], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        for line in Path(self.f.name).read_text().splitlines():
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """The oracle, as it stands, on the host cores (the CPU reference arm of this tier)."""
+    if rank != 0:
+        return None
+    import oracle
+    cfg = si.config(args.config, N=args.n, eps=args.eps)
+    N = cfg.N
+    x = oracle.mesh(N, cfg.eps, cfg.sigma, cfg.beta_x)
+    y = oracle.mesh(N, cfg.eps, cfg.sigma, cfg.beta_y)
+    c1, c2, r, f = si.sample_2d(cfg, x, y)
+
+    def step():
+        P = oracle.Oracle2D(N, cfg.eps, x, y, c1, c2, r)      # setup
+        res = P.solve(f, weighted=cfg.weighted, stop_abs=cfg.stop_abs, tol=cfg.tol)
+        P.close()
+        return res
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = step()
+    dt = (time.perf_counter() - t0) / args.steps
+    val = cfg.unknowns / dt
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": _workload(cfg), "N": N, "unknowns": cfg.unknowns, "iters": res["iters"]},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"one full {cfg.name} solve (setup + FGMRES, {res['iters']} iterations) "
+                                       f"per step, single-threaded C oracle"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    return line
+
+
+# ---------------------------------------------------------------------------- our arm
+def cpu_baseline(cfg):
+    """The oracle timed on this host on a bounded sample: one full solve of the same workload
+    (~10 s of single-threaded CPU work at 4096^2)."""
+    import oracle
+    N = cfg.N
+    x = oracle.mesh(N, cfg.eps, cfg.sigma, cfg.beta_x)
+    y = oracle.mesh(N, cfg.eps, cfg.sigma, cfg.beta_y)
+    c1, c2, r, f = si.sample_2d(cfg, x, y)
+    t0 = time.perf_counter()
+    P = oracle.Oracle2D(N, cfg.eps, x, y, c1, c2, r)
+    res = P.solve(f, weighted=cfg.weighted, stop_abs=cfg.stop_abs, tol=cfg.tol)
+    dt = time.perf_counter() - t0
+    P.close()
+    return {"value": cfg.unknowns / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"one full {cfg.name} solve (setup + FGMRES, {res['iters']} iterations), {dt:.2f} s"}
+
+
+def run_ours(args, rank, world):
+    import torch
+    import paper_2108_13468_b200 as spp
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    cfg = si.config(args.config, N=args.n, eps=args.eps)
+    N, m = cfg.N, cfg.N - 1
+    x = spp.spp_shishkin_mesh(N, cfg.eps, cfg.sigma, cfg.beta_x)
+    y = spp.spp_shishkin_mesh(N, cfg.eps, cfg.sigma, cfg.beta_y)
+    c1, c2, r, f = si.sample_2d(cfg, x, y)
+    host = [np.ascontiguousarray(a).ravel() for a in (c1, c2, r, f)]
+    d_c1, d_c2, d_r, d_f = [torch.from_numpy(a).to(dev) for a in host]
+    u = torch.empty_like(d_f)
+    o = spp.spp_default_options(2)
+    o.stop = spp.SPP_STOP_REL_JACOBI if cfg.weighted else (spp.SPP_STOP_ABS_L2 if cfg.stop_abs else spp.SPP_STOP_REL_L2)
+    o.tol = cfg.tol
+    stream = torch.cuda.current_stream(dev)
+    S = spp.Solver(2, N, cfg.eps, x, y, d_c1, d_c2, d_r, options=o, stream=stream)
+
+    def step(c1_, c2_, r_, f_, u_):
+        S.setup(c1_, c2_, r_)
+        return S.solve(f_, u_)
+
+    # warm-up with every kernel class profiled, to find the dominant kernel class
+    S.profile_enable(1)
+    res = None
+    for _ in range(args.warmup):
+        res = step(d_c1, d_c2, d_r, d_f, u)
+    prof = S.profile()
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    dom_idx = list(prof).index(dom)
+    if args.profile_all and rank == 0:
+        tot = sum(v["ms"] for v in prof.values())
+        for k, v in prof.items():
+            if v["launches"]:
+                print(f"[prof] {k:18s} launches={v['launches']:6d} ms={v['ms']:9.3f} ({100*v['ms']/tot:5.1f}%) "
+                      f"GB/s={v['bytes']/max(v['ms'],1e-9)/1e6:8.1f}", file=sys.stderr)
+    S.profile_reset()
+    S.profile_enable(1 << dom_idx)
+
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(dev.index)
+    clk.start()
+    l0 = S.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = []
+    e0.record(stream)
+    for _ in range(args.steps):
+        res = step(d_c1, d_c2, d_r, d_f, u)
+        iters.append(res.stats["iters"])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    launches = S.kernel_launches() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    prof = S.profile()[dom]
+    S.profile_enable(0)
+
+    # e2e: the same step through the public API with pinned HOST buffers (H2D of c1, c2, r, f
+    # and D2H of u inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        hp = [torch.from_numpy(a).pin_memory() for a in host]
+        hu = torch.empty(m * m, dtype=torch.float64).pin_memory()
+        step(hp[0], hp[1], hp[2], hp[3], hu)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        ne = max(1, min(args.steps, 3))
+        for _ in range(ne):
+            step(hp[0], hp[1], hp[2], hp[3], hu)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / ne
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": cfg.unknowns * world / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": 4 * m * m * 8, "d2h_bytes_per_step": m * m * 8, "ms_per_step": ems}
+
+    if rank != 0:
+        return None
+    peak, peak_kind = _peaks()
+    avg_ms = prof["ms"] / max(prof["launches"], 1)
+    avg_bytes = prof["bytes"] / max(prof["launches"], 1)
+    achieved = avg_bytes / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(f"{cfg.name}:{dom}")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": cfg.unknowns * world / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": _workload(cfg), "N": N, "unknowns": cfg.unknowns,
+                   "iters_per_solve": iters[-1], "mg_cycles_per_apply": [res.stats["mg_cycles_min"], res.stats["mg_cycles_max"]],
+                   "time_to_solution_s": ms * 1e-3, "setup_s": res.stats["setup_s"],
+                   "l2": "inputs larger than L2 (each grid function 134 MB > 126 MB L2)",
+                   "parallelism": "replicas" if world > 1 else "single GPU"},
+        "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "avg_launch_ms": avg_ms, "algorithmic_bytes_per_launch": avg_bytes},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    return line
+
+
+def main():
+    args = _args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group(backend)
+    line = run_reference(args, rank, world) if args.impl == "reference" else run_ours(args, rank, world)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

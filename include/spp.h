@@ -1,0 +1,194 @@
+/*
+ * spp.h -- C ABI of the B200-native solver for singularly perturbed convection-diffusion
+ * on Shishkin meshes (hot path of arXiv 2108.13468).
+ *
+ *   -eps Lap(u) - c . grad(u) + r u = f  on (0,1)^dim,  u = 0 on the boundary
+ *   (eq:1D / eq:2D), first-order upwind finite differences (eq:stencil_1d,
+ *   P:242-247; 5-point stencil P:964-987) on a (tensor-product) Shishkin mesh (eq:tau 1D,
+ *   P:278-284; eq:tau exponential), solved by FGMRES right-
+ *   preconditioned with the paper's block preconditioner: 1D eq:block_M; 2D
+ *   eq:2D blocks = downstream Gauss-Seidel on I, line solves on
+ *   Y and X, full-coarsening multigrid on the corner
+ *   (P:1263-1287).
+ *
+ * Everything runs in sm_100a CUDA kernels in fp64.  No CPU fallback: every entry point that
+ * computes returns SPP_E_CUDA if no usable device is present.
+ *
+ * Conventions
+ *   - N ("n" below) = number of mesh intervals per axis; interior unknowns (N-1)^dim.
+ *   - Grid functions passed through the ABI are "compact": (N-1)^dim doubles, x fastest,
+ *     index (j-1)*(N-1) + (i-1) for node (x_i, y_j), i, j = 1..N-1 (1D: i-1).
+ *   - Pointers are host or device (cudaMalloc'd / torch CUDA tensors) as `spp_mem` says.
+ *   - Ownership: the caller owns every buffer it passes.  spp_create copies what it needs
+ *     into library-owned device memory and keeps no caller pointer.  spp_solve reads f and
+ *     writes u_out / res_hist only during the call, on the context's stream, and
+ *     synchronises that stream before returning.
+ *   - Threading: one context per thread/stream; a context is not thread-safe; there is no
+ *     global mutable state except the thread-local error message.
+ *   - Errors: status codes only (no exceptions cross the ABI).  Positive = result valid with
+ *     a flag set; negative = failure, outputs undefined, spp_last_error() explains.
+ */
+#ifndef SPP_H
+#define SPP_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SPP_API __attribute__((visibility("default")))
+#else
+#define SPP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SPP_OK = 0,
+    SPP_NOT_CONVERGED = 1,  /* max_iters reached; last iterate + full history returned */
+    SPP_E_ARG = -1,         /* bad argument: N odd/too small, eps not in (0,1], NULL pointer ... */
+    SPP_E_MESH = -2,        /* coordinates are not a piecewise-uniform mesh broken at N/2     */
+    SPP_E_COEF = -3,        /* c1 <= 0, c2 <= 0 (2D), r < 0, or non-finite  */
+    SPP_E_PIVOT = -4,       /* zero / non-finite Thomas pivot                          */
+    SPP_E_MG_CAP = -5,      /* corner MG hit mg_max_cycles in strict mode                      */
+    SPP_E_CUDA = -6,        /* CUDA runtime error, or no usable device                         */
+    SPP_E_NCCL = -7,
+    SPP_E_NOMEM = -8,       /* device or host allocation failed                                */
+    SPP_E_STATE = -9        /* call not valid in this context state                            */
+} spp_status;
+
+typedef enum { SPP_HOST = 0, SPP_DEVICE = 1 } spp_mem;
+
+typedef enum {
+    SPP_STOP_REL_JACOBI = 0, /* ||D^{-1}(f - A u)||_2 <= tol ||D^{-1} f||_2 (recurrence), the
+                                BASELINE "relative residual" (reading R11)       */
+    SPP_STOP_REL_L2 = 1,     /* ||f - A u||_2 <= tol ||f||_2 (recurrence, unweighted)        */
+    SPP_STOP_ABS_L2 = 2,     /* ||f - A u||_2 <= tol (paper 2D: tol = 10 N^{-1} ln N)*/
+    SPP_STOP_ABS_MAX = 3     /* true ||f - A u||_inf <= tol (paper 1D: K N^{-1} ln N);
+                                1D with side = SPP_LEFT only                                 */
+} spp_stop;
+
+typedef enum {
+    SPP_RIGHT_FLEXIBLE = 0,  /* FGMRES, right preconditioned, flexible         */
+    SPP_LEFT = 1             /* left-preconditioned GMRES, 1D paper mode         */
+} spp_side;
+
+typedef struct {
+    int32_t dim;             /* 1 or 2                                                       */
+    int32_t n;               /* N intervals per axis: even, >= 4 (1D) / >= 8 with N/2 a power
+                                of two (2D, full coarsening of the corner)            */
+    double eps;              /* perturbation parameter, (0, 1]                               */
+    const double *x, *y;     /* HOST node coordinates, N+1 each: x[0]=0, x[N]=1, uniform on
+                                [0, x[N/2]] and on [x[N/2], 1] (Shishkin); y NULL
+                                in 1D.  The library uses tau = x[N/2] (reading R12).          */
+    const double *c1, *c2, *r; /* coefficient samples at interior nodes (compact layout);
+                                c2 NULL in 1D.  Residency per `mem`.                        */
+    spp_mem mem;
+} spp_problem;
+
+typedef struct {
+    spp_side side;
+    spp_stop stop;
+    double tol;
+    int32_t max_iters;       /* Arnoldi steps (default 200)                           */
+    int32_t restart;         /* 0 = no restart (paper); other values reserved         */
+    double mg_reduction;     /* corner MG relative reduction of ||S_0 rho||_2 (1e-3) */
+    int32_t mg_max_cycles;   /* cycle cap (20)                                        */
+    int32_t mg_fixed_cycles; /* 0 = adaptive (paper); > 0 = exactly this many (parity mode)  */
+    int32_t mg_coarsest;     /* coarsen until <= this many points per axis (4)        */
+    int32_t fixed_iters;     /* 0 = run to tolerance; > 0 = exactly this many Arnoldi steps  */
+    int32_t mg_strict;       /* 1 = return SPP_E_MG_CAP when the cap is hit                  */
+    int32_t reserved[7];
+} spp_options;
+
+typedef struct {
+    int32_t iters;           /* Arnoldi steps = preconditioner applications         */
+    int32_t converged;
+    int32_t mg_cycles_total, mg_cycles_min, mg_cycles_max, mg_cap_hits, applies;
+    int32_t kernel_launches; /* CUDA kernels launched by this call                           */
+    double res0, res_final;  /* monitored residual (per `stop`) at start / end               */
+    double true_res_l2_rel;     /* ||f - A u||_2 / ||f||_2 after the solve                   */
+    double true_res_jacobi_rel; /* ||D^{-1}(f - A u)||_2 / ||D^{-1} f||_2                    */
+    double setup_s, solve_s;    /* device time of the last spp_setup / this spp_solve        */
+} spp_stats;
+
+typedef struct spp_ctx spp_ctx;
+
+/* Defaults: right/flexible, SPP_STOP_REL_JACOBI, tol 1e-8, 200 iterations, MG 1e-3 / 20 /
+ * adaptive / coarsest 4. */
+SPP_API void spp_default_options(int32_t dim, spp_options *o);
+
+/* Shishkin mesh on the host (eq:tau 1D P:278-284 / eq:tau exponential P:914-928):
+ * tau = min(1/2, sigma*eps*ln(n)/beta); n/2 uniform intervals on [0,tau] and on [tau,1].
+ * x_out: n+1 doubles (host).  SPP_E_ARG for odd n < 4, eps not in (0,1], sigma/beta <= 0. */
+SPP_API spp_status spp_shishkin_mesh(int32_t n, double eps, double sigma, double beta, double *x_out);
+
+/* Validate the problem, allocate the device workspace on `cuda_stream` (NULL = legacy default
+ * stream) and run the setup (coefficients, corner multigrid levels, line factorisations;
+ * counted in time-to-solution as the paper does). */
+SPP_API spp_status spp_create(const spp_problem *p, const spp_options *o, void *cuda_stream, spp_ctx **out);
+
+/* Re-run the setup for new coefficient samples on the same mesh (c2 NULL in 1D). */
+SPP_API spp_status spp_setup(spp_ctx *c, const double *c1, const double *c2, const double *r, spp_mem mem);
+
+/* Solve A u = f.  f, u_out: compact grid functions with residency `mem`.  res_hist (host,
+ * may be NULL) receives the monitored residual, iters+1 entries truncated at res_hist_cap.
+ * st (host, may be NULL).  Returns SPP_OK, SPP_NOT_CONVERGED or an error. */
+SPP_API spp_status spp_solve(spp_ctx *c, const double *f, double *u_out, spp_mem mem,
+                     double *res_hist, int32_t res_hist_cap, spp_stats *st);
+
+/* Test hooks (per-kernel parity with the oracle).  in/out are DEVICE pointers in the compact
+ * layout of the stage:  global grid (N-1)^2 for MATVEC, PRECOND, MII, MYY, MXX;
+ * corner block (N/2)^2 for CORNER_SOLVE, and level-l corner grids (n_l)^2 for GS_SWEEP,
+ * VCYCLE, RESTRICT (in: level l, out: level l+1), PROLONG_ADD (in: level l+1, out: level l,
+ * accumulated), LEVEL_RESIDUAL (in: [b | e] stacked, out: rho).
+ *   MATVEC     out = A in (unweighted, difference form)
+ *   PRECOND    out = M^{-1} in                      (cycles_out: corner MG cycles)
+ *   MII        out = in with region I replaced by M_II^{-1} in_I
+ *   MYY / MXX  out = in with region Y / X replaced by its line solves, using `out`'s current
+ *              values as the already-solved neighbours (call MII first; out is in/out)
+ *   CORNER_RHS out (corner, (N/2)^2) = b_C built from in (global) and out's X/Y neighbours --
+ *              in is the stacked pair [q | z] (2*(N-1)^2)
+ *   GS_SWEEP   out = one downstream GS sweep of A_l e = b from e = out, b = in
+ *   VCYCLE     out = V(1,1) cycle on level l for rhs in, zero initial guess
+ *   CORNER_SOLVE out = M_CC^{-1} in (adaptive cycles; cycles_out). */
+typedef enum {
+    SPP_STAGE_MATVEC = 0, SPP_STAGE_MII = 1, SPP_STAGE_MYY = 2, SPP_STAGE_MXX = 3,
+    SPP_STAGE_CORNER_RHS = 4, SPP_STAGE_GS_SWEEP = 5, SPP_STAGE_VCYCLE = 6,
+    SPP_STAGE_CORNER_SOLVE = 7, SPP_STAGE_PRECOND = 8, SPP_STAGE_RESTRICT = 9,
+    SPP_STAGE_PROLONG_ADD = 10, SPP_STAGE_LEVEL_RESIDUAL = 11
+} spp_stage;
+SPP_API spp_status spp_apply_stage(spp_ctx *c, spp_stage s, int32_t level, const double *in, double *out,
+                           int32_t *cycles_out);
+
+/* Total CUDA kernels launched by this context since spp_create (setup + solves + hooks). */
+SPP_API int64_t spp_kernel_launches(const spp_ctx *c);
+
+/* Number of corner MG levels and the unknowns per axis of level l. */
+SPP_API int32_t spp_mg_levels(const spp_ctx *c);
+SPP_API int32_t spp_mg_level_n(const spp_ctx *c, int32_t l);
+
+/* Per-kernel-class device timing (CUDA events on the context stream).  enable != 0 records
+ * events around every launch of the listed classes during subsequent spp_solve calls.
+ * spp_profile_get returns, for class k, the launch count, total milliseconds and the
+ * algorithmic bytes moved accumulated since the last reset.
+ * Classes: 0 spmv, 1 sweep_I, 2 lines_XY, 3 mg_sweep, 4 mg_resid_restrict, 5 mg_prolong,
+ * 6 mg_update, 7 mgs (Krylov vector ops), 8 setup, 9 other. */
+#define SPP_PROF_CLASSES 10
+SPP_API spp_status spp_profile_enable(spp_ctx *c, int32_t enable);
+SPP_API spp_status spp_profile_reset(spp_ctx *c);
+SPP_API spp_status spp_profile_get(const spp_ctx *c, int32_t k, int64_t *launches, double *ms, double *bytes);
+SPP_API const char *spp_profile_name(int32_t k);
+
+SPP_API void spp_destroy(spp_ctx *c);
+
+/* Last error message for this context (or the thread-local one when c == NULL). */
+SPP_API const char *spp_last_error(const spp_ctx *c);
+
+/* Library version string. */
+SPP_API const char *spp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPP_H */

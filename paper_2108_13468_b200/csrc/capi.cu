@@ -1,0 +1,840 @@
+// capi.cu -- the C ABI (include/spp.h): context management, setup, the FGMRES driver
+// (P:1306-1316), the block preconditioner (eq:2D blocks) and the corner
+// multigrid driver.  Every arithmetic step runs in the sm_100a kernels of
+// k_core.cu / k_sweep.cu / k_lines.cu / k_1d.cu; the host only orchestrates launches and does
+// the O(k^2) Givens/Hessenberg bookkeeping of GMRES ("host, k <= a few hundred
+// scalars").
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "kernels.cuh"
+
+using namespace spp;
+
+static thread_local std::string g_err;
+
+#define FAIL(ctx, code, ...)                                                  \
+    do {                                                                      \
+        char _b[512];                                                         \
+        snprintf(_b, sizeof(_b), __VA_ARGS__);                                \
+        if (ctx) ((Ctx *)(ctx))->err = _b;                                    \
+        g_err = _b;                                                           \
+        return code;                                                          \
+    } while (0)
+
+#define CK(ctx, expr)                                                         \
+    do {                                                                      \
+        cudaError_t _e = (expr);                                              \
+        if (_e != cudaSuccess)                                                \
+            FAIL(ctx, SPP_E_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+    } while (0)
+
+namespace spp {
+
+// ------------------------------------------------------------------------------------------ profiling
+static const char *kProfNames[SPP_PROF_CLASSES] = {"spmv", "sweep_I", "lines_XY", "mg_sweep",
+                                                   "mg_resid_restrict", "mg_prolong", "mg_update",
+                                                   "krylov_vec", "setup", "other"};
+
+ProfScope::ProfScope(Ctx *c_, int cls_, double bytes_) : c(c_), cls(cls_), bytes(bytes_)
+{
+    if (!c || !(c->prof_on & (1 << cls))) { c = nullptr; return; }
+    if (c->ev_used + 2 > c->ev_pool.size()) {
+        for (int k = 0; k < 64; ++k) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            c->ev_pool.push_back(e);
+        }
+    }
+    a = c->ev_pool[c->ev_used++];
+    cudaEventRecord(a, c->st);
+}
+ProfScope::~ProfScope()
+{
+    if (!c) return;
+    cudaEvent_t b = c->ev_pool[c->ev_used++];
+    cudaEventRecord(b, c->st);
+    c->pend.push_back({cls, a, b, bytes});
+}
+
+static void prof_collect(Ctx *c)
+{
+    if (c->pend.empty()) { c->ev_used = 0; return; }
+    cudaEventSynchronize(c->pend.back().b);
+    for (auto &p : c->pend) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, p.a, p.b);
+        c->prof[p.cls].launches++;
+        c->prof[p.cls].ms += ms;
+        c->prof[p.cls].bytes += p.bytes;
+    }
+    c->pend.clear();
+    c->ev_used = 0;
+}
+
+// ------------------------------------------------------------------------------------------ helpers
+static inline int nblk(long work, int tpb = 256, int cap = 148 * 16)
+{
+    long b = (work + tpb - 1) / tpb;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return (int)b;
+}
+
+static double host_sum(const double *p, int k)
+{
+    double s = 0.0;
+    for (int i = 0; i < k; ++i) s += p[i];
+    return s;
+}
+
+// D2H of a partial-sum block and host reduction in fixed order
+static cudaError_t fetch_sum(Ctx *c, const double *part, double *out)
+{
+    cudaError_t e = cudaMemcpyAsync(c->hpin, part, sizeof(double) * kRedBlocks, cudaMemcpyDeviceToHost, c->st);
+    if (e != cudaSuccess) return e;
+    e = cudaStreamSynchronize(c->st);
+    if (e != cudaSuccess) return e;
+    *out = host_sum(c->hpin, kRedBlocks);
+    return cudaSuccess;
+}
+
+static double *part_slot(Ctx *c, int k) { return c->part + (size_t)k * kRedBlocks; }
+
+// ------------------------------------------------------------------------------------------ sweeps
+static SweepArgs sweep_level(Ctx *c, int l, const double *q, bool scaled, double *z)
+{
+    Level &L = c->lev[l];
+    SweepArgs a{};
+    a.q = q; a.qp = L.pitch;
+    a.s = scaled ? L.cd : nullptr; a.sp = L.cpitch;
+    a.ca = L.ca; a.cn = L.cn; a.cp = L.cpitch;
+    a.z = z; a.zp = L.pitch;
+    a.ilo = 1; a.ihi = L.n; a.jlo = 1; a.jhi = L.n;
+    a.rows_out = 512; a.halo = 0;
+    a.flags = c->flags; a.epoch = 0;
+    return a;
+}
+
+static void mg_sweep(Ctx *c, int l, const double *q, bool scaled, double *z)
+{
+    Level &L = c->lev[l];
+    SweepArgs a = sweep_level(c, l, q, scaled, z);
+    launch_sweep(c, a, true, 3, 32.0 * L.n * (double)L.n + (scaled ? 8.0 * L.n * (double)L.n : 0.0));
+}
+
+// V(1,1) cycle for A_l e = b, zero initial guess.  Result in lev[l].e.
+static void vcycle(Ctx *c, int l, const double *b)
+{
+    Level &L = c->lev[l];
+    const int nl = L.n;
+    const double nn = (double)nl * nl;
+    const int gb = nblk((long)nl * nl);
+    if (l == c->L - 1) {
+        mg_sweep(c, l, b, true, L.e);                         // sweep 1 from e = 0
+        for (int s = 1; s < 4; ++s) {                         // "four sweeps"
+            {
+                ProfScope ps(c, 5, 40.0 * nn);
+                k_gs_prep<<<gb, 256, 0, c->st>>>(nl, L.pitch, L.cpitch, L.e, b, L.aW, L.aS, L.cd, L.q);
+                c->launches++;
+            }
+            mg_sweep(c, l, L.q, false, L.e);
+        }
+        return;
+    }
+    Level &C = c->lev[l + 1];
+    mg_sweep(c, l, b, true, L.e);                             // pre-smoothing from zero
+    {
+        ProfScope ps(c, 4, 48.0 * nn + 8.0 * nn + 8.0 * C.n * (double)C.n);
+        k_mg_resid<<<gb, 256, 0, c->st>>>(nl, L.pitch, L.cpitch, L.e, nullptr, b, L.aE, L.aN, L.rr,
+                                         L.aW, L.aS, L.hb, L.kb, L.rho, nullptr);
+        k_restrict<<<nblk((long)C.n * C.n), 256, 0, c->st>>>(nl, L.pitch, L.rho, L.hb, L.kb, C.n, C.pitch,
+                                                              C.hb, C.kb, C.b);
+        c->launches += 2;
+    }
+    vcycle(c, l + 1, C.b);
+    {
+        ProfScope ps(c, 5, 8.0 * nn + 2.0 * nn + 8.0 * nn + 8.0 * nn + 8.0 * nn);
+        k_prolong_prep<<<gb, 256, 0, c->st>>>(nl, L.pitch, L.cpitch, L.e, C.e, C.pitch, b, L.aW, L.aS, L.cd, L.q);
+        c->launches++;
+    }
+    mg_sweep(c, l, L.q, false, L.e);                          // post-smoothing
+}
+
+// M_CC^{-1} b_C: stationary V-cycle iteration until ||S_0 rho|| <= red ||S_0 b|| (P:1283-1287,
+// reading R6), z = 0 start, cap.  b0sq = ||S_0 b||^2.  Result in c->Zc.  Returns cycles.
+static int corner_solve(Ctx *c, const double *bc, double b0sq, int *cap_hit, cudaError_t *err)
+{
+    Level &L0 = c->lev[0];
+    const int n = L0.n;
+    const int gb = nblk((long)n * n);
+    *cap_hit = 0;
+    *err = cudaMemsetAsync(c->Zc, 0, sizeof(double) * L0.elems, c->st);
+    const double b0 = std::sqrt(b0sq);
+    double res = b0;
+    const double *rho = bc;
+    int cycles = 0;
+    const int fixed = c->opt.mg_fixed_cycles;
+    for (;;) {
+        if (fixed > 0) { if (cycles >= fixed) break; }
+        else {
+            if (res <= c->opt.mg_reduction * b0) break;
+            if (cycles >= c->opt.mg_max_cycles) { *cap_hit = 1; break; }
+        }
+        vcycle(c, 0, rho);
+        const bool need_norm = fixed <= 0;
+        {
+            ProfScope ps(c, 6, 8.0 * 7 * (double)n * n);
+            k_mg_resid<<<kRedBlocks, kRedThreads, 0, c->st>>>(n, L0.pitch, L0.cpitch, c->Zc, L0.e, bc, L0.aE,
+                L0.aN, L0.rr, L0.aW, L0.aS, L0.hb, L0.kb, L0.b, need_norm ? part_slot(c, 0) : nullptr);
+            c->launches++;
+        }
+        // k_mg_resid formed rho from z + e; commit z += e
+        k_mg_add<<<gb, 256, 0, c->st>>>(n, L0.pitch, c->Zc, L0.e);
+        c->launches++;
+        rho = L0.b;
+        cycles++;
+        if (need_norm) {
+            double s = 0;
+            cudaError_t e = fetch_sum(c, part_slot(c, 0), &s);
+            if (e != cudaSuccess) { *err = e; return cycles; }
+            res = std::sqrt(s);
+        }
+    }
+    return cycles;
+}
+
+// z = M^{-1} v (eq:2D blocks by block back-substitution I -> Y -> X -> C).
+// v, z: padded global grids.  In Jacobi mode the preconditioner input is D v (reading R11).
+static int apply_precond(Ctx *c, const double *v, double *z, int *cap_hit, cudaError_t *err)
+{
+    const int N = c->N, n = c->n;
+    // M_II
+    SweepArgs a{};
+    a.q = v; a.qp = c->P;
+    a.s = c->weighted ? nullptr : c->cd; a.sp = c->P;
+    a.ca = c->ca; a.cn = c->cn; a.cp = c->P;
+    a.z = z; a.zp = c->P;
+    a.ilo = n + 1; a.ihi = N - 1; a.jlo = n + 1; a.jhi = N - 1;
+    a.rows_out = 512; a.halo = 0; a.flags = c->flags;
+    launch_sweep(c, a, true, 1, 32.0 * (double)(n - 1) * (n - 1));
+    // M_YY and M_XX (one launch, both chains)
+    launch_lines(c, v, z);
+    // corner
+    Level &L0 = c->lev[0];
+    {
+        ProfScope ps(c, 9, 40.0 * (double)n * n);
+        k_corner_rhs<<<kRedBlocks, kRedThreads, 0, c->st>>>(N, c->P, L0.pitch, v, z, c->aE, c->aN, c->rr, c->aW,
+                                                            c->aS, L0.hb, L0.kb, c->weighted, c->Bc, part_slot(c, 1));
+        c->launches++;
+    }
+    double b0sq = 0;
+    if (c->opt.mg_fixed_cycles <= 0) {
+        cudaError_t e = fetch_sum(c, part_slot(c, 1), &b0sq);
+        if (e != cudaSuccess) { *err = e; return 0; }
+    }
+    int cyc = corner_solve(c, c->Bc, b0sq, cap_hit, err);
+    k_corner_out<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, c->Zc, c->P, z);
+    c->launches++;
+    return cyc;
+}
+
+}  // namespace spp
+
+// =========================================================================================== ABI
+extern "C" {
+
+const char *spp_version(void) { return "spp-b200 0.1 (sm_100a, fp64)"; }
+
+const char *spp_last_error(const spp_ctx *c)
+{
+    if (c) return ((const Ctx *)c)->err.c_str();
+    return g_err.c_str();
+}
+
+const char *spp_profile_name(int32_t k) { return (k >= 0 && k < SPP_PROF_CLASSES) ? kProfNames[k] : "?"; }
+
+void spp_default_options(int32_t dim, spp_options *o)
+{
+    if (!o) return;
+    memset(o, 0, sizeof(*o));
+    o->side = SPP_RIGHT_FLEXIBLE;
+    o->stop = SPP_STOP_REL_JACOBI;
+    o->tol = dim == 1 ? 1e-10 : 1e-8;
+    o->max_iters = 200;
+    o->restart = 0;
+    o->mg_reduction = 1e-3;
+    o->mg_max_cycles = 20;
+    o->mg_fixed_cycles = 0;
+    o->mg_coarsest = 4;
+    o->fixed_iters = 0;
+    o->mg_strict = 0;
+}
+
+spp_status spp_shishkin_mesh(int32_t n, double eps, double sigma, double beta, double *x)
+{
+    if (!x || n < 4 || (n % 2) != 0 || !(eps > 0.0) || eps > 1.0 || !(sigma > 0.0) || !(beta > 0.0))
+        FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_shishkin_mesh: bad arguments (n=%d eps=%g sigma=%g beta=%g)",
+             n, eps, sigma, beta);
+    // eq:tau 1D / eq:tau exponential
+    double tau = sigma * eps * std::log((double)n) / beta;
+    if (tau > 0.5) tau = 0.5;
+    const int h = n / 2;
+    const double w = tau / h, W = (1.0 - tau) / h;
+    for (int i = 0; i < h; ++i) x[i] = i * w;
+    x[h] = tau;
+    for (int i = h + 1; i < n; ++i) x[i] = tau + (i - h) * W;
+    x[n] = 1.0;
+    return SPP_OK;
+}
+
+static spp_status check_mesh(const double *x, int N, double *tau, Ctx *c)
+{
+    if (!x) FAIL(c, SPP_E_ARG, "mesh coordinates are NULL");
+    const int n = N / 2;
+    const double t = x[n];
+    if (x[0] != 0.0 || x[N] != 1.0 || !(t > 0.0) || !(t <= 0.5))
+        FAIL(c, SPP_E_MESH, "mesh: need x[0]=0, x[N]=1, 0 < x[N/2] <= 1/2");
+    const double h = t / n, H = (1.0 - t) / n;
+    for (int i = 0; i <= N; ++i) {
+        const double want = i <= n ? i * h : t + (i - n) * H;
+        if (std::fabs(x[i] - want) > 1e-12 * (std::fabs(want) + h))
+            FAIL(c, SPP_E_MESH, "mesh: node %d = %.17g is not on the piecewise-uniform Shishkin mesh (want %.17g)",
+                 i, x[i], want);
+    }
+    *tau = t;
+    return SPP_OK;
+}
+
+static spp_status alloc_all(Ctx *c)
+{
+    const int N = c->N;
+    if (c->dim == 1) return SPP_OK;   // 1D allocates in k_1d.cu's setup
+    const int n = c->n, m = c->m;
+    c->P = round_up(N + 1, 16);
+    c->G = (size_t)(N + 1) * c->P;
+    const size_t G = c->G;
+    CK(c, cudaMalloc(&c->coef_block, sizeof(double) * (6 * G + 2 * (N + 1))));
+    CK(c, cudaMemsetAsync(c->coef_block, 0, sizeof(double) * (6 * G + 2 * (N + 1)), c->st));
+    c->aE = c->coef_block; c->aN = c->aE + G; c->rr = c->aN + G;
+    c->ca = c->rr + G; c->cn = c->ca + G; c->cd = c->cn + G;
+    c->aW = c->cd + G; c->aS = c->aW + (N + 1);
+    const size_t per = (size_t)(n - 1) * n;
+    CK(c, cudaMalloc(&c->fac, sizeof(double) * (8 * per + 4 * (size_t)n)));
+    c->tX = c->fac + 8 * per; c->tY = c->tX + n; c->kapX = c->tY + n; c->kapY = c->kapX + n;
+    const size_t cb = std::max<size_t>(3 * (size_t)m * m, 2 * per);
+    CK(c, cudaMalloc(&c->cbuf, sizeof(double) * cb));
+    // Krylov work vectors
+    CK(c, cudaMalloc(&c->w, sizeof(double) * 4 * G));
+    CK(c, cudaMemsetAsync(c->w, 0, sizeof(double) * 4 * G, c->st));
+    c->F = c->w + G; c->U = c->F + G; c->T1 = c->U + G;
+    const int maxit = c->opt.max_iters;
+    CK(c, cudaMalloc(&c->part, sizeof(double) * (size_t)(maxit + 8) * kRedBlocks));
+    CK(c, cudaMalloc(&c->dscal, sizeof(double) * (size_t)(3 * maxit + 64)));
+    CK(c, cudaMallocHost(&c->hpin, sizeof(double) * (size_t)(4 * kRedBlocks + 3 * maxit + 64)));
+    CK(c, cudaMalloc(&c->flags, sizeof(int) * 256));
+    CK(c, cudaMemsetAsync(c->flags, 0, sizeof(int) * 256, c->st));
+    // corner MG levels (levels until <= mg_coarsest per axis)
+    int nl = n, L = 1;
+    const int coarsest = c->opt.mg_coarsest > 0 ? c->opt.mg_coarsest : 4;
+    while (nl > coarsest && L < kMaxLevels) { nl /= 2; L++; }
+    c->L = L;
+    size_t tot = 0;
+    for (int l = 0; l < L; ++l) {
+        Level &Lv = c->lev[l];
+        Lv.n = n >> l;
+        Lv.pitch = round_up(Lv.n + 2, 16);
+        Lv.elems = (size_t)(Lv.n + 2) * Lv.pitch;
+        tot += 4 * Lv.elems + 4 * (size_t)(Lv.n + 2) + (l > 0 ? 6 * Lv.elems : 0);
+    }
+    tot += 2 * c->lev[0].elems;   // Zc, Bc
+    CK(c, cudaMalloc(&c->mg_block, sizeof(double) * tot));
+    CK(c, cudaMemsetAsync(c->mg_block, 0, sizeof(double) * tot, c->st));
+    double *p = c->mg_block;
+    for (int l = 0; l < L; ++l) {
+        Level &Lv = c->lev[l];
+        Lv.b = p; p += Lv.elems; Lv.e = p; p += Lv.elems; Lv.q = p; p += Lv.elems; Lv.rho = p; p += Lv.elems;
+        Lv.aW = p; p += Lv.n + 2; Lv.aS = p; p += Lv.n + 2; Lv.hb = p; p += Lv.n + 2; Lv.kb = p; p += Lv.n + 2;
+        if (l > 0) {
+            Lv.own = p;
+            double *aE = p; p += Lv.elems; double *aN = p; p += Lv.elems; double *rr = p; p += Lv.elems;
+            double *ca = p; p += Lv.elems; double *cn = p; p += Lv.elems; double *cd = p; p += Lv.elems;
+            Lv.aE = aE; Lv.aN = aN; Lv.rr = rr; Lv.ca = ca; Lv.cn = cn; Lv.cd = cd;
+            Lv.cpitch = Lv.pitch;
+        } else {
+            Lv.aE = c->aE; Lv.aN = c->aN; Lv.rr = c->rr; Lv.ca = c->ca; Lv.cn = c->cn; Lv.cd = c->cd;
+            Lv.cpitch = c->P;
+        }
+    }
+    c->Zc = p; p += c->lev[0].elems;
+    c->Bc = p; p += c->lev[0].elems;
+    return SPP_OK;
+}
+
+static cudaError_t ensure_vectors(Ctx *c, int k)
+{
+    // V[0..k], Z[0..k-1]
+    while ((int)c->V.size() <= k) {
+        double *p = nullptr;
+        cudaError_t e = cudaMalloc(&p, sizeof(double) * c->G);
+        if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(p, 0, sizeof(double) * c->G, c->st);
+        if (e != cudaSuccess) return e;
+        c->V.push_back(p);
+    }
+    while ((int)c->Z.size() < k) {
+        double *p = nullptr;
+        cudaError_t e = cudaMalloc(&p, sizeof(double) * c->G);
+        if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(p, 0, sizeof(double) * c->G, c->st);
+        if (e != cudaSuccess) return e;
+        c->Z.push_back(p);
+    }
+    return cudaSuccess;
+}
+
+static spp_status do_setup_2d(Ctx *c, const double *c1, const double *c2, const double *r, spp_mem mem)
+{
+    const int N = c->N, m = c->m;
+    const size_t mm = (size_t)m * m;
+    const double *d1 = c1, *d2 = c2, *d3 = r;
+    cudaEvent_t e0, e1;
+    CK(c, cudaEventCreate(&e0));
+    CK(c, cudaEventCreate(&e1));
+    CK(c, cudaEventRecord(e0, c->st));
+    if (mem == SPP_HOST) {
+        CK(c, cudaMemcpyAsync(c->cbuf, c1, sizeof(double) * mm, cudaMemcpyHostToDevice, c->st));
+        CK(c, cudaMemcpyAsync(c->cbuf + mm, c2, sizeof(double) * mm, cudaMemcpyHostToDevice, c->st));
+        CK(c, cudaMemcpyAsync(c->cbuf + 2 * mm, r, sizeof(double) * mm, cudaMemcpyHostToDevice, c->st));
+        d1 = c->cbuf; d2 = c->cbuf + mm; d3 = c->cbuf + 2 * mm;
+    }
+    int *bad = c->flags + 200;
+    CK(c, cudaMemsetAsync(bad, 0, sizeof(int), c->st));
+    k_validate<<<nblk((long)mm), 256, 0, c->st>>>((long)mm, d1, d2, d3, bad);
+    k_coef_1d<<<nblk(N + 1), 256, 0, c->st>>>(N, c->eps, c->hx, c->Hx, c->hy, c->Hy, c->aW, c->aS);
+    k_coef_2d<<<nblk((long)mm), 256, 0, c->st>>>(N, c->P, c->eps, c->hx, c->Hx, c->hy, c->Hy, d1, d2, d3, c->aW,
+                                                c->aS, c->aE, c->aN, c->rr, c->ca, c->cn, c->cd);
+    Level &L0 = c->lev[0];
+    k_level0_1d<<<1, 256, 0, c->st>>>(N, c->hx, c->Hx, c->hy, c->Hy, c->aW, c->aS, L0.aW, L0.aS, L0.hb, L0.kb);
+    c->launches += 4;
+    for (int l = 1; l < c->L; ++l) {
+        Level &Lv = c->lev[l];
+        k_coef_level<<<nblk((long)Lv.n * Lv.n), 256, 0, c->st>>>(N, Lv.n, 1 << l, Lv.pitch, c->eps, c->hx, c->Hx,
+            c->hy, c->Hy, d1, d2, d3, Lv.aW, Lv.aS, Lv.hb, Lv.kb, (double *)Lv.aE, (double *)Lv.aN,
+            (double *)Lv.rr, (double *)Lv.ca, (double *)Lv.cn, (double *)Lv.cd);
+        c->launches++;
+    }
+    int hbad = 0;
+    CK(c, cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CK(c, cudaStreamSynchronize(c->st));
+    if (hbad) FAIL(c, SPP_E_COEF, "coefficients violate c1 > 0, c2 > 0, r >= 0 or are not finite (P:208-212, P:907)");
+    CK(c, setup_lines(c));
+    CK(c, cudaEventRecord(e1, c->st));
+    CK(c, cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&c->setup_ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CK(c, cudaGetLastError());
+    return SPP_OK;
+}
+
+spp_status spp_setup(spp_ctx *cx, const double *c1, const double *c2, const double *r, spp_mem mem)
+{
+    Ctx *c = (Ctx *)cx;
+    if (!c) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_setup: NULL context");
+    if (!c1 || !r || (c->dim == 2 && !c2)) FAIL(c, SPP_E_ARG, "spp_setup: NULL coefficient array");
+    if (c->dim == 1) return (spp_status)setup_1d(c, c1, r, mem);
+    return do_setup_2d(c, c1, c2, r, mem);
+}
+
+spp_status spp_create(const spp_problem *p, const spp_options *o, void *stream, spp_ctx **out)
+{
+    if (!p || !out) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_create: NULL argument");
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        FAIL((Ctx *)nullptr, SPP_E_CUDA, "spp_create: no CUDA device (this library has no CPU path)");
+    const int N = p->n;
+    if (p->dim != 1 && p->dim != 2) FAIL((Ctx *)nullptr, SPP_E_ARG, "dim must be 1 or 2");
+    if (N < 4 || (N % 2)) FAIL((Ctx *)nullptr, SPP_E_ARG, "N must be even and >= 4 (got %d)", N);
+    if (p->dim == 2 && (N < 8 || ((N / 2) & (N / 2 - 1))))
+        FAIL((Ctx *)nullptr, SPP_E_ARG, "2D needs N >= 8 with N/2 a power of two (got %d)", N);
+    if (!(p->eps > 0.0) || p->eps > 1.0) FAIL((Ctx *)nullptr, SPP_E_ARG, "eps must be in (0,1]");
+    Ctx *c = new (std::nothrow) Ctx();
+    if (!c) FAIL((Ctx *)nullptr, SPP_E_NOMEM, "host allocation failed");
+    c->dim = p->dim; c->N = N; c->n = N / 2; c->m = N - 1; c->eps = p->eps;
+    c->st = (cudaStream_t)stream;
+    if (o) c->opt = *o; else spp_default_options(p->dim, &c->opt);
+    if (c->opt.max_iters < 1) c->opt.max_iters = 1;
+    if (c->opt.mg_max_cycles < 1) c->opt.mg_max_cycles = 20;
+    if (!(c->opt.mg_reduction > 0.0)) c->opt.mg_reduction = 1e-3;
+    c->weighted = c->opt.stop == SPP_STOP_REL_JACOBI ? 1 : 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev);
+    spp_status s;
+    double tx = 0, ty = 0;
+    if ((s = check_mesh(p->x, N, &tx, c)) != SPP_OK) { g_err = c->err; delete c; return s; }
+    if (p->dim == 2 && (s = check_mesh(p->y, N, &ty, c)) != SPP_OK) { g_err = c->err; delete c; return s; }
+    c->tx = tx; c->ty = ty;
+    c->hx = tx / c->n; c->Hx = (1.0 - tx) / c->n;
+    c->hy = ty / c->n; c->Hy = (1.0 - ty) / c->n;
+    c->xh.assign(p->x, p->x + N + 1);
+    if ((s = alloc_all(c)) != SPP_OK) { g_err = c->err; spp_destroy((spp_ctx *)c); return s; }
+    if ((s = spp_setup((spp_ctx *)c, p->c1, p->c2, p->r, p->mem)) != SPP_OK) {
+        g_err = c->err;
+        spp_destroy((spp_ctx *)c);
+        return s;
+    }
+    *out = (spp_ctx *)c;
+    return SPP_OK;
+}
+
+void spp_destroy(spp_ctx *cx)
+{
+    Ctx *c = (Ctx *)cx;
+    if (!c) return;
+    if (c->st) cudaStreamSynchronize(c->st); else cudaDeviceSynchronize();
+    for (double *p : c->V) cudaFree(p);
+    for (double *p : c->Z) cudaFree(p);
+    cudaFree(c->coef_block); cudaFree(c->fac); cudaFree(c->cbuf); cudaFree(c->w);
+    cudaFree(c->part); cudaFree(c->dscal); cudaFree(c->flags); cudaFree(c->mg_block);
+    cudaFree(c->d_chunks); cudaFree(c->d1);
+    if (c->hpin) cudaFreeHost(c->hpin);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    delete c;
+}
+
+int64_t spp_kernel_launches(const spp_ctx *cx) { return cx ? ((const Ctx *)cx)->launches : 0; }
+
+int32_t spp_mg_levels(const spp_ctx *cx) { return cx ? ((const Ctx *)cx)->L : 0; }
+int32_t spp_mg_level_n(const spp_ctx *cx, int32_t l)
+{
+    const Ctx *c = (const Ctx *)cx;
+    return (c && l >= 0 && l < c->L) ? c->lev[l].n : 0;
+}
+
+spp_status spp_profile_enable(spp_ctx *cx, int32_t en)
+{
+    Ctx *c = (Ctx *)cx;
+    if (!c) return SPP_E_ARG;
+    c->prof_on = en ? (en == 1 ? 0x3ff : en) : 0;
+    return SPP_OK;
+}
+spp_status spp_profile_reset(spp_ctx *cx)
+{
+    Ctx *c = (Ctx *)cx;
+    if (!c) return SPP_E_ARG;
+    for (auto &r : c->prof) r = ProfRec();
+    return SPP_OK;
+}
+spp_status spp_profile_get(const spp_ctx *cx, int32_t k, int64_t *launches, double *ms, double *bytes)
+{
+    const Ctx *c = (const Ctx *)cx;
+    if (!c || k < 0 || k >= SPP_PROF_CLASSES) return SPP_E_ARG;
+    if (launches) *launches = c->prof[k].launches;
+    if (ms) *ms = c->prof[k].ms;
+    if (bytes) *bytes = c->prof[k].bytes;
+    return SPP_OK;
+}
+
+// ------------------------------------------------------------------------------------------ solve (2D)
+static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, double *hist, int hcap,
+                           spp_stats *st)
+{
+    const int m = c->m, maxit = c->opt.max_iters;
+    const long G = (long)c->G;
+    const size_t mm = (size_t)m * m;
+    const int64_t launches0 = c->launches;
+    cudaEvent_t e0, e1;
+    CK(c, cudaEventCreate(&e0));
+    CK(c, cudaEventCreate(&e1));
+    CK(c, cudaEventRecord(e0, c->st));
+    // f -> padded F
+    const double *fd = f;
+    if (mem == SPP_HOST) {
+        CK(c, cudaMemcpyAsync(c->cbuf, f, sizeof(double) * mm, cudaMemcpyHostToDevice, c->st));
+        fd = c->cbuf;
+    }
+    k_pack<<<nblk((long)mm), 256, 0, c->st>>>(m, c->P, fd, c->F);
+    c->launches++;
+    CK(c, ensure_vectors(c, 1));
+    const int weighted = c->weighted;
+    const int stop = c->opt.stop;
+    // v0 = W f / beta
+    {
+        ProfScope ps(c, 7, 48.0 * mm);
+        k_rhs<<<kRedBlocks, kRedThreads, 0, c->st>>>(m, c->P, c->F, c->aE, c->aN, c->rr, c->aW, c->aS, weighted,
+                                                     c->V[0], part_slot(c, 0));
+        c->launches++;
+    }
+    double bsq = 0;
+    CK(c, fetch_sum(c, part_slot(c, 0), &bsq));
+    const double beta = std::sqrt(bsq);
+    std::vector<double> H((size_t)(maxit + 1) * (maxit + 1), 0.0), cs(maxit + 1), sn(maxit + 1),
+        g(maxit + 2, 0.0), yv(maxit + 1);
+    if (hist && hcap > 0) hist[0] = beta;
+    int iters = 0, converged = 0, mg_tot = 0, mg_min = 1 << 30, mg_max = 0, caps = 0;
+    double resf = beta;
+    const double target = (stop == SPP_STOP_ABS_L2) ? c->opt.tol : c->opt.tol * beta;
+    CK(c, cudaMemsetAsync(c->U, 0, sizeof(double) * G, c->st));
+    if (beta == 0.0) converged = 1;
+    else {
+        k_scale<<<nblk(G / 2), 256, 0, c->st>>>(G, c->V[0], 1.0 / beta);
+        c->launches++;
+        g[0] = beta;
+        for (int k = 0; k < maxit; ++k) {
+            CK(c, ensure_vectors(c, k + 1));
+            int cap = 0;
+            cudaError_t err = cudaSuccess;
+            const int cyc = apply_precond(c, c->V[k], c->Z[k], &cap, &err);
+            CK(c, err);
+            if (cap && c->opt.mg_strict) FAIL(c, SPP_E_MG_CAP, "corner multigrid hit the cycle cap (%d)", c->opt.mg_max_cycles);
+            mg_tot += cyc; mg_min = std::min(mg_min, cyc); mg_max = std::max(mg_max, cyc); caps += cap;
+            // w = W A z_k, with <w, v_0>
+            {
+                ProfScope ps(c, 0, 48.0 * mm);
+                k_spmv<<<kRedBlocks, kRedThreads, 0, c->st>>>(m, c->P, c->Z[k], c->aE, c->aN, c->rr, c->aW, c->aS,
+                                                              weighted, c->w, c->V[0], part_slot(c, 0));
+                c->launches++;
+            }
+            // modified Gram-Schmidt: h_{j,k} for j = 0..k, then ||w||
+            for (int j = 1; j <= k; ++j) {
+                ProfScope ps(c, 7, 32.0 * G);
+                k_mgs<<<kRedBlocks, kRedThreads, 0, c->st>>>(G, c->w, c->V[j - 1], part_slot(c, j - 1),
+                                                             c->dscal + (j - 1), c->V[j], part_slot(c, j));
+                c->launches++;
+            }
+            {
+                ProfScope ps(c, 7, 24.0 * G + 16.0 * G);
+                k_mgs<<<kRedBlocks, kRedThreads, 0, c->st>>>(G, c->w, c->V[k], part_slot(c, k), c->dscal + k,
+                                                             c->w, part_slot(c, k + 1));
+                k_normalize<<<kRedBlocks, kRedThreads, 0, c->st>>>(G, c->w, part_slot(c, k + 1), c->dscal + k + 1,
+                                                                   c->V[k + 1]);
+                c->launches += 2;
+            }
+            CK(c, cudaMemcpyAsync(c->hpin, c->dscal, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, c->st));
+            CK(c, cudaStreamSynchronize(c->st));
+            double *h = &H[(size_t)k * (maxit + 1)];
+            for (int j = 0; j <= k + 1; ++j) h[j] = c->hpin[j];
+            // Givens (Saad 2003)
+            for (int i = 0; i < k; ++i) {
+                const double t = cs[i] * h[i] + sn[i] * h[i + 1];
+                h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+                h[i] = t;
+            }
+            const double den = std::hypot(h[k], h[k + 1]);
+            if (den == 0.0) { cs[k] = 1.0; sn[k] = 0.0; }
+            else { cs[k] = h[k] / den; sn[k] = h[k + 1] / den; }
+            const bool brk = !(h[k + 1] > 0.0);
+            h[k] = den; h[k + 1] = 0.0;
+            g[k + 1] = -sn[k] * g[k];
+            g[k] = cs[k] * g[k];
+            const double res = std::fabs(g[k + 1]);
+            iters = k + 1;
+            resf = res;
+            if (hist && k + 1 < hcap) hist[k + 1] = res;
+            if (brk) { converged = 1; break; }
+            if (c->opt.fixed_iters > 0) {
+                if (k + 1 >= c->opt.fixed_iters) { converged = res <= target; break; }
+            } else if (res <= target) { converged = 1; break; }
+        }
+        // y = R^{-1} g;  x = sum_j y_j z_j
+        for (int i = iters - 1; i >= 0; --i) {
+            double t = g[i];
+            for (int j = i + 1; j < iters; ++j) t -= H[(size_t)j * (maxit + 1) + i] * yv[j];
+            yv[i] = t / H[(size_t)i * (maxit + 1) + i];
+        }
+        // device copies of the Z pointers and y (pinned staging, pre-allocated device slots)
+        const double **hz = (const double **)(c->hpin + 4 * kRedBlocks);
+        double *hy = c->hpin + 4 * kRedBlocks + maxit + 8;
+        for (int j = 0; j < iters; ++j) { hz[j] = c->Z[j]; hy[j] = yv[j]; }
+        const double **dptr = (const double **)(c->dscal + maxit + 8);
+        double *dy = c->dscal + 2 * maxit + 16;
+        CK(c, cudaMemcpyAsync(dptr, hz, sizeof(double *) * iters, cudaMemcpyHostToDevice, c->st));
+        CK(c, cudaMemcpyAsync(dy, hy, sizeof(double) * iters, cudaMemcpyHostToDevice, c->st));
+        {
+            ProfScope ps(c, 7, 8.0 * G * (iters + 1));
+            k_update_x<<<nblk(G / 2), 256, 0, c->st>>>(G, iters, dptr, dy, c->U);
+            c->launches++;
+        }
+    }
+    CK(c, cudaEventRecord(e1, c->st));
+    // output
+    if (u) {
+        if (mem == SPP_HOST) {
+            k_unpack<<<nblk((long)mm), 256, 0, c->st>>>(m, c->P, c->U, c->cbuf);
+            CK(c, cudaMemcpyAsync(u, c->cbuf, sizeof(double) * mm, cudaMemcpyDeviceToHost, c->st));
+        } else {
+            k_unpack<<<nblk((long)mm), 256, 0, c->st>>>(m, c->P, c->U, u);
+        }
+        c->launches++;
+    }
+    CK(c, cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    // statistics: true residuals (after the timed region)
+    if (st) {
+        memset(st, 0, sizeof(*st));
+        k_spmv<<<kRedBlocks, kRedThreads, 0, c->st>>>(m, c->P, c->U, c->aE, c->aN, c->rr, c->aW, c->aS, 0, c->w,
+                                                      nullptr, nullptr);
+        k_resid_stats<<<kRedBlocks, kRedThreads, 0, c->st>>>(m, c->P, c->F, c->w, c->aE, c->aN, c->rr, c->aW, c->aS,
+                                                             c->part);
+        CK(c, cudaMemcpyAsync(c->hpin, c->part, sizeof(double) * 4 * kRedBlocks, cudaMemcpyDeviceToHost, c->st));
+        CK(c, cudaStreamSynchronize(c->st));
+        const double s0 = host_sum(c->hpin, kRedBlocks), s1 = host_sum(c->hpin + kRedBlocks, kRedBlocks);
+        const double s2 = host_sum(c->hpin + 2 * kRedBlocks, kRedBlocks), s3 = host_sum(c->hpin + 3 * kRedBlocks, kRedBlocks);
+        st->true_res_l2_rel = s2 > 0 ? std::sqrt(s0 / s2) : 0.0;
+        st->true_res_jacobi_rel = s3 > 0 ? std::sqrt(s1 / s3) : 0.0;
+        st->iters = iters; st->converged = converged;
+        st->mg_cycles_total = mg_tot; st->mg_cycles_min = iters ? mg_min : 0; st->mg_cycles_max = mg_max;
+        st->mg_cap_hits = caps; st->applies = iters;
+        st->kernel_launches = (int32_t)(c->launches - launches0);
+        st->res0 = beta; st->res_final = resf;
+        st->setup_s = c->setup_ms * 1e-3; st->solve_s = ms * 1e-3;
+    }
+    prof_collect(c);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CK(c, cudaGetLastError());
+    return converged ? SPP_OK : SPP_NOT_CONVERGED;
+}
+
+spp_status spp_solve(spp_ctx *cx, const double *f, double *u, spp_mem mem, double *hist, int32_t hcap,
+                     spp_stats *st)
+{
+    Ctx *c = (Ctx *)cx;
+    if (!c) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_solve: NULL context");
+    if (!f) FAIL(c, SPP_E_ARG, "spp_solve: NULL rhs");
+    if (c->dim == 1) return (spp_status)solve_1d_abi(c, f, u, mem, hist, hcap, st);
+    return solve_2d(c, f, u, mem, hist, hcap, st);
+}
+
+// ------------------------------------------------------------------------------------------ test hooks
+spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in, double *out, int32_t *cyc)
+{
+    Ctx *c = (Ctx *)cx;
+    if (!c || !in || !out) FAIL(c, SPP_E_ARG, "spp_apply_stage: NULL argument");
+    if (c->dim != 2) FAIL(c, SPP_E_STATE, "spp_apply_stage: 2D contexts only");
+    const int m = c->m, n = c->n;
+    const long mm = (long)m * m;
+    const long G = (long)c->G;
+    CK(c, ensure_vectors(c, 1));
+    double *A = c->V[0], *B = c->Z[0];
+    auto pk = [&](const double *src, double *dst) { k_pack<<<nblk(mm), 256, 0, c->st>>>(m, c->P, src, dst); };
+    auto up = [&](const double *src, double *dst) { k_unpack<<<nblk(mm), 256, 0, c->st>>>(m, c->P, src, dst); };
+    if (s == SPP_STAGE_MATVEC) {
+        pk(in, A);
+        k_spmv<<<kRedBlocks, kRedThreads, 0, c->st>>>(m, c->P, A, c->aE, c->aN, c->rr, c->aW, c->aS, 0, B, nullptr, nullptr);
+        up(B, out);
+    } else if (s == SPP_STAGE_PRECOND) {
+        pk(in, A);
+        int cap = 0; cudaError_t err = cudaSuccess;
+        // the hook applies the plain M^{-1} (unweighted input) regardless of the stop mode
+        const int w = c->weighted;
+        c->weighted = 0;
+        if (w) { c->weighted = 0; CK(c, setup_lines(c)); }
+        int k = apply_precond(c, A, B, &cap, &err);
+        c->weighted = w;
+        if (w) CK(c, setup_lines(c));
+        CK(c, err);
+        if (cyc) *cyc = k;
+        up(B, out);
+    } else if (s == SPP_STAGE_MII || s == SPP_STAGE_MYY || s == SPP_STAGE_MXX) {
+        pk(in, A);
+        // out holds the current z (compact): load it into B
+        pk(out, B);
+        const int w = c->weighted;
+        if (w) { c->weighted = 0; CK(c, setup_lines(c)); }
+        if (s == SPP_STAGE_MII) {
+            SweepArgs a{};
+            a.q = A; a.qp = c->P; a.s = c->cd; a.sp = c->P; a.ca = c->ca; a.cn = c->cn; a.cp = c->P;
+            a.z = B; a.zp = c->P; a.ilo = n + 1; a.ihi = m; a.jlo = n + 1; a.jhi = m;
+            a.rows_out = 512; a.flags = c->flags;
+            launch_sweep(c, a, true, 1, 0);
+        } else {
+            // run only the requested chain: temporarily restrict chunks
+            std::vector<LineChunk> keep = c->chunks, sel;
+            for (auto &ck : keep) if (ck.chain == (s == SPP_STAGE_MXX ? 0 : 1)) sel.push_back(ck);
+            CK(c, cudaMemcpyAsync(c->d_chunks, sel.data(), sizeof(LineChunk) * sel.size(), cudaMemcpyHostToDevice, c->st));
+            c->chunks = sel;
+            launch_lines(c, A, B);
+            c->chunks = keep;
+            CK(c, cudaMemcpyAsync(c->d_chunks, keep.data(), sizeof(LineChunk) * keep.size(), cudaMemcpyHostToDevice, c->st));
+        }
+        c->weighted = w;
+        if (w) CK(c, setup_lines(c));
+        up(B, out);
+    } else if (s == SPP_STAGE_CORNER_RHS) {
+        pk(in, A);
+        pk(in + mm, B);
+        Level &L0 = c->lev[0];
+        k_corner_rhs<<<kRedBlocks, kRedThreads, 0, c->st>>>(c->N, c->P, L0.pitch, A, B, c->aE, c->aN, c->rr, c->aW,
+                                                            c->aS, L0.hb, L0.kb, 0, c->Bc, part_slot(c, 0));
+        k_unpack_level<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, c->Bc, out);
+    } else if (s == SPP_STAGE_CORNER_SOLVE) {
+        Level &L0 = c->lev[0];
+        CK(c, cudaMemsetAsync(c->Bc, 0, sizeof(double) * L0.elems, c->st));
+        k_pack_level<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, in, c->Bc);
+        // ||S_0 b||^2 via the residual kernel with z = 0
+        CK(c, cudaMemsetAsync(c->Zc, 0, sizeof(double) * L0.elems, c->st));
+        k_mg_resid<<<kRedBlocks, kRedThreads, 0, c->st>>>(n, L0.pitch, L0.cpitch, c->Zc, nullptr, c->Bc, L0.aE, L0.aN,
+                                                          L0.rr, L0.aW, L0.aS, L0.hb, L0.kb, L0.rho, part_slot(c, 1));
+        double b0sq = 0;
+        CK(c, fetch_sum(c, part_slot(c, 1), &b0sq));
+        int cap = 0; cudaError_t err = cudaSuccess;
+        int k = corner_solve(c, c->Bc, b0sq, &cap, &err);
+        CK(c, err);
+        if (cyc) *cyc = k;
+        k_unpack_level<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, c->Zc, out);
+    } else {
+        if (l < 0 || l >= c->L) FAIL(c, SPP_E_ARG, "level %d out of range", l);
+        Level &Lv = c->lev[l];
+        const int nl = Lv.n;
+        const long nn = (long)nl * nl;
+        double *b = Lv.b, *e = Lv.e;
+        if (s == SPP_STAGE_GS_SWEEP) {
+            k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in, b);
+            k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, out, e);
+            k_gs_prep<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, Lv.cpitch, e, b, Lv.aW, Lv.aS, Lv.cd, Lv.q);
+            mg_sweep(c, l, Lv.q, false, e);
+            k_unpack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, e, out);
+        } else if (s == SPP_STAGE_VCYCLE) {
+            double *tmp = c->T1;   // level-l rhs must not alias lev[l].b (used by coarse levels)
+            CK(c, cudaMemsetAsync(tmp, 0, sizeof(double) * Lv.elems, c->st));
+            k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in, tmp);
+            vcycle(c, l, tmp);
+            k_unpack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, e, out);
+        } else if (s == SPP_STAGE_RESTRICT) {
+            if (l + 1 >= c->L) FAIL(c, SPP_E_ARG, "no coarser level");
+            Level &C = c->lev[l + 1];
+            k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in, Lv.rho);
+            k_restrict<<<nblk((long)C.n * C.n), 256, 0, c->st>>>(nl, Lv.pitch, Lv.rho, Lv.hb, Lv.kb, C.n, C.pitch,
+                                                                  C.hb, C.kb, C.b);
+            k_unpack_level<<<nblk((long)C.n * C.n), 256, 0, c->st>>>(C.n, C.pitch, C.b, out);
+        } else if (s == SPP_STAGE_PROLONG_ADD) {
+            if (l + 1 >= c->L) FAIL(c, SPP_E_ARG, "no coarser level");
+            Level &C = c->lev[l + 1];
+            k_pack_level<<<nblk((long)C.n * C.n), 256, 0, c->st>>>(C.n, C.pitch, in, C.e);
+            k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, out, e);
+            k_prolong_add<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, e, C.e, C.pitch);
+            k_unpack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, e, out);
+        } else if (s == SPP_STAGE_LEVEL_RESIDUAL) {
+            k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in, b);
+            k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in + nn, e);
+            k_mg_resid<<<kRedBlocks, kRedThreads, 0, c->st>>>(nl, Lv.pitch, Lv.cpitch, e, nullptr, b, Lv.aE, Lv.aN,
+                                                              Lv.rr, Lv.aW, Lv.aS, Lv.hb, Lv.kb, Lv.rho, nullptr);
+            k_unpack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, Lv.rho, out);
+        } else {
+            FAIL(c, SPP_E_ARG, "unknown stage %d", (int)s);
+        }
+    }
+    CK(c, cudaStreamSynchronize(c->st));
+    CK(c, cudaGetLastError());
+    (void)G;
+    return SPP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,491 @@
+// k_core.cu -- setup, stencil, Krylov-vector and multigrid-transfer kernels (sm_100a, fp64).
+//
+// All grid functions use the padded layout of spp_internal.cuh.  Reductions are
+// deterministic: producers run on a fixed grid of kRedBlocks blocks and write one partial per
+// block; consumers re-sum the partials in a fixed order (every block redundantly), so no
+// atomics and bit-identical results run to run.
+#include "kernels.cuh"
+
+namespace spp {
+
+// ===================================================================================== setup
+// 1D coefficients of the 5-point stencil in difference form (R12):
+// aW_i = eps/(hbar_i h_i), aS_j = eps/(kbar_j k_j).  Widths from the piecewise-uniform formula.
+__global__ void k_coef_1d(int N, double eps, double hx, double Hx, double hy, double Hy,
+                          double *aW, double *aS)
+{
+    const int n = N / 2;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= N; i += gridDim.x * blockDim.x) {
+        if (i < 1 || i > N - 1) { aW[i] = 0.0; aS[i] = 0.0; continue; }
+        const double h = i <= n ? hx : Hx, h1 = (i + 1) <= n ? hx : Hx, hb = 0.5 * (h + h1);
+        const double k = i <= n ? hy : Hy, k1 = (i + 1) <= n ? hy : Hy, kb = 0.5 * (k + k1);
+        aW[i] = eps / (hb * h);
+        aS[i] = eps / (kb * k);
+    }
+}
+
+// aE, aN, r, and the sweep coefficients aE/D, aN/D, 1/D on the padded global grid.
+// c1, c2, r are compact ((N-1)^2, x fastest).
+__global__ void k_coef_2d(int N, long P, double eps, double hx, double Hx, double hy, double Hy,
+                          const double *c1, const double *c2, const double *r, const double *aW,
+                          const double *aS, double *aE, double *aN, double *rr, double *ca,
+                          double *cn, double *cd)
+{
+    const int n = N / 2, m = N - 1;
+    const long tot = (long)m * m;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
+        const double h = i <= n ? hx : Hx, h1 = (i + 1) <= n ? hx : Hx, hb = 0.5 * (h + h1);
+        const double k = j <= n ? hy : Hy, k1 = (j + 1) <= n ? hy : Hy, kb = 0.5 * (k + k1);
+        const double e = eps / (hb * h1) + c1[p] / h1;
+        const double no = eps / (kb * k1) + c2[p] / k1;
+        const double rv = r[p];
+        const double D = ((aW[i] + e) + (aS[j] + no)) + rv;
+        const long g = (long)j * P + i;
+        aE[g] = e; aN[g] = no; rr[g] = rv;
+        ca[g] = e / D; cn[g] = no / D; cd[g] = 1.0 / D;
+        (void)h; (void)k;
+    }
+}
+
+// Corner multigrid level l >= 1 (R8): re-discretisation on the 1D mesh
+// that keeps every 2^l-th corner node plus x_0 and x_{n+1}; coefficients sampled at the
+// coarse nodes.  Widths: 2^l tau/(N/2) inside, (1-tau)/(N/2) for the last interval.
+__global__ void k_coef_level(int N, int nl, int step, long Pl, double eps, double hx, double Hx,
+                             double hy, double Hy, const double *c1, const double *c2,
+                             const double *r, double *aW, double *aS, double *hb, double *kb,
+                             double *aE, double *aN, double *rr, double *ca, double *cn, double *cd)
+{
+    const int m = N - 1;
+    const long tot = (long)nl * nl;
+    const double h = hx * step, k = hy * step;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int lq = (int)(p / nl) + 1, q = (int)(p % nl) + 1;
+        const double h1 = (q < nl) ? h : Hx, hbar = 0.5 * (h + h1);
+        const double k1 = (lq < nl) ? k : Hy, kbar = 0.5 * (k + k1);
+        const double aw = eps / (hbar * h), as = eps / (kbar * k);
+        if (lq == 1) { aW[q] = aw; hb[q] = hbar; }
+        if (q == 1) { aS[lq] = as; kb[lq] = kbar; }
+        const long g = (long)(lq * step - 1) * m + (q * step - 1);
+        const double e = eps / (hbar * h1) + c1[g] / h1;
+        const double no = eps / (kbar * k1) + c2[g] / k1;
+        const double rv = r[g];
+        const double D = ((aw + e) + (as + no)) + rv;
+        const long o = (long)lq * Pl + q;
+        aE[o] = e; aN[o] = no; rr[o] = rv;
+        ca[o] = e / D; cn[o] = no / D; cd[o] = 1.0 / D;
+    }
+}
+
+// Level 0 1D arrays (the level-0 operator is A_CC itself; its coefficients are the global
+// ones): copies of aW, aS on 1..n and hbar, kbar for the FE scaling S_0.
+__global__ void k_level0_1d(int N, double hx, double Hx, double hy, double Hy, const double *aW,
+                            const double *aS, double *lW, double *lS, double *hb, double *kb)
+{
+    const int n = N / 2;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q <= n + 1; q += gridDim.x * blockDim.x) {
+        if (q < 1 || q > n) { lW[q] = 0.0; lS[q] = 0.0; hb[q] = 0.0; kb[q] = 0.0; continue; }
+        const double h1 = (q < n) ? hx : Hx, k1 = (q < n) ? hy : Hy;
+        lW[q] = aW[q]; lS[q] = aS[q];
+        hb[q] = 0.5 * (hx + h1); kb[q] = 0.5 * (hy + k1);
+    }
+}
+
+// validation: c1 > 0, c2 > 0, r >= 0, all finite
+__global__ void k_validate(long tot, const double *c1, const double *c2, const double *r, int *bad)
+{
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const double a = c1[p], b = c2 ? c2[p] : 1.0, c = r[p];
+        if (!(a > 0.0) || !(b > 0.0) || !(c >= 0.0) || !isfinite(a) || !isfinite(b) || !isfinite(c))
+            atomicOr(bad, 1);
+    }
+}
+
+// ===================================================================================== layout
+__global__ void k_pack(int m, long P, const double *src, double *dst)   // compact -> padded
+{
+    const long tot = (long)m * m;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
+        dst[(long)j * P + i] = src[p];
+    }
+}
+__global__ void k_unpack(int m, long P, const double *src, double *dst)  // padded -> compact
+{
+    const long tot = (long)m * m;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
+        dst[p] = src[(long)j * P + i];
+    }
+}
+
+// ===================================================================================== reductions
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
+
+// block-wide sum; result valid in thread 0
+__device__ __forceinline__ double block_sum(double v, double *sm)
+{
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) sm[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < nw ? sm[lane] : 0.0;
+        v = warp_sum(v);
+    }
+    return v;
+}
+
+// every block re-sums the kRedBlocks partials in the same order
+__device__ __forceinline__ double sum_partials(const double *part, double *sm)
+{
+    __shared__ double s_res;
+    if (threadIdx.x < 32) {
+        double v = 0.0;
+        for (int b = threadIdx.x; b < kRedBlocks; b += 32) v += part[b];
+        v = warp_sum(v);
+        if (threadIdx.x == 0) s_res = v;
+    }
+    __syncthreads();
+    (void)sm;
+    return s_res;
+}
+
+// ===================================================================================== stencil
+// w = A z (difference form; R12); weighted: w = (A z)/D.
+// Fused: partial of <w, v0> (first MGS dot) when v0 != nullptr.
+__global__ void __launch_bounds__(kRedThreads) k_spmv(int m, long P, const double *__restrict__ z,
+    const double *__restrict__ aE, const double *__restrict__ aN, const double *__restrict__ rr,
+    const double *__restrict__ aW, const double *__restrict__ aS, int weighted, double *w,
+    const double *__restrict__ v0, double *part)
+{
+    __shared__ double sm[32];
+    double acc = 0.0;
+    const long rows = m;
+    // one block-iteration = one row segment of 2*blockDim columns, double2 stores
+    const int segw = 2 * blockDim.x;
+    const long nseg = (P + segw - 1) / segw;
+    for (long it = blockIdx.x; it < rows * nseg; it += gridDim.x) {
+        const int j = (int)(it / nseg) + 1;
+        const int i0 = (int)(it % nseg) * segw + 2 * threadIdx.x;
+        const long g = (long)j * P + i0;
+        if (i0 >= P) continue;
+        double out[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int i = i0 + u;
+            double val = 0.0;
+            if (i >= 1 && i <= m) {
+                const long q = g + u;
+                const double c = z[q];
+                const double e = aE[q], no = aN[q], rv = rr[q], ww = aW[i], ss = aS[j];
+                val = ww * (c - z[q - 1]) + e * (c - z[q + 1]) + ss * (c - z[q - P]) + no * (c - z[q + P]) + rv * c;
+                if (weighted) val /= ((ww + e) + (ss + no)) + rv;
+            }
+            out[u] = val;
+        }
+        *reinterpret_cast<double2 *>(w + g) = make_double2(out[0], out[1]);
+        if (v0) {
+            const double2 vv = *reinterpret_cast<const double2 *>(v0 + g);
+            acc += out[0] * vv.x + out[1] * vv.y;
+        }
+    }
+    if (part) {
+        const double s = block_sum(acc, sm);
+        if (threadIdx.x == 0) part[blockIdx.x] = s;
+    }
+}
+
+// true residual statistics: sums of (f-Au)^2, ((f-Au)/D)^2, f^2, (f/D)^2
+__global__ void __launch_bounds__(kRedThreads) k_resid_stats(int m, long P, const double *f,
+    const double *Au, const double *aE, const double *aN, const double *rr, const double *aW,
+    const double *aS, double *part4)
+{
+    __shared__ double sm[32];
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    const long tot = (long)m * m;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
+        const long g = (long)j * P + i;
+        const double D = ((aW[i] + aE[g]) + (aS[j] + aN[g])) + rr[g];
+        const double r = f[g] - Au[g];
+        s0 += r * r; s1 += (r / D) * (r / D); s2 += f[g] * f[g]; s3 += (f[g] / D) * (f[g] / D);
+    }
+    double t;
+    t = block_sum(s0, sm); if (threadIdx.x == 0) part4[blockIdx.x] = t;
+    t = block_sum(s1, sm); if (threadIdx.x == 0) part4[kRedBlocks + blockIdx.x] = t;
+    t = block_sum(s2, sm); if (threadIdx.x == 0) part4[2 * kRedBlocks + blockIdx.x] = t;
+    t = block_sum(s3, sm); if (threadIdx.x == 0) part4[3 * kRedBlocks + blockIdx.x] = t;
+}
+
+// ===================================================================================== Krylov vectors
+// out = f / D (weighted) or f, partial ||out||^2
+__global__ void __launch_bounds__(kRedThreads) k_rhs(int m, long P, const double *f, const double *aE,
+    const double *aN, const double *rr, const double *aW, const double *aS, int weighted, double *out,
+    double *part)
+{
+    __shared__ double sm[32];
+    double acc = 0.0;
+    const long tot = (long)m * m;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
+        const long g = (long)j * P + i;
+        double v = f[g];
+        if (weighted) v /= ((aW[i] + aE[g]) + (aS[j] + aN[g])) + rr[g];
+        out[g] = v;
+        acc += v * v;
+    }
+    const double s = block_sum(acc, sm);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// x *= alpha (alpha from host)
+__global__ void k_scale(long n2, double *x, double alpha)
+{
+    const long n = n2 / 2;
+    double2 *x2 = reinterpret_cast<double2 *>(x);
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < n; p += (long)gridDim.x * blockDim.x) {
+        double2 a = x2[p];
+        a.x *= alpha; a.y *= alpha;
+        x2[p] = a;
+    }
+}
+
+// MGS step: h = sum(part_in) (stored to hslot by block 0);
+// w -= h * x;  part_out = <w, y>  (y == w gives ||w||^2).
+__global__ void __launch_bounds__(kRedThreads) k_mgs(long n2, double *w, const double *__restrict__ x,
+    const double *part_in, double *hslot, const double *y, double *part_out)
+{
+    __shared__ double sm[32];
+    const double h = sum_partials(part_in, sm);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *hslot = h;
+    double acc = 0.0;
+    const long n = n2 / 2;
+    double2 *w2 = reinterpret_cast<double2 *>(w);
+    const double2 *x2 = reinterpret_cast<const double2 *>(x);
+    const double2 *y2 = reinterpret_cast<const double2 *>(y);
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < n; p += (long)gridDim.x * blockDim.x) {
+        double2 a = w2[p];
+        const double2 b = x2[p];
+        a.x -= h * b.x; a.y -= h * b.y;
+        w2[p] = a;
+        if (y == w) acc += a.x * a.x + a.y * a.y;
+        else { const double2 c = y2[p]; acc += a.x * c.x + a.y * c.y; }
+    }
+    const double s = block_sum(acc, sm);
+    if (threadIdx.x == 0) part_out[blockIdx.x] = s;
+}
+
+// h = sqrt(sum(part_in)) -> hslot;  v = w / h (0 if h == 0)
+__global__ void __launch_bounds__(kRedThreads) k_normalize(long n2, const double *w, const double *part_in,
+                                                           double *hslot, double *v)
+{
+    __shared__ double sm[32];
+    const double h = sqrt(sum_partials(part_in, sm));
+    if (blockIdx.x == 0 && threadIdx.x == 0) *hslot = h;
+    const double inv = h > 0.0 ? 1.0 / h : 0.0;
+    const long n = n2 / 2;
+    const double2 *w2 = reinterpret_cast<const double2 *>(w);
+    double2 *v2 = reinterpret_cast<double2 *>(v);
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < n; p += (long)gridDim.x * blockDim.x) {
+        const double2 a = w2[p];
+        v2[p] = make_double2(a.x * inv, a.y * inv);
+    }
+}
+
+// x = sum_j y_j Z_j  ("construction of the solution once converged")
+__global__ void k_update_x(long n2, int k, const double *const *Z, const double *y, double *x)
+{
+    const long n = n2 / 2;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < n; p += (long)gridDim.x * blockDim.x) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int j = 0; j < k; ++j) {
+            const double2 a = reinterpret_cast<const double2 *>(Z[j])[p];
+            acc.x += y[j] * a.x; acc.y += y[j] * a.y;
+        }
+        reinterpret_cast<double2 *>(x)[p] = acc;
+    }
+}
+
+// ===================================================================================== corner MG
+// Corner right-hand side (first block row of eq:2D blocks):
+//   b_C = s v_C + [j = n] aN z(i, n+1) + [i = n] aE z(n+1, j),   s = D (weighted) or 1,
+// written to the level-0 value grid; partial ||S_0 b_C||^2 (S_0 = diag(hbar_i kbar_j)).
+__global__ void __launch_bounds__(kRedThreads) k_corner_rhs(int N, long P, long P0, const double *v,
+    const double *z, const double *aE, const double *aN, const double *rr, const double *aW,
+    const double *aS, const double *hb, const double *kb, int weighted, double *bc, double *part)
+{
+    __shared__ double sm[32];
+    const int n = N / 2;
+    double acc = 0.0;
+    const long tot = (long)n * n;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(p / n) + 1, i = (int)(p % n) + 1;
+        const long g = (long)j * P + i;
+        double s = 1.0;
+        if (weighted) s = ((aW[i] + aE[g]) + (aS[j] + aN[g])) + rr[g];
+        double b = s * v[g];
+        if (j == n) b += aN[g] * z[g + P];
+        if (i == n) b += aE[g] * z[g + 1];
+        bc[(long)j * P0 + i] = b;
+        const double t = (hb[i] * kb[j]) * b;
+        acc += t * t;
+    }
+    const double s = block_sum(acc, sm);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// z += e; rho = b - A z (level grid, difference form); partial ||S rho||^2.  If e == nullptr
+// only the residual is formed.
+__global__ void __launch_bounds__(kRedThreads) k_mg_resid(int nl, long Pv, long Pc, double *z,
+    const double *e, const double *b, const double *aE, const double *aN, const double *rr,
+    const double *aW, const double *aS, const double *hb, const double *kb, double *rho, double *part)
+{
+    __shared__ double sm[32];
+    double acc = 0.0;
+    const long tot = (long)nl * nl;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
+        const long g = (long)j * Pv + i, c = (long)j * Pc + i;
+        double zc, zw, ze, zs, zn;
+        if (e) {
+            zc = z[g] + e[g];
+            zw = (i > 1) ? z[g - 1] + e[g - 1] : 0.0;
+            ze = (i < nl) ? z[g + 1] + e[g + 1] : 0.0;
+            zs = (j > 1) ? z[g - Pv] + e[g - Pv] : 0.0;
+            zn = (j < nl) ? z[g + Pv] + e[g + Pv] : 0.0;
+        } else {
+            zc = z[g]; zw = z[g - 1]; ze = z[g + 1]; zs = z[g - Pv]; zn = z[g + Pv];
+        }
+        const double Az = aW[i] * (zc - zw) + aE[c] * (zc - ze) + aS[j] * (zc - zs) + aN[c] * (zc - zn) + rr[c] * zc;
+        const double r = b[g] - Az;
+        rho[g] = r;
+        if (part) { const double t = (hb[i] * kb[j]) * r; acc += t * t; }
+    }
+    if (part) {
+        const double s = block_sum(acc, sm);
+        if (threadIdx.x == 0) part[blockIdx.x] = s;
+    }
+}
+
+// z += e on the level grid (separate pass when the residual is not needed)
+__global__ void k_mg_add(int nl, long Pv, double *z, const double *e)
+{
+    const long tot = (long)nl * nl;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
+        const long g = (long)j * Pv + i;
+        z[g] += e[g];
+    }
+}
+
+// b_c = S_c^{-1} P^T S_f rho_f: coarse (I,J) gathers fine (2I+a, 2J+b),
+// a, b in {-1,0,1}, weights (1 - |a|/2)(1 - |b|/2), fine indices restricted to 1..nf.
+__global__ void k_restrict(int nf, long Pf, const double *rho, const double *hbf, const double *kbf,
+                           int nc, long Pc, const double *hbc, const double *kbc, double *bc)
+{
+    const long tot = (long)nc * nc;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int J = (int)(p / nc) + 1, I = (int)(p % nc) + 1;
+        double s = 0.0;
+#pragma unroll
+        for (int b = -1; b <= 1; ++b) {
+            const int j = 2 * J + b;
+            if (j < 1 || j > nf) continue;
+            const double wb = b == 0 ? 1.0 : 0.5;
+            double sr = 0.0;
+#pragma unroll
+            for (int a = -1; a <= 1; ++a) {
+                const int i = 2 * I + a;
+                if (i < 1 || i > nf) continue;
+                const double wa = a == 0 ? 1.0 : 0.5;
+                sr += wa * (hbf[i] * rho[(long)j * Pf + i]);
+            }
+            s += wb * (kbf[j] * sr);
+        }
+        bc[(long)J * Pc + I] = s / (hbc[I] * kbc[J]);
+    }
+}
+
+// bilinear interpolation of the coarse correction at fine node (i, j)
+__device__ __forceinline__ double interp(const double *ec, long Pc, int i, int j)
+{
+    // coarse index of even fine node 2I is I; odd 2I+1 is between I and I+1 (ghost 0 at I = 0)
+    const int I0 = i >> 1, J0 = j >> 1;
+    const bool oi = i & 1, oj = j & 1;
+    if (!oi && !oj) return ec[(long)J0 * Pc + I0];
+    if (oi && !oj) return 0.5 * (ec[(long)J0 * Pc + I0] + ec[(long)J0 * Pc + I0 + 1]);
+    if (!oi && oj) return 0.5 * (ec[(long)J0 * Pc + I0] + ec[(long)(J0 + 1) * Pc + I0]);
+    return 0.25 * ((ec[(long)J0 * Pc + I0] + ec[(long)J0 * Pc + I0 + 1]) +
+                   (ec[(long)(J0 + 1) * Pc + I0] + ec[(long)(J0 + 1) * Pc + I0 + 1]));
+}
+
+// Post-smoothing preparation: with e' = e + P e_c (never stored), form the GS right-hand side
+// of the E/N-implicit sweep:  q = (b + aW e'(i-1,j) + aS e'(i,j-1)) / D.
+__global__ void k_prolong_prep(int nl, long Pv, long Pk, const double *e, const double *ec, long Pcv,
+                               const double *b, const double *aW, const double *aS, const double *cd,
+                               double *q)
+{
+    const long tot = (long)nl * nl;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
+        const long g = (long)j * Pv + i;
+        const double ew = (i > 1) ? e[g - 1] + interp(ec, Pcv, i - 1, j) : 0.0;
+        const double es = (j > 1) ? e[g - Pv] + interp(ec, Pcv, i, j - 1) : 0.0;
+        q[g] = (b[g] + aW[i] * ew + aS[j] * es) * cd[(long)j * Pk + i];
+    }
+}
+
+// Gauss-Seidel preparation for a sweep from a nonzero e: q = (b + aW e_W + aS e_S) / D
+__global__ void k_gs_prep(int nl, long Pv, long Pk, const double *e, const double *b, const double *aW,
+                          const double *aS, const double *cd, double *q)
+{
+    const long tot = (long)nl * nl;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
+        const long g = (long)j * Pv + i;
+        q[g] = (b[g] + aW[i] * e[g - 1] + aS[j] * e[g - Pv]) * cd[(long)j * Pk + i];
+    }
+}
+
+// final prolongation for the PROLONG_ADD test hook: e += P e_c
+__global__ void k_prolong_add(int nl, long Pv, double *e, const double *ec, long Pcv)
+{
+    const long tot = (long)nl * nl;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
+        e[(long)j * Pv + i] += interp(ec, Pcv, i, j);
+    }
+}
+
+// copy the corner iterate into the global preconditioned vector
+__global__ void k_corner_out(int n, long P0, const double *zc, long P, double *z)
+{
+    const long tot = (long)n * n;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(p / n) + 1, i = (int)(p % n) + 1;
+        z[(long)j * P + i] = zc[(long)j * P0 + i];
+    }
+}
+
+// level grid compact <-> padded (test hooks)
+__global__ void k_pack_level(int nl, long Pv, const double *src, double *dst)
+{
+    const long tot = (long)nl * nl;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x)
+        dst[(long)(p / nl + 1) * Pv + (p % nl + 1)] = src[p];
+}
+__global__ void k_unpack_level(int nl, long Pv, const double *src, double *dst)
+{
+    const long tot = (long)nl * nl;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x)
+        dst[p] = src[(long)(p / nl + 1) * Pv + (p % nl + 1)];
+}
+
+}  // namespace spp

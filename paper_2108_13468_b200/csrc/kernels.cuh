@@ -1,0 +1,63 @@
+// kernels.cuh -- declarations of the kernels shared between translation units.
+#pragma once
+#include "spp_internal.cuh"
+
+namespace spp {
+
+__global__ void k_coef_1d(int N, double eps, double hx, double Hx, double hy, double Hy, double *aW, double *aS);
+__global__ void k_coef_2d(int N, long P, double eps, double hx, double Hx, double hy, double Hy,
+                          const double *c1, const double *c2, const double *r, const double *aW,
+                          const double *aS, double *aE, double *aN, double *rr, double *ca,
+                          double *cn, double *cd);
+__global__ void k_coef_level(int N, int nl, int step, long Pl, double eps, double hx, double Hx,
+                             double hy, double Hy, const double *c1, const double *c2,
+                             const double *r, double *aW, double *aS, double *hb, double *kb,
+                             double *aE, double *aN, double *rr, double *ca, double *cn, double *cd);
+__global__ void k_level0_1d(int N, double hx, double Hx, double hy, double Hy, const double *aW,
+                            const double *aS, double *lW, double *lS, double *hb, double *kb);
+__global__ void k_validate(long tot, const double *c1, const double *c2, const double *r, int *bad);
+__global__ void k_pack(int m, long P, const double *src, double *dst);
+__global__ void k_unpack(int m, long P, const double *src, double *dst);
+__global__ void k_spmv(int m, long P, const double *z, const double *aE, const double *aN,
+                       const double *rr, const double *aW, const double *aS, int weighted, double *w,
+                       const double *v0, double *part);
+__global__ void k_resid_stats(int m, long P, const double *f, const double *Au, const double *aE,
+                              const double *aN, const double *rr, const double *aW, const double *aS,
+                              double *part4);
+__global__ void k_rhs(int m, long P, const double *f, const double *aE, const double *aN,
+                      const double *rr, const double *aW, const double *aS, int weighted,
+                      double *out, double *part);
+__global__ void k_scale(long n2, double *x, double alpha);
+__global__ void k_mgs(long n2, double *w, const double *x, const double *part_in, double *hslot,
+                      const double *y, double *part_out);
+__global__ void k_normalize(long n2, const double *w, const double *part_in, double *hslot, double *v);
+__global__ void k_update_x(long n2, int k, const double *const *Z, const double *y, double *x);
+__global__ void k_corner_rhs(int N, long P, long P0, const double *v, const double *z,
+                             const double *aE, const double *aN, const double *rr, const double *aW,
+                             const double *aS, const double *hb, const double *kb, int weighted,
+                             double *bc, double *part);
+__global__ void k_mg_resid(int nl, long Pv, long Pc, double *z, const double *e, const double *b,
+                           const double *aE, const double *aN, const double *rr, const double *aW,
+                           const double *aS, const double *hb, const double *kb, double *rho,
+                           double *part);
+__global__ void k_mg_add(int nl, long Pv, double *z, const double *e);
+__global__ void k_restrict(int nf, long Pf, const double *rho, const double *hbf, const double *kbf,
+                           int nc, long Pc, const double *hbc, const double *kbc, double *bc);
+__global__ void k_prolong_prep(int nl, long Pv, long Pk, const double *e, const double *ec, long Pcv,
+                               const double *b, const double *aW, const double *aS, const double *cd,
+                               double *q);
+__global__ void k_gs_prep(int nl, long Pv, long Pk, const double *e, const double *b, const double *aW,
+                          const double *aS, const double *cd, double *q);
+__global__ void k_prolong_add(int nl, long Pv, double *e, const double *ec, long Pcv);
+__global__ void k_corner_out(int n, long P0, const double *zc, long P, double *z);
+__global__ void k_pack_level(int nl, long Pv, const double *src, double *dst);
+__global__ void k_unpack_level(int nl, long Pv, const double *src, double *dst);
+
+void launch_lines(Ctx *c, const double *v, double *z);
+
+// 1D solver (k_1d.cu)
+spp_status setup_1d(Ctx *c, const double *cc, const double *r, spp_mem mem);
+spp_status solve_1d_abi(Ctx *c, const double *f, double *u, spp_mem mem, double *hist, int hcap,
+                        spp_stats *st);
+
+}  // namespace spp

@@ -1,0 +1,137 @@
+// spp_internal.cuh -- device layout, context and kernel declarations of the B200 solver.
+//
+// Layout: every 2D grid function lives in a padded array
+// with a zero ghost ring: node (i, j) at [j * pitch + i], i, j = 0 .. n+1 where 1..n are the
+// unknowns of that grid and 0 / n+1 the (homogeneous Dirichlet) ghosts; pitch is a multiple
+// of 16 doubles so 16-column blocks are 128-byte aligned.  Ghosts and padding hold zeros and
+// every kernel preserves that, so vector kernels run over the flat array.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "spp.h"
+
+namespace spp {
+
+constexpr int kMaxLevels = 24;
+constexpr int kWarp = 32;
+constexpr int kRedBlocks = 592;      // 4 x 148 SMs: fixed grid for deterministic reductions
+constexpr int kRedThreads = 256;
+
+inline long round_up(long a, long b) { return (a + b - 1) / b * b; }
+
+// ------------------------------------------------------------------------------------------
+// wavefront sweep  z(i,j) = s(i,j) q(i,j) + ca(i,j) z(i+1,j) + cn(i,j) z(i,j+1)
+// over the rectangle [ilo,ihi] x [jlo,jhi]; zero inflow at i = ihi+1 and j = jhi+1.
+// ------------------------------------------------------------------------------------------
+struct SweepArgs {
+    const double *q; long qp;            // rhs (value layout)
+    const double *s; long sp;            // optional per-node scale (nullptr -> 1)
+    const double *ca, *cn; long cp;      // aE/D and aN/D (coefficient layout)
+    double *z; long zp;                  // output (value layout)
+    int ilo, ihi, jlo, jhi;
+    int rows_out;                        // output rows per CTA (multiple of 32)
+    int halo;                            // halo rows recomputed above each CTA (HALO mode)
+    int *flags; int epoch;               // EXACT mode inter-CTA progress
+};
+
+// line-chain solve (M_XX / M_YY): see k_lines.cu
+struct LineChain {
+    int nlines, len;        // lines in the chain, unknowns per line
+    long vstride;           // address step along a line in the value grid
+    long vline;             // address step from line l to line l+1 (the next line processed)
+    long v0;                // value-grid address of element 0 of line 0
+    long istep;             // value-grid address offset of the I-neighbour of the last element
+    const double *p, *e, *al, *be;  // factors, line-major [l * len + k]
+    const double *t;        // per-line coupling factor to I at the last element
+};
+struct LineChunk { int chain, first, last, start; };   // lines [first,last] owned, processing from `start`
+
+struct Level {
+    int n = 0;                           // unknowns per axis
+    long pitch = 0;                      // value pitch
+    size_t elems = 0;
+    const double *aE = nullptr, *aN = nullptr, *rr = nullptr;   // coefficients (coef pitch cpitch)
+    const double *ca = nullptr, *cn = nullptr, *cd = nullptr;   // aE/D, aN/D, 1/D
+    long cpitch = 0;
+    double *aW = nullptr, *aS = nullptr, *hb = nullptr, *kb = nullptr;   // 1D [n+2]
+    double *own = nullptr;               // owned coefficient block (levels >= 1)
+    double *b = nullptr, *e = nullptr, *q = nullptr, *rho = nullptr;     // work (value layout)
+};
+
+struct ProfRec { int64_t launches = 0; double ms = 0, bytes = 0; };
+
+struct Ctx {
+    int dim = 0, N = 0, n = 0, m = 0;    // N intervals, n = N/2, m = N-1
+    double eps = 0;
+    spp_options opt{};
+    cudaStream_t st = nullptr;
+    int weighted = 1;
+    std::string err;
+    // mesh (widths from the piecewise-uniform formula with tau = x[N/2])
+    double tx = 0, ty = 0, hx = 0, Hx = 0, hy = 0, Hy = 0;
+    std::vector<double> xh, yh;
+    // global padded grid
+    long P = 0; size_t G = 0;
+    double *aE = nullptr, *aN = nullptr, *rr = nullptr;         // coefficients
+    double *ca = nullptr, *cn = nullptr, *cd = nullptr;         // aE/D, aN/D, 1/D
+    double *aW = nullptr, *aS = nullptr;                        // [N+1]
+    double *coef_block = nullptr;
+    // line factors
+    double *fac = nullptr;                 // X then Y: 4 arrays each of (n-1)*n
+    double *tX = nullptr, *tY = nullptr, *kapX = nullptr, *kapY = nullptr;
+    LineChain chX{}, chY{};
+    std::vector<LineChunk> chunks; LineChunk *d_chunks = nullptr; int nchunks_alloc = 0;
+    int lines_threads = 256;
+    // Krylov
+    std::vector<double *> V, Z;
+    double *w = nullptr, *F = nullptr, *U = nullptr, *T1 = nullptr;
+    double *part = nullptr;                // reduction partials [kMaxParts][kRedBlocks]
+    double *dscal = nullptr;               // device scalars
+    double *hpin = nullptr;                // pinned host mirror of scalars
+    int vec_alloc = 0;
+    // corner MG
+    int L = 0;
+    Level lev[kMaxLevels];
+    double *Zc = nullptr, *Bc = nullptr;   // corner iterate / rhs (level-0 value layout)
+    double *mg_block = nullptr;
+    int *flags = nullptr; int epoch = 0;
+    // 1D
+    double *d1 = nullptr;
+    // compact staging buffers
+    double *cbuf = nullptr;
+    // statistics / profiling
+    int64_t launches = 0;
+    int prof_on = 0;
+    ProfRec prof[SPP_PROF_CLASSES];
+    std::vector<cudaEvent_t> ev_pool; size_t ev_used = 0;
+    struct PendingProf { int cls; cudaEvent_t a, b; double bytes; };
+    std::vector<PendingProf> pend;
+    float setup_ms = 0;
+    int sm_count = 148;
+};
+
+// kernels / launchers (defined in the .cu files)
+void launch_sweep(Ctx *c, const SweepArgs &a, bool exact, int cls, double bytes);
+cudaError_t setup_global(Ctx *c, const double *c1, const double *c2, const double *r);
+cudaError_t setup_levels(Ctx *c, const double *c1, const double *c2, const double *r);
+cudaError_t setup_lines(Ctx *c);
+void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double> &ky);
+
+// profiling helpers
+struct ProfScope {
+    Ctx *c; int cls; double bytes; cudaEvent_t a = nullptr;
+    ProfScope(Ctx *c_, int cls_, double bytes_);
+    ~ProfScope();
+};
+
+}  // namespace spp
+
+#define SPP_CUDA_TRY(expr)                                                   \
+    do {                                                                     \
+        cudaError_t _e = (expr);                                             \
+        if (_e != cudaSuccess) return _e;                                    \
+    } while (0)
