@@ -6,6 +6,7 @@
 // scalars").
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -103,78 +104,44 @@ static cudaError_t fetch_sum(Ctx *c, const double *part, double *out)
 
 static double *part_slot(Ctx *c, int k) { return c->part + (size_t)k * kRedBlocks; }
 
-// ------------------------------------------------------------------------------------------ sweeps
-static SweepArgs sweep_level(Ctx *c, int l, const double *q, bool scaled, double *z)
+// ------------------------------------------------------------------------------------------ corner MG
+// V(1,1) cycle for A_l e = R, zero initial guess ("standard V(1,1) cycling", one
+// downstream GS sweep before and after the coarse-grid correction; coarsest grid: "four sweeps",
+// P:1208-1209 / P:1281-1283).  Returns the buffer holding e (lev[l].e or lev[l].q).
+static double *vcycle(Ctx *c, int l, const double *R)
 {
     Level &L = c->lev[l];
-    SweepArgs a{};
-    a.q = q; a.qp = L.pitch;
-    a.s = scaled ? L.cd : nullptr; a.sp = L.cpitch;
-    a.ca = L.ca; a.cn = L.cn; a.cp = L.cpitch;
-    a.z = z; a.zp = L.pitch;
-    a.ilo = 1; a.ihi = L.n; a.jlo = 1; a.jhi = L.n;
-    a.rows_out = 512; a.halo = 0;
-    a.flags = c->flags; a.epoch = 0;
-    return a;
-}
-
-static void mg_sweep(Ctx *c, int l, const double *q, bool scaled, double *z)
-{
-    Level &L = c->lev[l];
-    SweepArgs a = sweep_level(c, l, q, scaled, z);
-    launch_sweep(c, a, true, 3, 32.0 * L.n * (double)L.n + (scaled ? 8.0 * L.n * (double)L.n : 0.0));
-}
-
-// V(1,1) cycle for A_l e = b, zero initial guess.  Result in lev[l].e.
-static void vcycle(Ctx *c, int l, const double *b)
-{
-    Level &L = c->lev[l];
-    const int nl = L.n;
-    const double nn = (double)nl * nl;
-    const int gb = nblk((long)nl * nl);
+    double *ea = L.e, *eb = L.q;
     if (l == c->L - 1) {
-        mg_sweep(c, l, b, true, L.e);                         // sweep 1 from e = 0
-        for (int s = 1; s < 4; ++s) {                         // "four sweeps"
-            {
-                ProfScope ps(c, 5, 40.0 * nn);
-                k_gs_prep<<<gb, 256, 0, c->st>>>(nl, L.pitch, L.cpitch, L.e, b, L.aW, L.aS, L.cd, L.q);
-                c->launches++;
-            }
-            mg_sweep(c, l, L.q, false, L.e);
-        }
-        return;
+        launch_gs(c, l, 0, R, nullptr, ea, nullptr);
+        launch_gs(c, l, 1, R, ea, eb, nullptr);
+        launch_gs(c, l, 1, R, eb, ea, nullptr);
+        launch_gs(c, l, 1, R, ea, eb, nullptr);
+        return eb;
     }
     Level &C = c->lev[l + 1];
-    mg_sweep(c, l, b, true, L.e);                             // pre-smoothing from zero
-    {
-        ProfScope ps(c, 4, 48.0 * nn + 8.0 * nn + 8.0 * C.n * (double)C.n);
-        k_mg_resid<<<gb, 256, 0, c->st>>>(nl, L.pitch, L.cpitch, L.e, nullptr, b, L.aE, L.aN, L.rr,
-                                         L.aW, L.aS, L.hb, L.kb, L.rho, nullptr);
-        k_restrict<<<nblk((long)C.n * C.n), 256, 0, c->st>>>(nl, L.pitch, L.rho, L.hb, L.kb, C.n, C.pitch,
-                                                              C.hb, C.kb, C.b);
-        c->launches += 2;
-    }
-    vcycle(c, l + 1, C.b);
-    {
-        ProfScope ps(c, 5, 8.0 * nn + 2.0 * nn + 8.0 * nn + 8.0 * nn + 8.0 * nn);
-        k_prolong_prep<<<gb, 256, 0, c->st>>>(nl, L.pitch, L.cpitch, L.e, C.e, C.pitch, b, L.aW, L.aS, L.cd, L.q);
-        c->launches++;
-    }
-    mg_sweep(c, l, L.q, false, L.e);                          // post-smoothing
+    launch_gs(c, l, 0, R, nullptr, ea, nullptr);             // pre-smoothing from zero
+    launch_resid_restrict(c, l, R, ea);                       // C.b = S^-1 P^T S (R - A_l ea)
+    const double *ec = vcycle(c, l + 1, C.b);
+    launch_gs(c, l, 1, R, ea, eb, ec);                        // post-smoothing from ea + P ec
+    return eb;
 }
 
-// M_CC^{-1} b_C: stationary V-cycle iteration until ||S_0 rho|| <= red ||S_0 b|| (P:1283-1287,
-// reading R6), z = 0 start, cap.  b0sq = ||S_0 b||^2.  Result in c->Zc.  Returns cycles.
-static int corner_solve(Ctx *c, const double *bc, double b0sq, int *cap_hit, cudaError_t *err)
+// M_CC^{-1} b_C: stationary V-cycle iteration z <- z + V(b_C - A_CC z) from z = 0 until
+// ||S_0 rho||_2 <= mg_reduction ||S_0 b_C||_2 (reading R6), cap mg_max_cycles
+// (S:496); or exactly mg_fixed_cycles cycles (reading R17).  b0sq = ||S_0 b_C||^2.
+// *zout = the buffer holding z (nullptr when no cycle ran: z = 0).  Returns the cycle count.
+static int corner_solve(Ctx *c, const double *bc, double b0sq, int *cap_hit, cudaError_t *err,
+                        const double **zout)
 {
     Level &L0 = c->lev[0];
-    const int n = L0.n;
-    const int gb = nblk((long)n * n);
     *cap_hit = 0;
-    *err = cudaMemsetAsync(c->Zc, 0, sizeof(double) * L0.elems, c->st);
+    *err = cudaSuccess;
     const double b0 = std::sqrt(b0sq);
     double res = b0;
-    const double *rho = bc;
+    const double *R = bc;
+    const double *z = nullptr;
+    double *zb[2] = {c->Zc, c->Zc2};
     int cycles = 0;
     const int fixed = c->opt.mg_fixed_cycles;
     for (;;) {
@@ -183,27 +150,33 @@ static int corner_solve(Ctx *c, const double *bc, double b0sq, int *cap_hit, cud
             if (res <= c->opt.mg_reduction * b0) break;
             if (cycles >= c->opt.mg_max_cycles) { *cap_hit = 1; break; }
         }
-        vcycle(c, 0, rho);
-        const bool need_norm = fixed <= 0;
-        {
-            ProfScope ps(c, 6, 8.0 * 7 * (double)n * n);
-            k_mg_resid<<<kRedBlocks, kRedThreads, 0, c->st>>>(n, L0.pitch, L0.cpitch, c->Zc, L0.e, bc, L0.aE,
-                L0.aN, L0.rr, L0.aW, L0.aS, L0.hb, L0.kb, L0.b, need_norm ? part_slot(c, 0) : nullptr);
-            c->launches++;
-        }
-        // k_mg_resid formed rho from z + e; commit z += e
-        k_mg_add<<<gb, 256, 0, c->st>>>(n, L0.pitch, c->Zc, L0.e);
-        c->launches++;
-        rho = L0.b;
+        const double *e = vcycle(c, 0, R);
+        double *zn = zb[cycles & 1];
+        launch_cycle_update(c, z, e, zn, bc, L0.rho, part_slot(c, 0));   // z += e; rho = b - A z
+        z = zn;
+        R = L0.rho;
         cycles++;
-        if (need_norm) {
+        if (fixed <= 0) {
             double s = 0;
-            cudaError_t e = fetch_sum(c, part_slot(c, 0), &s);
-            if (e != cudaSuccess) { *err = e; return cycles; }
+            cudaError_t e2 = fetch_sum(c, part_slot(c, 0), &s);
+            if (e2 != cudaSuccess) { *err = e2; break; }
             res = std::sqrt(s);
         }
     }
+    *zout = z;
     return cycles;
+}
+
+// M_II solve on region I = [n+1, N-1]^2: z = (D - E - N)^{-1} (s v), s = 1/D
+// (scaled, unweighted mode) or 1 (Jacobi mode: the input is already D v, reading R11); the exact
+// chained row-scan sweep of k_mg.cu with the level origin at (n, n) of the global grid.
+static void launch_mii(Ctx *c, const double *v, double *z, bool scaled)
+{
+    WaveArgs a{};
+    a.nl = c->n - 1; a.pv = c->P; a.pc = c->P; a.ioff = c->n; a.joff = c->n;
+    a.q = v; a.s = scaled ? c->cd : nullptr; a.ca = c->ca; a.cn = c->cn; a.z = z;
+    const double nn = (double)a.nl * a.nl;
+    launch_wave_chain(c, a, 1, nn * (scaled ? 40.0 : 32.0));
 }
 
 // z = M^{-1} v (eq:2D blocks by block back-substitution I -> Y -> X -> C).
@@ -211,15 +184,8 @@ static int corner_solve(Ctx *c, const double *bc, double b0sq, int *cap_hit, cud
 static int apply_precond(Ctx *c, const double *v, double *z, int *cap_hit, cudaError_t *err)
 {
     const int N = c->N, n = c->n;
-    // M_II
-    SweepArgs a{};
-    a.q = v; a.qp = c->P;
-    a.s = c->weighted ? nullptr : c->cd; a.sp = c->P;
-    a.ca = c->ca; a.cn = c->cn; a.cp = c->P;
-    a.z = z; a.zp = c->P;
-    a.ilo = n + 1; a.ihi = N - 1; a.jlo = n + 1; a.jhi = N - 1;
-    a.rows_out = 512; a.halo = 0; a.flags = c->flags;
-    launch_sweep(c, a, true, 1, 32.0 * (double)(n - 1) * (n - 1));
+    // M_II: exact downstream triangular solve on region I
+    launch_mii(c, v, z, !c->weighted);
     // M_YY and M_XX (one launch, both chains)
     launch_lines(c, v, z);
     // corner
@@ -235,8 +201,13 @@ static int apply_precond(Ctx *c, const double *v, double *z, int *cap_hit, cudaE
         cudaError_t e = fetch_sum(c, part_slot(c, 1), &b0sq);
         if (e != cudaSuccess) { *err = e; return 0; }
     }
-    int cyc = corner_solve(c, c->Bc, b0sq, cap_hit, err);
-    k_corner_out<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, c->Zc, c->P, z);
+    const double *zc = nullptr;
+    int cyc = corner_solve(c, c->Bc, b0sq, cap_hit, err, &zc);
+    if (!zc) {
+        *err = cudaMemsetAsync(c->Zc, 0, sizeof(double) * L0.elems, c->st);
+        zc = c->Zc;
+    }
+    k_corner_out<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, zc, c->P, z);
     c->launches++;
     return cyc;
 }
@@ -290,6 +261,31 @@ spp_status spp_shishkin_mesh(int32_t n, double eps, double sigma, double beta, d
     return SPP_OK;
 }
 
+// SPP_TUNE="gs_tile_rows=128,gs_tile_cols=256,..." overrides kernel tunables (experiments only;
+// every setting computes the same result to rounding).
+static void parse_tune(Ctx *c)
+{
+    const char *env = getenv("SPP_TUNE");
+    if (!env) return;
+    std::string s(env);
+    size_t pos = 0;
+    while (pos < s.size()) {
+        size_t end = s.find(',', pos);
+        if (end == std::string::npos) end = s.size();
+        const std::string kv = s.substr(pos, end - pos);
+        const size_t eq = kv.find('=');
+        if (eq != std::string::npos) {
+            const std::string k = kv.substr(0, eq);
+            const int v = atoi(kv.c_str() + eq + 1);
+            if (k == "gs_warps") c->tune.gs_warps = v;
+            else if (k == "gs_tile_cols") c->tune.gs_tile_cols = v;
+            else if (k == "gs_max_halo") c->tune.gs_max_halo = v;
+            else if (k == "sweep_warps") c->tune.sweep_warps = v;
+        }
+        pos = end + 1;
+    }
+}
+
 static spp_status check_mesh(const double *x, int N, double *tau, Ctx *c)
 {
     if (!x) FAIL(c, SPP_E_ARG, "mesh coordinates are NULL");
@@ -331,11 +327,19 @@ static spp_status alloc_all(Ctx *c)
     CK(c, cudaMemsetAsync(c->w, 0, sizeof(double) * 4 * G, c->st));
     c->F = c->w + G; c->U = c->F + G; c->T1 = c->U + G;
     const int maxit = c->opt.max_iters;
-    CK(c, cudaMalloc(&c->part, sizeof(double) * (size_t)(maxit + 8) * kRedBlocks));
+    CK(c, cudaMalloc(&c->part, sizeof(double) * (size_t)(std::max(maxit, kMaxLevels) + 8) * kRedBlocks));
     CK(c, cudaMalloc(&c->dscal, sizeof(double) * (size_t)(3 * maxit + 64)));
-    CK(c, cudaMallocHost(&c->hpin, sizeof(double) * (size_t)(4 * kRedBlocks + 3 * maxit + 64)));
+    CK(c, cudaMallocHost(&c->hpin, sizeof(double) * std::max<size_t>(4 * kRedBlocks + 3 * (size_t)maxit + 64,
+                                                                      (size_t)kMaxLevels * kRedBlocks)));
     CK(c, cudaMalloc(&c->flags, sizeof(int) * 256));
     CK(c, cudaMemsetAsync(c->flags, 0, sizeof(int) * 256, c->st));
+    {   // exact chained sweep: one progress flag and one inflow row per CTA
+        const int W = std::max(1, std::min(c->tune.sweep_warps, 8));
+        const long ncta = (n + 32L * W - 1) / (32L * W) + 1;
+        c->chain_ld = n + 32;
+        CK(c, cudaMalloc(&c->chain, sizeof(double) * (size_t)(ncta * c->chain_ld)));
+        CK(c, cudaMalloc(&c->chain_flags, sizeof(int) * (size_t)(ncta + 1)));
+    }
     // corner MG levels (levels until <= mg_coarsest per axis)
     int nl = n, L = 1;
     const int coarsest = c->opt.mg_coarsest > 0 ? c->opt.mg_coarsest : 4;
@@ -347,15 +351,16 @@ static spp_status alloc_all(Ctx *c)
         Lv.n = n >> l;
         Lv.pitch = round_up(Lv.n + 2, 16);
         Lv.elems = (size_t)(Lv.n + 2) * Lv.pitch;
-        tot += 4 * Lv.elems + 4 * (size_t)(Lv.n + 2) + (l > 0 ? 6 * Lv.elems : 0);
+        tot += 5 * Lv.elems + 4 * (size_t)(Lv.n + 2) + (l > 0 ? 6 * Lv.elems : 0);
     }
-    tot += 2 * c->lev[0].elems;   // Zc, Bc
+    tot += 3 * c->lev[0].elems;   // Zc, Zc2, Bc
     CK(c, cudaMalloc(&c->mg_block, sizeof(double) * tot));
     CK(c, cudaMemsetAsync(c->mg_block, 0, sizeof(double) * tot, c->st));
     double *p = c->mg_block;
     for (int l = 0; l < L; ++l) {
         Level &Lv = c->lev[l];
         Lv.b = p; p += Lv.elems; Lv.e = p; p += Lv.elems; Lv.q = p; p += Lv.elems; Lv.rho = p; p += Lv.elems;
+        Lv.g = p; p += Lv.elems;
         Lv.aW = p; p += Lv.n + 2; Lv.aS = p; p += Lv.n + 2; Lv.hb = p; p += Lv.n + 2; Lv.kb = p; p += Lv.n + 2;
         if (l > 0) {
             Lv.own = p;
@@ -369,6 +374,7 @@ static spp_status alloc_all(Ctx *c)
         }
     }
     c->Zc = p; p += c->lev[0].elems;
+    c->Zc2 = p; p += c->lev[0].elems;
     c->Bc = p; p += c->lev[0].elems;
     return SPP_OK;
 }
@@ -431,6 +437,7 @@ static spp_status do_setup_2d(Ctx *c, const double *c1, const double *c2, const 
     CK(c, cudaStreamSynchronize(c->st));
     if (hbad) FAIL(c, SPP_E_COEF, "coefficients violate c1 > 0, c2 > 0, r >= 0 or are not finite (P:208-212, P:907)");
     CK(c, setup_lines(c));
+    CK(c, setup_mg_tiles(c));
     CK(c, cudaEventRecord(e1, c->st));
     CK(c, cudaEventSynchronize(e1));
     cudaEventElapsedTime(&c->setup_ms, e0, e1);
@@ -471,9 +478,11 @@ spp_status spp_create(const spp_problem *p, const spp_options *o, void *stream, 
     if (c->opt.mg_max_cycles < 1) c->opt.mg_max_cycles = 20;
     if (!(c->opt.mg_reduction > 0.0)) c->opt.mg_reduction = 1e-3;
     c->weighted = c->opt.stop == SPP_STOP_REL_JACOBI ? 1 : 0;
+    parse_tune(c);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (wave_init() != cudaSuccess) { delete c; FAIL((Ctx *)nullptr, SPP_E_CUDA, "kernel attribute setup failed"); }
     spp_status s;
     double tx = 0, ty = 0;
     if ((s = check_mesh(p->x, N, &tx, c)) != SPP_OK) { g_err = c->err; delete c; return s; }
@@ -501,6 +510,7 @@ void spp_destroy(spp_ctx *cx)
     for (double *p : c->Z) cudaFree(p);
     cudaFree(c->coef_block); cudaFree(c->fac); cudaFree(c->cbuf); cudaFree(c->w);
     cudaFree(c->part); cudaFree(c->dscal); cudaFree(c->flags); cudaFree(c->mg_block);
+    cudaFree(c->chain); cudaFree(c->chain_flags);
     cudaFree(c->d_chunks); cudaFree(c->d1);
     if (c->hpin) cudaFreeHost(c->hpin);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -749,11 +759,7 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
         const int w = c->weighted;
         if (w) { c->weighted = 0; CK(c, setup_lines(c)); }
         if (s == SPP_STAGE_MII) {
-            SweepArgs a{};
-            a.q = A; a.qp = c->P; a.s = c->cd; a.sp = c->P; a.ca = c->ca; a.cn = c->cn; a.cp = c->P;
-            a.z = B; a.zp = c->P; a.ilo = n + 1; a.ihi = m; a.jlo = n + 1; a.jhi = m;
-            a.rows_out = 512; a.flags = c->flags;
-            launch_sweep(c, a, true, 1, 0);
+            launch_mii(c, A, B, true);
         } else {
             // run only the requested chain: temporarily restrict chunks
             std::vector<LineChunk> keep = c->chunks, sel;
@@ -785,10 +791,12 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
         double b0sq = 0;
         CK(c, fetch_sum(c, part_slot(c, 1), &b0sq));
         int cap = 0; cudaError_t err = cudaSuccess;
-        int k = corner_solve(c, c->Bc, b0sq, &cap, &err);
+        const double *zc = nullptr;
+        int k = corner_solve(c, c->Bc, b0sq, &cap, &err, &zc);
         CK(c, err);
+        if (!zc) { CK(c, cudaMemsetAsync(c->Zc, 0, sizeof(double) * L0.elems, c->st)); zc = c->Zc; }
         if (cyc) *cyc = k;
-        k_unpack_level<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, c->Zc, out);
+        k_unpack_level<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, zc, out);
     } else {
         if (l < 0 || l >= c->L) FAIL(c, SPP_E_ARG, "level %d out of range", l);
         Level &Lv = c->lev[l];
@@ -796,23 +804,26 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
         const long nn = (long)nl * nl;
         double *b = Lv.b, *e = Lv.e;
         if (s == SPP_STAGE_GS_SWEEP) {
-            k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in, b);
+            // one downstream GS sweep from e0 = out for rhs in (out-of-place kernel, e -> q)
+            double *rhs = c->T1;
+            CK(c, cudaMemsetAsync(rhs, 0, sizeof(double) * Lv.elems, c->st));
+            k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in, rhs);
             k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, out, e);
-            k_gs_prep<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, Lv.cpitch, e, b, Lv.aW, Lv.aS, Lv.cd, Lv.q);
-            mg_sweep(c, l, Lv.q, false, e);
-            k_unpack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, e, out);
+            launch_gs(c, l, 1, rhs, e, Lv.q, nullptr);
+            k_unpack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, Lv.q, out);
         } else if (s == SPP_STAGE_VCYCLE) {
-            double *tmp = c->T1;   // level-l rhs must not alias lev[l].b (used by coarse levels)
+            double *tmp = c->T1;   // level-l rhs must not alias the level buffers used by vcycle
             CK(c, cudaMemsetAsync(tmp, 0, sizeof(double) * Lv.elems, c->st));
             k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in, tmp);
-            vcycle(c, l, tmp);
-            k_unpack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, e, out);
+            const double *res = vcycle(c, l, tmp);
+            k_unpack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, res, out);
         } else if (s == SPP_STAGE_RESTRICT) {
+            // the fused residual-restriction kernel with e = 0 restricts R = in
             if (l + 1 >= c->L) FAIL(c, SPP_E_ARG, "no coarser level");
             Level &C = c->lev[l + 1];
+            CK(c, cudaMemsetAsync(e, 0, sizeof(double) * Lv.elems, c->st));
             k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in, Lv.rho);
-            k_restrict<<<nblk((long)C.n * C.n), 256, 0, c->st>>>(nl, Lv.pitch, Lv.rho, Lv.hb, Lv.kb, C.n, C.pitch,
-                                                                  C.hb, C.kb, C.b);
+            launch_resid_restrict(c, l, Lv.rho, e);
             k_unpack_level<<<nblk((long)C.n * C.n), 256, 0, c->st>>>(C.n, C.pitch, C.b, out);
         } else if (s == SPP_STAGE_PROLONG_ADD) {
             if (l + 1 >= c->L) FAIL(c, SPP_E_ARG, "no coarser level");

@@ -374,45 +374,6 @@ __global__ void __launch_bounds__(kRedThreads) k_mg_resid(int nl, long Pv, long 
     }
 }
 
-// z += e on the level grid (separate pass when the residual is not needed)
-__global__ void k_mg_add(int nl, long Pv, double *z, const double *e)
-{
-    const long tot = (long)nl * nl;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
-        const long g = (long)j * Pv + i;
-        z[g] += e[g];
-    }
-}
-
-// b_c = S_c^{-1} P^T S_f rho_f: coarse (I,J) gathers fine (2I+a, 2J+b),
-// a, b in {-1,0,1}, weights (1 - |a|/2)(1 - |b|/2), fine indices restricted to 1..nf.
-__global__ void k_restrict(int nf, long Pf, const double *rho, const double *hbf, const double *kbf,
-                           int nc, long Pc, const double *hbc, const double *kbc, double *bc)
-{
-    const long tot = (long)nc * nc;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int J = (int)(p / nc) + 1, I = (int)(p % nc) + 1;
-        double s = 0.0;
-#pragma unroll
-        for (int b = -1; b <= 1; ++b) {
-            const int j = 2 * J + b;
-            if (j < 1 || j > nf) continue;
-            const double wb = b == 0 ? 1.0 : 0.5;
-            double sr = 0.0;
-#pragma unroll
-            for (int a = -1; a <= 1; ++a) {
-                const int i = 2 * I + a;
-                if (i < 1 || i > nf) continue;
-                const double wa = a == 0 ? 1.0 : 0.5;
-                sr += wa * (hbf[i] * rho[(long)j * Pf + i]);
-            }
-            s += wb * (kbf[j] * sr);
-        }
-        bc[(long)J * Pc + I] = s / (hbc[I] * kbc[J]);
-    }
-}
-
 // bilinear interpolation of the coarse correction at fine node (i, j)
 __device__ __forceinline__ double interp(const double *ec, long Pc, int i, int j)
 {
@@ -426,35 +387,7 @@ __device__ __forceinline__ double interp(const double *ec, long Pc, int i, int j
                    (ec[(long)(J0 + 1) * Pc + I0] + ec[(long)(J0 + 1) * Pc + I0 + 1]));
 }
 
-// Post-smoothing preparation: with e' = e + P e_c (never stored), form the GS right-hand side
-// of the E/N-implicit sweep:  q = (b + aW e'(i-1,j) + aS e'(i,j-1)) / D.
-__global__ void k_prolong_prep(int nl, long Pv, long Pk, const double *e, const double *ec, long Pcv,
-                               const double *b, const double *aW, const double *aS, const double *cd,
-                               double *q)
-{
-    const long tot = (long)nl * nl;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
-        const long g = (long)j * Pv + i;
-        const double ew = (i > 1) ? e[g - 1] + interp(ec, Pcv, i - 1, j) : 0.0;
-        const double es = (j > 1) ? e[g - Pv] + interp(ec, Pcv, i, j - 1) : 0.0;
-        q[g] = (b[g] + aW[i] * ew + aS[j] * es) * cd[(long)j * Pk + i];
-    }
-}
-
-// Gauss-Seidel preparation for a sweep from a nonzero e: q = (b + aW e_W + aS e_S) / D
-__global__ void k_gs_prep(int nl, long Pv, long Pk, const double *e, const double *b, const double *aW,
-                          const double *aS, const double *cd, double *q)
-{
-    const long tot = (long)nl * nl;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
-        const long g = (long)j * Pv + i;
-        q[g] = (b[g] + aW[i] * e[g - 1] + aS[j] * e[g - Pv]) * cd[(long)j * Pk + i];
-    }
-}
-
-// final prolongation for the PROLONG_ADD test hook: e += P e_c
+// prolongation and correction e += P e_c
 __global__ void k_prolong_add(int nl, long Pv, double *e, const double *ec, long Pcv)
 {
     const long tot = (long)nl * nl;

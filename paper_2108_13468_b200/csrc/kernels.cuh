@@ -40,14 +40,6 @@ __global__ void k_mg_resid(int nl, long Pv, long Pc, double *z, const double *e,
                            const double *aE, const double *aN, const double *rr, const double *aW,
                            const double *aS, const double *hb, const double *kb, double *rho,
                            double *part);
-__global__ void k_mg_add(int nl, long Pv, double *z, const double *e);
-__global__ void k_restrict(int nf, long Pf, const double *rho, const double *hbf, const double *kbf,
-                           int nc, long Pc, const double *hbc, const double *kbc, double *bc);
-__global__ void k_prolong_prep(int nl, long Pv, long Pk, const double *e, const double *ec, long Pcv,
-                               const double *b, const double *aW, const double *aS, const double *cd,
-                               double *q);
-__global__ void k_gs_prep(int nl, long Pv, long Pk, const double *e, const double *b, const double *aW,
-                          const double *aS, const double *cd, double *q);
 __global__ void k_prolong_add(int nl, long Pv, double *e, const double *ec, long Pcv);
 __global__ void k_corner_out(int n, long P0, const double *zc, long P, double *z);
 __global__ void k_pack_level(int nl, long Pv, const double *src, double *dst);

@@ -23,21 +23,6 @@ constexpr int kRedThreads = 256;
 
 inline long round_up(long a, long b) { return (a + b - 1) / b * b; }
 
-// ------------------------------------------------------------------------------------------
-// wavefront sweep  z(i,j) = s(i,j) q(i,j) + ca(i,j) z(i+1,j) + cn(i,j) z(i,j+1)
-// over the rectangle [ilo,ihi] x [jlo,jhi]; zero inflow at i = ihi+1 and j = jhi+1.
-// ------------------------------------------------------------------------------------------
-struct SweepArgs {
-    const double *q; long qp;            // rhs (value layout)
-    const double *s; long sp;            // optional per-node scale (nullptr -> 1)
-    const double *ca, *cn; long cp;      // aE/D and aN/D (coefficient layout)
-    double *z; long zp;                  // output (value layout)
-    int ilo, ihi, jlo, jhi;
-    int rows_out;                        // output rows per CTA (multiple of 32)
-    int halo;                            // halo rows recomputed above each CTA (HALO mode)
-    int *flags; int epoch;               // EXACT mode inter-CTA progress
-};
-
 // line-chain solve (M_XX / M_YY): see k_lines.cu
 struct LineChain {
     int nlines, len;        // lines in the chain, unknowns per line
@@ -60,6 +45,30 @@ struct Level {
     double *aW = nullptr, *aS = nullptr, *hb = nullptr, *kb = nullptr;   // 1D [n+2]
     double *own = nullptr;               // owned coefficient block (levels >= 1)
     double *b = nullptr, *e = nullptr, *q = nullptr, *rho = nullptr;     // work (value layout)
+    double *g = nullptr;                 // GS right-hand side (k_gs_prep)
+    // GS tiling (k_mg.cu): tile_rows <= 0 -> one CTA sweeps the level; halo = certified rows /
+    // columns recomputed above / right of each tile (-1: none certifiable -> exact chained sweep)
+    int tile_rows = 0, tile_cols = 0, tile_warps = 0, halo_x = 0, halo_y = 0;
+    double contraction = 0.0;            // max (aE + aN) / D over the level
+};
+
+// corner GS sweep arguments (k_mg.cu)
+// downstream sweep z = s q + ca z_E + cn z_N on [1, nl]^2 (k_mg.cu)
+struct WaveArgs {
+    int nl; long pv, pc;
+    int ioff, joff;                      // node (i, j) lives at array index (i+ioff, j+joff)
+    const double *q, *s, *ca, *cn;       // s == nullptr: 1
+    double *z;
+    int rows_out, cols_out, halo_y, halo_x;
+    int *chain_flags; double *chain_buf; long chain_ld;   // exact chained mode
+};
+
+// tunables (defaults in spp_create; overridable through SPP_TUNE="key=val,..." for experiments)
+struct Tune {
+    int gs_warps = 4;          // warps (32-row strips) per GS tile
+    int gs_tile_cols = 512;    // output columns per GS tile
+    int gs_max_halo = 128;     // no certified halo below this -> exact chained sweep
+    int sweep_warps = 4;       // warps per CTA of the exact chained sweep (M_II)
 };
 
 struct ProfRec { int64_t launches = 0; double ms = 0, bytes = 0; };
@@ -97,6 +106,10 @@ struct Ctx {
     int L = 0;
     Level lev[kMaxLevels];
     double *Zc = nullptr, *Bc = nullptr;   // corner iterate / rhs (level-0 value layout)
+    double *Zc2 = nullptr;                 // ping-pong partner of Zc
+    double *chain = nullptr; long chain_ld = 0;   // inflow buffer of the exact chained sweep
+    int *chain_flags = nullptr;
+    Tune tune;
     double *mg_block = nullptr;
     int *flags = nullptr; int epoch = 0;
     // 1D
@@ -115,11 +128,18 @@ struct Ctx {
 };
 
 // kernels / launchers (defined in the .cu files)
-void launch_sweep(Ctx *c, const SweepArgs &a, bool exact, int cls, double bytes);
 cudaError_t setup_global(Ctx *c, const double *c1, const double *c2, const double *r);
 cudaError_t setup_levels(Ctx *c, const double *c1, const double *c2, const double *r);
 cudaError_t setup_lines(Ctx *c);
 void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double> &ky);
+// corner multigrid (k_mg.cu)
+void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, double *enew, const double *ec);
+void launch_wave_chain(Ctx *c, WaveArgs a, int cls, double bytes);
+cudaError_t wave_init();
+void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e);
+void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew, const double *b, double *rho,
+                         double *part);
+cudaError_t setup_mg_tiles(Ctx *c);
 
 // profiling helpers
 struct ProfScope {
