@@ -174,9 +174,11 @@ static void launch_mii(Ctx *c, const double *v, double *z, bool scaled)
 {
     WaveArgs a{};
     a.nl = c->n - 1; a.pv = c->P; a.pc = c->P; a.ioff = c->n; a.joff = c->n;
-    a.q = v; a.s = scaled ? c->cd : nullptr; a.ca = c->ca; a.cn = c->cn; a.z = z;
+    a.q = v; a.z = z; a.cd = c->cd;
+    if (scaled) { a.ca = c->ya; a.cn = c->yn; }   // D z = v + aE z_E + aN z_N (y-form)
+    else { a.ca = c->ca; a.cn = c->cn; }          // z = (D v)/D + ca z_E + cn z_N (z-form)
     const double nn = (double)a.nl * a.nl;
-    launch_wave_chain(c, a, 1, nn * (scaled ? 40.0 : 32.0));
+    launch_wave_chain(c, a, c->N + 1, c->N + 1, scaled, 1, nn * (scaled ? 40.0 : 32.0));
 }
 
 // z = M^{-1} v (eq:2D blocks by block back-substitution I -> Y -> X -> C).
@@ -312,19 +314,21 @@ static spp_status alloc_all(Ctx *c)
     c->P = round_up(N + 1, 16);
     c->G = (size_t)(N + 1) * c->P;
     const size_t G = c->G;
-    CK(c, cudaMalloc(&c->coef_block, sizeof(double) * (6 * G + 2 * (N + 1))));
-    CK(c, cudaMemsetAsync(c->coef_block, 0, sizeof(double) * (6 * G + 2 * (N + 1)), c->st));
+    // kTmaSlack: the sheared TMA boxes of k_wave may read a few dozen elements past the last row
+    CK(c, cudaMalloc(&c->coef_block, sizeof(double) * (8 * G + 2 * (N + 1) + kTmaSlack)));
+    CK(c, cudaMemsetAsync(c->coef_block, 0, sizeof(double) * (8 * G + 2 * (N + 1) + kTmaSlack), c->st));
     c->aE = c->coef_block; c->aN = c->aE + G; c->rr = c->aN + G;
     c->ca = c->rr + G; c->cn = c->ca + G; c->cd = c->cn + G;
-    c->aW = c->cd + G; c->aS = c->aW + (N + 1);
+    c->ya = c->cd + G; c->yn = c->ya + G;
+    c->aW = c->yn + G; c->aS = c->aW + (N + 1);
     const size_t per = (size_t)(n - 1) * n;
     CK(c, cudaMalloc(&c->fac, sizeof(double) * (8 * per + 4 * (size_t)n)));
     c->tX = c->fac + 8 * per; c->tY = c->tX + n; c->kapX = c->tY + n; c->kapY = c->kapX + n;
     const size_t cb = std::max<size_t>(3 * (size_t)m * m, 2 * per);
     CK(c, cudaMalloc(&c->cbuf, sizeof(double) * cb));
     // Krylov work vectors
-    CK(c, cudaMalloc(&c->w, sizeof(double) * 4 * G));
-    CK(c, cudaMemsetAsync(c->w, 0, sizeof(double) * 4 * G, c->st));
+    CK(c, cudaMalloc(&c->w, sizeof(double) * (4 * G + kTmaSlack)));
+    CK(c, cudaMemsetAsync(c->w, 0, sizeof(double) * (4 * G + kTmaSlack), c->st));
     c->F = c->w + G; c->U = c->F + G; c->T1 = c->U + G;
     const int maxit = c->opt.max_iters;
     CK(c, cudaMalloc(&c->part, sizeof(double) * (size_t)(std::max(maxit, kMaxLevels) + 8) * kRedBlocks));
@@ -354,6 +358,7 @@ static spp_status alloc_all(Ctx *c)
         tot += 5 * Lv.elems + 4 * (size_t)(Lv.n + 2) + (l > 0 ? 6 * Lv.elems : 0);
     }
     tot += 3 * c->lev[0].elems;   // Zc, Zc2, Bc
+    tot += kTmaSlack;
     CK(c, cudaMalloc(&c->mg_block, sizeof(double) * tot));
     CK(c, cudaMemsetAsync(c->mg_block, 0, sizeof(double) * tot, c->st));
     double *p = c->mg_block;
@@ -365,11 +370,11 @@ static spp_status alloc_all(Ctx *c)
         if (l > 0) {
             Lv.own = p;
             double *aE = p; p += Lv.elems; double *aN = p; p += Lv.elems; double *rr = p; p += Lv.elems;
-            double *ca = p; p += Lv.elems; double *cn = p; p += Lv.elems; double *cd = p; p += Lv.elems;
-            Lv.aE = aE; Lv.aN = aN; Lv.rr = rr; Lv.ca = ca; Lv.cn = cn; Lv.cd = cd;
+            double *ya = p; p += Lv.elems; double *yn = p; p += Lv.elems; double *cd = p; p += Lv.elems;
+            Lv.aE = aE; Lv.aN = aN; Lv.rr = rr; Lv.ya = ya; Lv.yn = yn; Lv.cd = cd;
             Lv.cpitch = Lv.pitch;
         } else {
-            Lv.aE = c->aE; Lv.aN = c->aN; Lv.rr = c->rr; Lv.ca = c->ca; Lv.cn = c->cn; Lv.cd = c->cd;
+            Lv.aE = c->aE; Lv.aN = c->aN; Lv.rr = c->rr; Lv.ya = c->ya; Lv.yn = c->yn; Lv.cd = c->cd;
             Lv.cpitch = c->P;
         }
     }
@@ -384,17 +389,17 @@ static cudaError_t ensure_vectors(Ctx *c, int k)
     // V[0..k], Z[0..k-1]
     while ((int)c->V.size() <= k) {
         double *p = nullptr;
-        cudaError_t e = cudaMalloc(&p, sizeof(double) * c->G);
+        cudaError_t e = cudaMalloc(&p, sizeof(double) * (c->G + kTmaSlack));
         if (e != cudaSuccess) return e;
-        e = cudaMemsetAsync(p, 0, sizeof(double) * c->G, c->st);
+        e = cudaMemsetAsync(p, 0, sizeof(double) * (c->G + kTmaSlack), c->st);
         if (e != cudaSuccess) return e;
         c->V.push_back(p);
     }
     while ((int)c->Z.size() < k) {
         double *p = nullptr;
-        cudaError_t e = cudaMalloc(&p, sizeof(double) * c->G);
+        cudaError_t e = cudaMalloc(&p, sizeof(double) * (c->G + kTmaSlack));
         if (e != cudaSuccess) return e;
-        e = cudaMemsetAsync(p, 0, sizeof(double) * c->G, c->st);
+        e = cudaMemsetAsync(p, 0, sizeof(double) * (c->G + kTmaSlack), c->st);
         if (e != cudaSuccess) return e;
         c->Z.push_back(p);
     }
@@ -425,12 +430,16 @@ static spp_status do_setup_2d(Ctx *c, const double *c1, const double *c2, const 
     Level &L0 = c->lev[0];
     k_level0_1d<<<1, 256, 0, c->st>>>(N, c->hx, c->Hx, c->hy, c->Hy, c->aW, c->aS, L0.aW, L0.aS, L0.hb, L0.kb);
     c->launches += 4;
+    launch_ycoef(c, m, c->P, c->aE, c->aN, c->cd, c->ya, c->yn);
     for (int l = 1; l < c->L; ++l) {
         Level &Lv = c->lev[l];
+        // (k_coef_level writes aE/D, aN/D into ya, yn; launch_ycoef then replaces them by the
+        // y-form couplings aE/D_E, aN/D_N once the whole cd of the level exists)
         k_coef_level<<<nblk((long)Lv.n * Lv.n), 256, 0, c->st>>>(N, Lv.n, 1 << l, Lv.pitch, c->eps, c->hx, c->Hx,
             c->hy, c->Hy, d1, d2, d3, Lv.aW, Lv.aS, Lv.hb, Lv.kb, (double *)Lv.aE, (double *)Lv.aN,
-            (double *)Lv.rr, (double *)Lv.ca, (double *)Lv.cn, (double *)Lv.cd);
+            (double *)Lv.rr, (double *)Lv.ya, (double *)Lv.yn, (double *)Lv.cd);
         c->launches++;
+        launch_ycoef(c, Lv.n, Lv.pitch, Lv.aE, Lv.aN, Lv.cd, (double *)Lv.ya, (double *)Lv.yn);
     }
     int hbad = 0;
     CK(c, cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
@@ -671,6 +680,7 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
             c->launches++;
         }
     }
+    if (c->sticky != cudaSuccess) { const cudaError_t se = c->sticky; c->sticky = cudaSuccess; CK(c, se); }
     CK(c, cudaEventRecord(e1, c->st));
     // output
     if (u) {
@@ -844,6 +854,7 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
     }
     CK(c, cudaStreamSynchronize(c->st));
     CK(c, cudaGetLastError());
+    if (c->sticky != cudaSuccess) { const cudaError_t se = c->sticky; c->sticky = cudaSuccess; CK(c, se); }
     (void)G;
     return SPP_OK;
 }

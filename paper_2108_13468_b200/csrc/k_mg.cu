@@ -4,47 +4,70 @@
 // (P:1276-1280), and the outer stationary-iteration update with the FE-rescaled corner norm
 // (reading R6).
 //
-// Downstream sweep (K3/K4 "wave", DESIGN.md "Corner GS" / "M_II"): on a rectangle of nodes,
-//     z(i,j) = s(i,j) q(i,j) + ca(i,j) z(i+1,j) + cn(i,j) z(i,j+1),   j descending, i descending,
-// with zero inflow beyond the top / right edge.  One GS sweep of the corner multigrid is this
-// recurrence with q = b, s = 1/D from zero, or with q = g = (b + aW e_old(i-1,j) + aS
-// e_old(i,j-1)) / D, s = 1 (k_gs_prep, fused with the prolongation e_old = e + P e_c); M_II is
-// q = v (s = 1/D unweighted, 1 Jacobi mode, reading R11) on region I.
-// Schedule: one warp per 32-row strip, one lane per row, lane t one column behind lane t-1 (the
-// North value arrives by __shfl_up_sync, the East value is the lane's own previous result).
-// Operands are staged into padded shared memory by coalesced cp.async copies of 16-column row
-// segments: each row's segment is pre-skewed by its lane offset, so at local step s0+k every lane
-// reads band column k (conflict-free, row stride 17 doubles), and the results are written back
-// into the band and stored as coalesced row segments.  A 3-slot ring keeps two chunks in flight.
-// Warps of a CTA are chained through a shared-memory edge ring.  Tiles of a level run in
-// parallel, each recomputing a certified halo of `halo_y` rows above and `halo_x` columns right of
-// its output tile from zero inflow (|error| <= rho^min(halo) max|z|,
-// rho = max (aE+aN)/D < 1 per level, halo with rho^halo <= 1e-17), so the result equals the
-// sequential sweep to below fp64 rounding.  Without a certified halo (M_II: no influence decay in
-// region I at small eps, SURVEY [chk-9]) the row strips are chained top-to-bottom across CTAs
-// through global memory (cooperative launch), which is the sequential sweep.
+// Downstream sweep (K3/K4 "wave", DESIGN.md "Corner GS" / "M_II").  The GS sweep
+//     D z(i,j) = q(i,j) + aE z(i+1,j) + aN z(i,j+1),   j descending, i descending,
+// with zero inflow beyond the top / right edge, runs in one of two forms:
+//   YFORM: y = D z obeys  y = q + ya y(i+1,j) + yn y(i,j+1),  ya = aE/D_E, yn = aN/D_N, and
+//          z = y / D is formed when the result is written back (corner MG levels; M_II in
+//          unweighted mode);
+//   z-form: z = q + ca z(i+1,j) + cn z(i,j+1), ca = aE/D, cn = aN/D, where the caller's q is
+//          already divided by D (M_II in Jacobi mode: the preconditioner input is D v, R11).
+// One corner GS sweep is q = b from zero, or q = b + aW e'(i-1,j) + aS e'(i,j-1) (k_gs_prep,
+// fused with the prolongation e' = e + P e_c).
+//
+// Schedule: one warp per 32-row strip, one lane per row, lane t two columns behind lane t-1 (the
+// North value, computed by lane t-1 two steps earlier, arrives by __shfl_up_sync; the East value
+// is the lane's own previous result).  With that 2-column skew the band of operands a warp needs
+// for 16 consecutive steps is a rectangle in the *sheared* view of an array, element (X, R) at
+// address base + R (pitch-2) + X, i.e. row R shifted right by 2R columns.  Each array gets one
+// such overlapping 2D TMA tensor map (the row stride (pitch-2)*8 B is a multiple of 16 B), and a
+// warp stages a 32-row x 16-column box per array per chunk with one cp.async.bulk.tensor
+// (128B swizzle, mbarrier completion) into a 3-slot ring -- two chunks in flight, plus a TMA L2
+// prefetch 4 chunks ahead.  At local step k every lane reads box column 15-k of its row.  Results
+// go to a padded 2-slot band and are written back as coalesced row segments (the write-back of
+// chunk c-1 is interleaved with the steps of chunk c).  Warps of a CTA are chained through a
+// shared-memory edge ring.  Tiles of a level run in parallel, each recomputing a certified halo of
+// `halo_y` rows above and `halo_x` columns right of its output tile from zero inflow (DESIGN.md
+// "Certified halos": |error| <= rho^min(halo) max|y|, rho = max (ya+yn) < 1 per level, halo with
+// rho^halo <= 1e-17), so the result equals the sequential sweep to below fp64 rounding.  Without a
+// certified halo (M_II: no influence decay in region I at small eps, SURVEY [chk-9]) the row
+// strips are chained top-to-bottom across CTAs through global memory (cooperative launch), which
+// is the sequential sweep.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <tuple>
+#include <type_traits>
 
 #include "kernels.cuh"
 
 namespace spp {
 
-constexpr int WCW = 16;          // columns per chunk
-constexpr int WPAD = WCW + 1;    // padded shared-memory row stride (doubles)
-constexpr int WNS = 3;           // ring slots (one consumed, two in flight)
-constexpr int WMAXW = 4;         // warps per CTA (max; 3-slot rings of 4 arrays fill 209 KB)
-constexpr int WEB = 64;          // edge ring (columns)
+constexpr int WCW = 16;          // columns per chunk (box width, 128 bytes)
+constexpr int WNS = 3;           // staging ring slots (one consumed, two in flight)
+constexpr int WNA = 3;           // staged arrays: q, a1, a2
+constexpr int WBOX = 32 * WCW;   // doubles per box
+constexpr int WSLOT = WNA * WBOX;             // doubles per staging slot (12 KB)
+constexpr int WZP = WCW + 1;                  // padded result band row stride
+constexpr int WZB = 32 * WZP;                 // doubles per result band
+constexpr int WCDB = 16 * 32;                 // doubles per write-back scale band (1/D of one chunk)
+constexpr int WWARP = (WNS * WSLOT + 2 * WZB + 2 * WCDB + 127) / 128 * 128;   // doubles per warp (1 KB multiple)
+constexpr int WMAXW = 4;         // warps per CTA (max)
+constexpr int WEB = 128;         // edge ring (columns)
 constexpr int WPF = 4;           // L2 prefetch distance (chunks)
+constexpr int WLAG = 2;          // lane-to-lane skew (columns)
+
+struct WaveMaps { CUtensorMap q, a1, a2, cd; };   // cd: L2 prefetch only
 
 __device__ __forceinline__ void cp_async8(double *dst, const double *src, bool valid)
 {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    const int n = valid ? 8 : 0;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ int ld_acquire(const int *p)
 {
@@ -52,17 +75,34 @@ __device__ __forceinline__ int ld_acquire(const int *p)
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-
-template <bool HAS_S, bool CHAIN>
-__global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a)
+__device__ __forceinline__ void tma_load(unsigned dst, const CUtensorMap *tm, int x, int y, unsigned bar)
 {
-    constexpr int NA = HAS_S ? 4 : 3;                   // staged arrays: q, ca, cn (, s)
-    constexpr int SLOT = NA * 32 * WPAD;                // doubles per ring slot
-    extern __shared__ double smem[];
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(dst), "l"(tm), "r"(x), "r"(y), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap *tm, int x, int y)
+{
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(tm), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity)
+{
+    asm volatile("{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W%=;\n}"
+                 ::"r"(bar), "r"(parity) : "memory");
+}
+
+template <bool YFORM, bool CHAIN>
+__global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a, const __grid_constant__ WaveMaps m)
+{
+    extern __shared__ double smem_raw[];
     __shared__ double edge[WMAXW][WEB];
     __shared__ int prod[WMAXW], cons[WMAXW];
+    __shared__ __align__(8) unsigned long long bars[WMAXW][WNS];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
     if (threadIdx.x < WMAXW) { prod[threadIdx.x] = 0; cons[threadIdx.x] = 0; }
+    if (lane == 0)
+        for (int s = 0; s < WNS; ++s)
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&bars[w][s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     const int nl = a.nl;
     // tile (CHAIN: blockIdx.y = row strip block, full width)
@@ -71,105 +111,176 @@ __global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a)
     const int top = min(nl, out_top + a.halo_y);
     const int out_right = nl - (int)blockIdx.x * a.cols_out;
     const int out_left = max(1, out_right - a.cols_out + 1);
-    const int right = min(nl, out_right + a.halo_x);
+    // The TMA box origin X0 = right + ioff + 2(wtop + joff) - 15 - 16c must be even (16-byte
+    // aligned) for the swizzled box, so (right + ioff) must be odd: otherwise one more column is
+    // swept -- a genuine halo column inside the level, or the zero ghost column nl+1 where q = 0
+    // and the sweep stays exactly 0.
+    const int right0 = min(nl, out_right + a.halo_x);
+    const int right = ((right0 + a.ioff) & 1) ? right0 : right0 + 1;
     const int ncols = right - out_left + 1;
     const int wtop = top - 32 * w;
     if (wtop < out_bot) return;                         // no rows for this warp
     const int nwa = min(W, (top - out_bot) / 32 + 1);
-    const int row = wtop - lane;
-    const bool rvalid = row >= out_bot;
     const bool has_consumer = w + 1 < nwa;
     const bool chain_in = CHAIN && w == 0 && blockIdx.y > 0;
     const bool chain_out = CHAIN && w == nwa - 1 && (int)blockIdx.y + 1 < (int)gridDim.y;
-    const int nsteps = ncols + 31;
+    const int nsteps = ncols + WLAG * 31;
     const int nch = (nsteps + WCW - 1) / WCW;
-    double *ring = smem + (size_t)w * WNS * SLOT;
-    const double *base[4] = {a.q, a.ca, a.cn, a.s};
-    const long pitch[4] = {a.pv, a.pc, a.pc, a.pc};
-
-    // stage chunk c: element (t, k) of the band <- (row wtop - t, column right - (16c - t + k))
-    auto issue = [&](int c) {
-        double *sl = ring + (size_t)(c % WNS) * SLOT;
-#pragma unroll
-        for (int e = 0; e < WCW; ++e) {
-            const int p = e * 32 + lane, t = p / WCW, k = p % WCW;
-            const int r = wtop - t, qq = c * WCW - t + k, col = right - qq;
-            const bool ok = r >= out_bot && qq >= 0 && qq < ncols;
-            const long rj = (long)(ok ? r : out_bot) + a.joff, ci = (long)(ok ? col : out_left) + a.ioff;
-#pragma unroll
-            for (int ar = 0; ar < NA; ++ar)
-                cp_async8(sl + (ar * 32 + t) * WPAD + k, base[ar] + rj * pitch[ar] + ci, ok);
-        }
-        cp_commit();
+    // 128B-swizzled TMA boxes need 1 KB aligned shared memory (pointer arithmetic on the shared
+    // array keeps the accesses in the shared state space: LDS/STS, not generic LD/ST)
+    double *smem = smem_raw + (((1024u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u) >> 3);
+    double *ring = smem + (size_t)w * WWARP;
+    double *zband = ring + WNS * WSLOT;
+    double *cdband = zband + 2 * WZB;                   // [chunk & 1][e][lane]: 1/D of the write-back elements
+    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+    // box origin in the sheared view: X = col + 2R (array coordinates), rows wtop-31..wtop
+    const int Xb = right + a.ioff + WLAG * (wtop + a.joff) - (WCW - 1);   // X0 of chunk 0
+    const int R0 = wtop - 31 + a.joff;
+    auto issue = [&](int c) {                           // lane 0 only
+        const int s = c % WNS;
+        const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[w][s]);
+        const unsigned dst = ring_s + (unsigned)(s * WSLOT * 8);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(WSLOT * 8) : "memory");
+        const int x = Xb - c * WCW;
+        tma_load(dst, &m.q, x, R0, bar);
+        tma_load(dst + WBOX * 8, &m.a1, x, R0, bar);
+        tma_load(dst + 2 * WBOX * 8, &m.a2, x, R0, bar);
     };
-    issue(0);
-    if (nch > 1) issue(1); else cp_commit();
-    double zprev = 0.0;
-    const int drow = wtop - lane;                       // row written by this lane in the write-back
-    (void)drow;
-    for (int c = 0; c < nch; ++c) {
-        if (c + 2 < nch) issue(c + 2); else cp_commit();
-        {   // L2 prefetch WPF chunks ahead: one address per row segment
-            const int cp = c + WPF;
-            if (cp < nch && lane < 32 && rvalid) {
-                const int qq = cp * WCW - lane + WCW / 2, col = right - qq;
-                if (qq >= 0 && qq < ncols) {
-                    const long rj = (long)row + a.joff, ci = (long)col + a.ioff;
+    if (lane == 0) {
+        issue(0);
+        if (nch > 1) issue(1);
+    }
+    // this lane's row and swizzled box offsets: element (row 31-t, column x') lives at byte
+    // (31-t)*128 + ((x'/2) ^ ((31-t)&7))*16 + (x'&1)*8
+    const int br = 31 - lane;
+    const int rowoff = br * WCW;                         // doubles
+    const int sw = br & 7;
+    const int row = wtop - lane;
+    const bool rvalid = row >= out_bot;
+    // write-back mapping: element e -> band row t = 2e + lane/16, step k = 15 - lane%16
+    const int th = lane >> 4, kk = lane & 15;
+    const int tmax = wtop - out_bot;
+    const int pv = (int)a.pv, pc = (int)a.pc;
+    // offset of (row wtop - th, col right - 15 + kk + 2 th) for chunk 0, element 0; per element
+    // e: row -2, col +4; per chunk: col -16
+    const int wv0 = (wtop - th + a.joff) * pv + right - (WCW - 1) + kk + WLAG * th + a.ioff;
+    const int wc0 = (wtop - th + a.joff) * pc + right - (WCW - 1) + kk + WLAG * th + a.ioff;
+    const int dwv = 2 * WLAG - 2 * pv, dwc = 2 * WLAG - 2 * pc;
+    auto wb = [&](int c, int e, double cdv) {
+        const double *zb = zband + (size_t)(c & 1) * WZB;
+        const int t = 2 * e + th, k = WCW - 1 - kk, idx = c * WCW + k - WLAG * t;
+        const int col = right - idx;
+        if (t <= tmax && wtop - t <= out_top && idx >= 0 && idx < ncols && col <= out_right) {
+            const double y = zb[t * WZP + k];
+            a.z[wv0 + e * dwv - c * WCW] = YFORM ? cdv * y : y;
+        }
+    };
+    // 1/D of the write-back elements of chunk c, staged by cp.async one chunk ahead of use
+    auto stage_cd = [&](int c) {
+        if (!YFORM) return;
+        double *cb = cdband + (size_t)(c & 1) * WCDB;
 #pragma unroll
-                    for (int ar = 0; ar < NA; ++ar)
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(base[ar] + rj * pitch[ar] + ci));
-                }
+        for (int e = 0; e < 16; ++e) {
+            const int t = 2 * e + th, k = WCW - 1 - kk, idx = c * WCW + k - WLAG * t;
+            const bool ok = t <= tmax && idx >= 0 && idx < ncols;
+            cp_async8(cb + e * 32 + lane, a.cd + (ok ? wc0 + e * dwc - c * WCW : 0), ok);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    const bool rows_all = wtop - 31 >= out_bot;         // all 32 rows of the warp are swept rows
+    const bool rows_out_all = rows_all && wtop <= out_top;   // ... and output rows
+    double z1 = 0.0, z2 = 0.0;                          // own results of the last two steps
+    for (int c = 0; c < nch; ++c) {
+        if (lane == 0) {
+            if (c + 2 < nch) issue(c + 2);
+            if (c + WPF < nch) {
+                const int x = Xb - (c + WPF) * WCW;
+                tma_prefetch(&m.q, x, R0); tma_prefetch(&m.a1, x, R0); tma_prefetch(&m.a2, x, R0);
+                if (YFORM) tma_prefetch(&m.cd, x, R0);
             }
         }
-        cp_wait<2>();
-        __syncwarp();
-        double *sl = ring + (size_t)(c % WNS) * SLOT;
-        // North inflow of lane 0 for the columns of this chunk.  Every wait loop below is executed
-        // by all 32 lanes (warp-uniform condition): a lane-divergent spin leaves the warp diverged
-        // and sends the shuffles of the step loop down the slow emulation path.
-        double ein[WCW];
-#pragma unroll
-        for (int k = 0; k < WCW; ++k) ein[k] = 0.0;
+        // interior chunks (warp-uniform test): every lane's element valid, every written-back
+        // element an output node -- no per-element predicates
+        const bool fast = rows_all && c * WCW - WLAG * 31 >= 0 && c * WCW + WCW - 1 < ncols &&
+                          (c == 0 || (rows_out_all && (c - 1) * WCW - WLAG * 31 >= right - out_right));
+        stage_cd(c);
+        if (YFORM) asm volatile("cp.async.wait_group 1;" ::: "memory");   // chunk c-1's 1/D band
+        const double *cdb = cdband + (size_t)((c + 1) & 1) * WCDB;
+        // North inflow of lane 0 for the columns of this chunk (all wait loops warp-uniform: a
+        // lane-divergent spin sends the shuffles below down the slow emulation path)
         const int need = min(ncols, c * WCW + WCW);
+        const double *ein_src = nullptr;                // inflow row (edge ring) or null = 0
+        double ein_g[WCW];
         if (w > 0) {
             while (*((volatile int *)&prod[w - 1]) < need) { }
             __threadfence_block();
-#pragma unroll
-            for (int k = 0; k < WCW; ++k) ein[k] = *((volatile double *)&edge[w - 1][(c * WCW + k) & (WEB - 1)]);
-            __syncwarp();
-            if (lane == 0) *((volatile int *)&cons[w]) = need;
+            ein_src = &edge[w - 1][0];
         } else if (chain_in) {
             while (ld_acquire(a.chain_flags + blockIdx.y - 1) < need) { }
             const double *src = a.chain_buf + (long)(blockIdx.y - 1) * a.chain_ld;
 #pragma unroll
-            for (int k = 0; k < WCW; ++k) ein[k] = (c * WCW + k < ncols) ? __ldcg(src + c * WCW + k) : 0.0;
+            for (int k = 0; k < WCW; ++k) ein_g[k] = (c * WCW + k < ncols) ? __ldcg(src + c * WCW + k) : 0.0;
         }
-        // back-pressure on the edge ring
-        if (has_consumer) {
-            const int lim = c * WCW + WCW - 31 - WEB;
+        if (has_consumer) {                             // back-pressure on the edge ring
+            const int lim = c * WCW + WCW - WLAG * 31 - WEB;
             if (lim > 0) { while (*((volatile int *)&cons[w + 1]) < lim) { } }
         }
+        mbar_wait((unsigned)__cvta_generic_to_shared(&bars[w][c % WNS]), (unsigned)((c / WNS) & 1));
         __syncwarp();
-        double *qb = sl + lane * WPAD, *ab = sl + (32 + lane) * WPAD, *nb = sl + (64 + lane) * WPAD;
-        const double *sb = sl + (96 + lane) * WPAD;
+        const double *sq = ring + (size_t)(c % WNS) * WSLOT;
+        double *zb = zband + (size_t)(c & 1) * WZB;
+        const double *zbp = zband + (size_t)((c + 1) & 1) * WZB;   // chunk c-1's results
+        // Steps in two groups of 8: all shared-memory operands of a group are loaded before its
+        // dependent FMA chain runs (stores to the result band would otherwise pin every load
+        // behind the previous step's store), results are stored after the group.
+        auto group = [&](auto fast_tag, auto g_tag) {
+            constexpr bool F = decltype(fast_tag)::value;
+            constexpr int G = decltype(g_tag)::value;
+            double Q[8], A1[8], A2[8], E[8], YB[8];
 #pragma unroll
-        for (int k = 0; k < WCW; ++k) {
-            const int qq = c * WCW + k - lane;
-            double zN = __shfl_up_sync(0xffffffffu, zprev, 1);
-            if (lane == 0) zN = ein[k];
-            const double sq = HAS_S ? sb[k] * qb[k] : qb[k];
-            const double t = fma(ab[k], zprev, sq);
-            double z = fma(nb[k], zN, t);
-            const bool ok = rvalid && qq >= 0 && qq < ncols;
-            z = ok ? z : 0.0;
-            qb[k] = z;                                  // result in place of q
-            if (lane == 31 && ok) {
-                if (has_consumer) edge[w][qq & (WEB - 1)] = z;
-                if (chain_out) __stcg(a.chain_buf + (long)blockIdx.y * a.chain_ld + qq, z);
+            for (int u = 0; u < 8; ++u) {
+                const int k = 8 * G + u;
+                const int xo = rowoff + ((((WCW - 1 - k) >> 1) ^ sw) << 1) + ((WCW - 1 - k) & 1);
+                Q[u] = sq[xo]; A1[u] = sq[WBOX + xo]; A2[u] = sq[2 * WBOX + xo];
+                E[u] = ein_src ? ein_src[(c * WCW + k) & (WEB - 1)] : (chain_in ? ein_g[k] : 0.0);
+                if (c > 0) YB[u] = zbp[(2 * k + th) * WZP + WCW - 1 - kk];
             }
-            zprev = z;
-        }
-        const int done = min(ncols, max(0, c * WCW + WCW - 31));
+            if (G == 1 && w > 0 && lane == 0) *((volatile int *)&cons[w]) = need;
+            double Z[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = 8 * G + u;
+                double zN = __shfl_up_sync(0xffffffffu, z2, 1);
+                if (lane == 0) zN = E[u];
+                double z = fma(A2[u], zN, fma(A1[u], z1, Q[u]));
+                if (!F) {
+                    const int idx = c * WCW + k - WLAG * lane;
+                    z = (rvalid && idx >= 0 && idx < ncols) ? z : 0.0;
+                }
+                Z[u] = z;
+                z2 = z1; z1 = z;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = 8 * G + u;
+                const int idx = c * WCW + k - WLAG * lane;
+                zb[lane * WZP + k] = Z[u];
+                if (lane == 31 && idx >= 0 && idx < ncols) {
+                    if (has_consumer) edge[w][idx & (WEB - 1)] = Z[u];
+                    if (CHAIN && chain_out) __stcg(a.chain_buf + (long)blockIdx.y * a.chain_ld + idx, Z[u]);
+                }
+                if (c > 0) {                            // interleaved write-back of chunk c-1
+                    const double cdv = YFORM ? cdb[k * 32 + lane] : 1.0;
+                    if (F) a.z[wv0 + k * dwv - (c - 1) * WCW] = YFORM ? cdv * YB[u] : YB[u];
+                    else wb(c - 1, k, cdv);
+                }
+            }
+        };
+        if (fast) { group(std::true_type{}, std::integral_constant<int, 0>{}); group(std::true_type{}, std::integral_constant<int, 1>{}); }
+        else { group(std::false_type{}, std::integral_constant<int, 0>{}); group(std::false_type{}, std::integral_constant<int, 1>{}); }
+        const int done = min(ncols, max(0, c * WCW + WCW - WLAG * 31));
         if (lane == 31) {
             if (has_consumer) {
                 __threadfence_block();
@@ -178,48 +289,100 @@ __global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a)
             if (chain_out) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.chain_flags + blockIdx.y), "r"(done) : "memory");
         }
         __syncwarp();
-        // coalesced write-back of the output rows: element (t, k) -> (wtop - t, right - (16c - t + k))
-#pragma unroll
-        for (int e = 0; e < WCW; ++e) {
-            const int p = e * 32 + lane, t = p / WCW, k = p % WCW;
-            const int r = wtop - t, qq = c * WCW - t + k, col = right - qq;
-            if (r >= out_bot && r <= out_top && qq >= 0 && qq < ncols && col <= out_right)
-                a.z[(long)(r + a.joff) * a.pv + col + a.ioff] = sl[t * WPAD + k];
-        }
-        __syncwarp();
     }
-    cp_wait<0>();
+    {   // write-back of the last chunk
+        const int c = nch - 1;
+        if (YFORM) asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        const double *cdb = cdband + (size_t)(c & 1) * WCDB;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) wb(c, e, YFORM ? cdb[e * 32 + lane] : 1.0);
+    }
 }
 
-static size_t wave_smem(int warps, bool has_s)
+static size_t wave_smem(int warps) { return sizeof(double) * (size_t)warps * WWARP + 1024; }
+
+// SPP_DEBUG_SYNC=1: synchronise and report after every launch of this file (debugging aid)
+static void dbg_sync(Ctx *c, const char *what)
 {
-    return sizeof(double) * (size_t)warps * WNS * (has_s ? 4 : 3) * 32 * WPAD;
+    static int on = -1;
+    if (on < 0) { const char *e = getenv("SPP_DEBUG_SYNC"); on = (e && e[0] == '1') ? 1 : 0; }
+    if (!on) return;
+    cudaError_t e = cudaStreamSynchronize(c->st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    fprintf(stderr, "[spp-debug] %s: %s\n", what, cudaGetErrorString(e));
 }
+
+// ---------------------------------------------------------------------------------- tensor maps
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
 cudaError_t wave_init()
 {
-    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wave_smem(WMAXW, true)));
-    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wave_smem(WMAXW, false)));
-    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wave_smem(WMAXW, true)));
-    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wave_smem(WMAXW, false)));
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        SPP_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&g_encode, cudaEnableDefault, &q));
+        if (!g_encode || q != cudaDriverEntryPointSuccess) return cudaErrorNotSupported;
+    }
+    const int sm = (int)wave_smem(WMAXW);
+    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     return cudaSuccess;
 }
 
-// Tiled (certified halo) or single-tile sweep of a level-shaped square [1, nl]^2.
-void launch_wave(Ctx *c, WaveArgs a, int warps, int cls, double bytes)
+// Sheared view of a padded array of `rows` rows x `pitch` doubles: element (X, R) at
+// base + R (pitch - 2) + X; box 16 x 32, 128B swizzle.  Cached per (pointer, pitch, rows).
+static const CUtensorMap *sheared_map(Ctx *c, const double *base, long pitch, long rows)
 {
-    const bool hs = a.s != nullptr;
+    auto key = std::make_tuple((const void *)base, pitch, rows);
+    auto it = c->tmaps.find(key);
+    if (it != c->tmaps.end()) return &it->second;
+    CUtensorMap tm;
+    cuuint64_t dim[2] = {(cuuint64_t)(pitch + WLAG * rows + 64), (cuuint64_t)rows};
+    cuuint64_t str[1] = {(cuuint64_t)(pitch - WLAG) * sizeof(double)};
+    cuuint32_t box[2] = {WCW, 32}, es[2] = {1, 1};
+    CUresult rc = g_encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)base, dim, str, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) return nullptr;
+    return &(c->tmaps[key] = tm);
+}
+
+static bool wave_maps(Ctx *c, const WaveArgs &a, long rows_v, long rows_c, WaveMaps *m)
+{
+    const CUtensorMap *q = sheared_map(c, a.q, a.pv, rows_v);
+    const CUtensorMap *x = sheared_map(c, a.ca, a.pc, rows_c);
+    const CUtensorMap *y = sheared_map(c, a.cn, a.pc, rows_c);
+    const CUtensorMap *d = sheared_map(c, a.cd, a.pc, rows_c);
+    if (!q || !x || !y || !d) return false;
+    m->q = *q; m->a1 = *x; m->a2 = *y; m->cd = *d;
+    return true;
+}
+
+// Tiled (certified halo) or single-tile sweep of a level-shaped square [1, nl]^2 of an array with
+// `rows` rows.
+void launch_wave(Ctx *c, WaveArgs a, long rows_v, long rows_c, int warps, bool yform, int cls, double bytes)
+{
+    WaveMaps m;
+    if (!wave_maps(c, a, rows_v, rows_c, &m)) { c->sticky = cudaErrorInvalidValue; return; }
+    static int dbg = -1;
+    if (dbg < 0) { const char *e = getenv("SPP_WAVE_DBG"); dbg = e ? atoi(e) : 0; }
+    a.dbg = dbg;
     const dim3 grid((a.nl + a.cols_out - 1) / a.cols_out, (a.nl + a.rows_out - 1) / a.rows_out);
-    const size_t sm = wave_smem(warps, hs);
+    const size_t sm = wave_smem(warps);
     ProfScope ps(c, cls, bytes);
-    if (hs) k_wave<true, false><<<grid, warps * 32, sm, c->st>>>(a);
-    else k_wave<false, false><<<grid, warps * 32, sm, c->st>>>(a);
+    if (yform) k_wave<true, false><<<grid, warps * 32, sm, c->st>>>(a, m);
+    else k_wave<false, false><<<grid, warps * 32, sm, c->st>>>(a, m);
     c->launches++;
+    dbg_sync(c, "k_wave tiled");
 }
 
 // Exact sweep: row strips of 32*W rows chained top-to-bottom across CTAs (cooperative launch).
-void launch_wave_chain(Ctx *c, WaveArgs a, int cls, double bytes)
+void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform, int cls, double bytes)
 {
+    WaveMaps m;
+    if (!wave_maps(c, a, rows_v, rows_c, &m)) { c->sticky = cudaErrorInvalidValue; return; }
     const int W = std::max(1, std::min(c->tune.sweep_warps, WMAXW));
     a.rows_out = 32 * W; a.halo_y = 0;
     a.cols_out = a.nl; a.halo_x = 0;
@@ -228,19 +391,18 @@ void launch_wave_chain(Ctx *c, WaveArgs a, int cls, double bytes)
     a.chain_buf = c->chain;
     a.chain_ld = c->chain_ld;
     cudaMemsetAsync(c->chain_flags, 0, sizeof(int) * (ncta + 1), c->st);
-    const bool hs = a.s != nullptr;
-    const size_t sm = wave_smem(W, hs);
-    void *args[] = {(void *)&a};
+    const size_t sm = wave_smem(W);
+    void *args[] = {(void *)&a, (void *)&m};
     ProfScope ps(c, cls, bytes);
-    if (hs) cudaLaunchCooperativeKernel((void *)k_wave<true, true>, dim3(1, ncta), dim3(32 * W), args, sm, c->st);
+    if (yform) cudaLaunchCooperativeKernel((void *)k_wave<true, true>, dim3(1, ncta), dim3(32 * W), args, sm, c->st);
     else cudaLaunchCooperativeKernel((void *)k_wave<false, true>, dim3(1, ncta), dim3(32 * W), args, sm, c->st);
     c->launches++;
+    dbg_sync(c, "k_wave chain");
 }
 
-// g = (b + aW e'(i-1,j) + aS e'(i,j-1)) / D with e' = e + P e_c (e_c may be null): the parallel
-// W/S part of a GS sweep from e', fused with the prolongation and coarse-grid correction
-// (P:1270-1275).  When ec != null, e is updated in place to e' (needed as the next sweep's
-// starting iterate is not: the post-smoothing result replaces it).
+// g = b + aW e'(i-1,j) + aS e'(i,j-1) with e' = e + P e_c (e_c may be null): the right-hand side
+// of the y-form recurrence of a GS sweep from e' (the parallel W/S part), fused with the
+// prolongation and coarse-grid correction; e' itself is never stored.
 __device__ __forceinline__ double interp_c(const double *ec, long Pc, int i, int j)
 {
     const int I0 = i >> 1, J0 = j >> 1;
@@ -252,8 +414,8 @@ __device__ __forceinline__ double interp_c(const double *ec, long Pc, int i, int
                    (ec[(long)(J0 + 1) * Pc + I0] + ec[(long)(J0 + 1) * Pc + I0 + 1]));
 }
 
-__global__ void __launch_bounds__(256) k_gs_prep(int nl, long pv, long pc, const double *__restrict__ e,
-    const double *__restrict__ ec, long pcv, const double *__restrict__ b, const double *__restrict__ cd,
+__global__ void __launch_bounds__(256) k_gs_prep(int nl, long pv, const double *__restrict__ e,
+    const double *__restrict__ ec, long pcv, const double *__restrict__ b,
     const double *__restrict__ aW, const double *__restrict__ aS, double *g)
 {
     const long tot = (long)nl * nl;
@@ -265,35 +427,37 @@ __global__ void __launch_bounds__(256) k_gs_prep(int nl, long pv, long pc, const
             ew += (i > 1) ? interp_c(ec, pcv, i - 1, j) : 0.0;
             es += (j > 1) ? interp_c(ec, pcv, i, j - 1) : 0.0;
         }
-        g[v] = cd[(long)j * pc + i] * ((b[v] + aW[i] * ew) + aS[j] * es);
+        g[v] = (b[v] + aW[i] * ew) + aS[j] * es;
     }
 }
 
 static inline int gblocks(long work) { long b = (work + 255) / 256; return (int)std::max(1L, std::min(b, 148L * 16)); }
 
-// One downstream GS sweep on level l: mode 0 from zero (e_new = wave(b, 1/D)); mode 1 from e_old
-// (+ P ec when ec != null): g = prep(e_old [+ P ec]), e_new = wave(g, 1).
+// One downstream GS sweep on level l (y-form): mode 0 from zero (q = b); mode 1 from e_old
+// (+ P ec when ec != null): q = prep(e_old [+ P ec]).
 void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, double *enew, const double *ec)
 {
     Level &L = c->lev[l];
     const double nn = (double)L.n * L.n;
     WaveArgs a{};
     a.nl = L.n; a.pv = L.pitch; a.pc = L.cpitch;
-    a.ca = L.ca; a.cn = L.cn; a.z = enew;
-    if (mode == 0) { a.q = b; a.s = L.cd; }
+    a.ca = L.ya; a.cn = L.yn; a.cd = L.cd; a.z = enew;
+    if (mode == 0) a.q = b;
     else {
         {
-            ProfScope ps(c, 5, nn * 32.0);
-            k_gs_prep<<<gblocks((long)L.n * L.n), 256, 0, c->st>>>(L.n, L.pitch, L.cpitch, eold, ec,
-                ec ? c->lev[l + 1].pitch : 0, b, L.cd, L.aW, L.aS, L.g);
+            ProfScope ps(c, 5, nn * 24.0);
+            k_gs_prep<<<gblocks((long)L.n * L.n), 256, 0, c->st>>>(L.n, L.pitch, eold, ec,
+                ec ? c->lev[l + 1].pitch : 0, b, L.aW, L.aS, L.g);
             c->launches++;
+            dbg_sync(c, "k_gs_prep");
         }
-        a.q = L.g; a.s = nullptr;
+        a.q = L.g;
     }
-    const double bytes = nn * (mode == 0 ? 40.0 : 32.0);
-    if (L.tile_warps == 0) { launch_wave_chain(c, a, 3, bytes); return; }
+    const double bytes = nn * 40.0;   // q, ya, yn, cd read; z written
+    const long rows_v = L.n + 2, rows_c = l == 0 ? c->N + 1 : L.n + 2;   // level 0 shares the global coefficients
+    if (L.tile_warps == 0) { launch_wave_chain(c, a, rows_v, rows_c, true, 3, bytes); return; }
     a.rows_out = L.tile_rows; a.cols_out = L.tile_cols; a.halo_y = L.halo_y; a.halo_x = L.halo_x;
-    launch_wave(c, a, L.tile_warps, 3, bytes);
+    launch_wave(c, a, rows_v, rows_c, L.tile_warps, true, 3, bytes);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -406,10 +570,12 @@ void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew,
 }
 
 // ------------------------------------------------------------------------------------------
-// Setup: rho_l = max over the level of (aE + aN) / D = ca + cn (the contraction factor of the
-// downstream recurrence that certifies the tile halos).  Partial maxima per block.
-// ------------------------------------------------------------------------------------------
-__global__ void k_level_rho(int nl, long pc, const double *ca, const double *cn, double *part)
+// Setup: rho_l = max over the level of (aE + aN) / D, the contraction factor of the downstream
+// recurrence in z-form (z = q/D + (aE/D) z_E + (aN/D) z_N).  The y-form sweep (y = D z) computes
+// the same z, so the truncation error of a zero-inflow halo of depth d is <= rho^d max|z|.
+// Couplings to the block boundary (i = nl East, j = nl North) multiply a zero inflow and are
+// excluded.  Partial maxima per block.
+__global__ void k_level_rho(int nl, long pc, const double *aE, const double *aN, const double *cd, double *part)
 {
     __shared__ double sm[32];
     double mx = 0.0;
@@ -417,7 +583,7 @@ __global__ void k_level_rho(int nl, long pc, const double *ca, const double *cn,
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
         const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
         const long q = (long)j * pc + i;
-        mx = fmax(mx, ca[q] + cn[q]);
+        mx = fmax(mx, ((i < nl ? aE[q] : 0.0) + (j < nl ? aN[q] : 0.0)) * cd[q]);
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
@@ -431,13 +597,32 @@ __global__ void k_level_rho(int nl, long pc, const double *ca, const double *cn,
     }
 }
 
+// ya = aE / D_E = aE(i,j) cd(i+1,j), yn = aN / D_N = aN(i,j) cd(i,j+1) on [1, nl]^2 (the ghost
+// ring of cd is zero, so the couplings to the block boundary vanish).
+__global__ void k_ycoef(int nl, long pc, const double *aE, const double *aN, const double *cd, double *ya, double *yn)
+{
+    const long tot = (long)nl * nl;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
+        const long q = (long)j * pc + i;
+        ya[q] = aE[q] * cd[q + 1];
+        yn[q] = aN[q] * cd[q + pc];
+    }
+}
+
+void launch_ycoef(Ctx *c, int nl, long pc, const double *aE, const double *aN, const double *cd, double *ya, double *yn)
+{
+    k_ycoef<<<gblocks((long)nl * nl), 256, 0, c->st>>>(nl, pc, aE, aN, cd, ya, yn);
+    c->launches++;
+}
+
 cudaError_t setup_mg_tiles(Ctx *c)
 {
     const Tune &T = c->tune;
     const int Wt = std::max(1, std::min(T.gs_warps, WMAXW));
     for (int l = 0; l < c->L; ++l) {
-        k_level_rho<<<kRedBlocks, kRedThreads, 0, c->st>>>(c->lev[l].n, c->lev[l].cpitch, c->lev[l].ca,
-                                                           c->lev[l].cn, c->part + (size_t)l * kRedBlocks);
+        k_level_rho<<<kRedBlocks, kRedThreads, 0, c->st>>>(c->lev[l].n, c->lev[l].cpitch, c->lev[l].aE,
+                                                           c->lev[l].aN, c->lev[l].cd, c->part + (size_t)l * kRedBlocks);
         c->launches++;
     }
     SPP_CUDA_TRY(cudaMemcpyAsync(c->hpin, c->part, sizeof(double) * kRedBlocks * c->L, cudaMemcpyDeviceToHost, c->st));

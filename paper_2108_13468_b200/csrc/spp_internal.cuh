@@ -9,7 +9,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cuda.h>
+
+#include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "spp.h"
@@ -20,6 +24,7 @@ constexpr int kMaxLevels = 24;
 constexpr int kWarp = 32;
 constexpr int kRedBlocks = 592;      // 4 x 148 SMs: fixed grid for deterministic reductions
 constexpr int kRedThreads = 256;
+constexpr long kTmaSlack = 1L << 16;     // doubles appended to grid allocations (TMA over-read)
 
 inline long round_up(long a, long b) { return (a + b - 1) / b * b; }
 
@@ -40,7 +45,7 @@ struct Level {
     long pitch = 0;                      // value pitch
     size_t elems = 0;
     const double *aE = nullptr, *aN = nullptr, *rr = nullptr;   // coefficients (coef pitch cpitch)
-    const double *ca = nullptr, *cn = nullptr, *cd = nullptr;   // aE/D, aN/D, 1/D
+    const double *ya = nullptr, *yn = nullptr, *cd = nullptr;   // aE/D_E, aN/D_N, 1/D
     long cpitch = 0;
     double *aW = nullptr, *aS = nullptr, *hb = nullptr, *kb = nullptr;   // 1D [n+2]
     double *own = nullptr;               // owned coefficient block (levels >= 1)
@@ -53,14 +58,15 @@ struct Level {
 };
 
 // corner GS sweep arguments (k_mg.cu)
-// downstream sweep z = s q + ca z_E + cn z_N on [1, nl]^2 (k_mg.cu)
+// downstream sweep on [1, nl]^2 (k_mg.cu): y = q + ca y_E + cn y_N, z = cd y (y-form) or z = y
 struct WaveArgs {
     int nl; long pv, pc;
     int ioff, joff;                      // node (i, j) lives at array index (i+ioff, j+joff)
-    const double *q, *s, *ca, *cn;       // s == nullptr: 1
+    const double *q, *ca, *cn, *cd;
     double *z;
     int rows_out, cols_out, halo_y, halo_x;
     int *chain_flags; double *chain_buf; long chain_ld;   // exact chained mode
+    int dbg;                             // debugging switches (0 in production)
 };
 
 // tunables (defaults in spp_create; overridable through SPP_TUNE="key=val,..." for experiments)
@@ -87,6 +93,7 @@ struct Ctx {
     long P = 0; size_t G = 0;
     double *aE = nullptr, *aN = nullptr, *rr = nullptr;         // coefficients
     double *ca = nullptr, *cn = nullptr, *cd = nullptr;         // aE/D, aN/D, 1/D
+    double *ya = nullptr, *yn = nullptr;                        // aE/D_E, aN/D_N (y-form sweeps)
     double *aW = nullptr, *aS = nullptr;                        // [N+1]
     double *coef_block = nullptr;
     // line factors
@@ -110,6 +117,8 @@ struct Ctx {
     double *chain = nullptr; long chain_ld = 0;   // inflow buffer of the exact chained sweep
     int *chain_flags = nullptr;
     Tune tune;
+    std::map<std::tuple<const void *, long, long>, CUtensorMap> tmaps;   // sheared TMA maps (k_mg.cu)
+    cudaError_t sticky = cudaSuccess;      // first launch-configuration error of a solve
     double *mg_block = nullptr;
     int *flags = nullptr; int epoch = 0;
     // 1D
@@ -134,7 +143,8 @@ cudaError_t setup_lines(Ctx *c);
 void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double> &ky);
 // corner multigrid (k_mg.cu)
 void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, double *enew, const double *ec);
-void launch_wave_chain(Ctx *c, WaveArgs a, int cls, double bytes);
+void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform, int cls, double bytes);
+void launch_ycoef(Ctx *c, int nl, long pc, const double *aE, const double *aN, const double *cd, double *ya, double *yn);
 cudaError_t wave_init();
 void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e);
 void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew, const double *b, double *rho,
