@@ -37,7 +37,7 @@ namespace spp {
 // ------------------------------------------------------------------------------------------ profiling
 static const char *kProfNames[SPP_PROF_CLASSES] = {"spmv", "sweep_I", "lines_XY", "mg_sweep",
                                                    "mg_resid_restrict", "mg_prolong", "mg_update",
-                                                   "krylov_vec", "setup", "other"};
+                                                   "krylov_vec", "setup", "other", "mg_coarse"};
 
 ProfScope::ProfScope(Ctx *c_, int cls_, double bytes_) : c(c_), cls(cls_), bytes(bytes_)
 {
@@ -112,6 +112,7 @@ static double *vcycle(Ctx *c, int l, const double *R)
 {
     Level &L = c->lev[l];
     double *ea = L.e, *eb = L.q;
+    if (launch_coarse_vcycle(c, l, R)) return eb;   // levels l..L-1 fused (smem-resident)
     if (l == c->L - 1) {
         launch_gs(c, l, 0, R, nullptr, ea, nullptr);
         launch_gs(c, l, 1, R, ea, eb, nullptr);
@@ -283,6 +284,7 @@ static void parse_tune(Ctx *c)
             else if (k == "gs_tile_cols") c->tune.gs_tile_cols = v;
             else if (k == "gs_max_halo") c->tune.gs_max_halo = v;
             else if (k == "sweep_warps") c->tune.sweep_warps = v;
+            else if (k == "coarse_max") c->tune.coarse_max = v;
         }
         pos = end + 1;
     }
@@ -539,7 +541,7 @@ spp_status spp_profile_enable(spp_ctx *cx, int32_t en)
 {
     Ctx *c = (Ctx *)cx;
     if (!c) return SPP_E_ARG;
-    c->prof_on = en ? (en == 1 ? 0x3ff : en) : 0;
+    c->prof_on = en ? (en == 1 ? 0x7ff : en) : 0;
     return SPP_OK;
 }
 spp_status spp_profile_reset(spp_ctx *cx)

@@ -28,55 +28,85 @@
 namespace spp {
 
 // ------------------------------------------------------------------------------ setup
-// One thread per line.  chain 0 = X (lines of constant y, j = N-1-l; element k -> i = k+1),
-// chain 1 = Y (lines of constant x, i = N-1-l; element k -> j = k+1).
-__global__ void k_line_factor(int chain, int N, long P, const double *aE, const double *aN,
-                              const double *rr, const double *aW, const double *aS, int weighted,
-                              double *p, double *e, double *al, double *be, double *t)
+// One thread per line, both chains in one launch (blockIdx.y = chain): chain 0 = X (lines of
+// constant y, j = N-1-l; element k -> i = k+1), chain 1 = Y (lines of constant x, i = N-1-l;
+// element k -> j = k+1).  The Thomas forward sweep (a dependent chain of reciprocals) runs with
+// the coefficient loads of 8 elements issued ahead; the certified contraction
+// kappa_l = max_k (T_l^{-1} c_l)_k is formed in the same kernel (forward part y = al y + e
+// alongside the factorisation, backward part from the scratch copy of y).
+struct LineFactorOut { double *p, *e, *al, *be, *t, *kap, *scratch; };
+
+__global__ void __launch_bounds__(64) k_line_factor(int N, long P, const double *__restrict__ aE,
+    const double *__restrict__ aN, const double *__restrict__ rr, const double *__restrict__ aW,
+    const double *__restrict__ aS, int weighted, LineFactorOut ox, LineFactorOut oy)
 {
+    const int chain = blockIdx.y;
+    const LineFactorOut &o = chain == 0 ? ox : oy;
     const int n = N / 2, nl = n - 1;
     const int l = blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= nl) return;
     const int line = N - 1 - l;
-    double gprev = 0.0, supprev = 0.0;
+    double gprev = 0.0, supprev = 0.0, y = 0.0;
+    const long base = (long)l * n;
+#pragma unroll 8
     for (int k = 0; k < n; ++k) {
         int i, j;
-        double sub, sup, cE;
         if (chain == 0) { i = k + 1; j = line; } else { i = line; j = k + 1; }
         const long g = (long)j * P + i;
-        const double vE = aE[g], vN = aN[g];
-        const double D = ((aW[i] + vE) + (aS[j] + vN)) + rr[g];
-        if (chain == 0) { sub = aW[i]; sup = vE; cE = vN; } else { sub = aS[j]; sup = vN; cE = vE; }
+        const double vE = __ldg(aE + g), vN = __ldg(aN + g), vr = __ldg(rr + g), vw = __ldg(aW + i), vs = __ldg(aS + j);
+        const double D = ((vw + vE) + (vs + vN)) + vr;
+        const double sub = chain == 0 ? vw : vs, sup = chain == 0 ? vE : vN, cE = chain == 0 ? vN : vE;
         const double den = (k == 0) ? D : D - sub * (supprev * gprev);
         const double gk = 1.0 / den;
-        const long o = (long)l * n + k;
-        p[o] = (weighted ? D : 1.0) * gk;
-        e[o] = cE * gk;
-        al[o] = (k == 0) ? 0.0 : sub * gk;
-        const double bek = (k == n - 1) ? 0.0 : sup * gk;
-        be[o] = bek;
-        if (k == n - 1) t[l] = sup * gk;     // coupling to the I neighbour of the last element
+        const double alk = (k == 0) ? 0.0 : sub * gk, ek = cE * gk;
+        o.p[base + k] = (weighted ? D : 1.0) * gk;
+        o.e[base + k] = ek;
+        o.al[base + k] = alk;
+        o.be[base + k] = (k == n - 1) ? 0.0 : sup * gk;
+        if (k == n - 1) o.t[l] = sup * gk;    // coupling to the I neighbour of the last element
+        y = alk * y + ek;                     // forward part of T^{-1} c
+        o.scratch[base + k] = y;
         gprev = gk; supprev = sup;
     }
-}
-
-// kappa_l = max_k (T_l^{-1} c_l)_k from the stored factors: forward y = al*y + e, backward.
-__global__ void k_line_kappa(int n, int nl, const double *e, const double *al, const double *be,
-                             double *scratch, double *kap)
-{
-    const int l = blockIdx.x * blockDim.x + threadIdx.x;
-    if (l >= nl) return;
-    const long o = (long)l * n;
-    double y = 0.0;
-    for (int k = 0; k < n; ++k) { y = al[o + k] * y + e[o + k]; scratch[o + k] = y; }
     double z = 0.0, mx = 0.0;
-    for (int k = n - 1; k >= 0; --k) { z = scratch[o + k] + be[o + k] * z; mx = fmax(mx, z); }
-    kap[l] = mx;
+#pragma unroll 8
+    for (int k = n - 1; k >= 0; --k) {
+        z = o.scratch[base + k] + o.be[base + k] * z;
+        mx = fmax(mx, z);
+    }
+    o.kap[l] = mx;
 }
 
 // ------------------------------------------------------------------------------ apply
 template <int K>
-__global__ void __launch_bounds__(512) k_lines(LineChain cx, LineChain cy, const LineChunk *chunks,
+struct LineRaw { double v[K], p[K], e[K], al[K], be[K], tI; };
+
+// raw operands of line l for this thread's K elements (loads only; nothing depends on the chain)
+template <int K>
+__device__ __forceinline__ void line_load(const LineChain &ch, int l, int k0, const double *__restrict__ v,
+                                          const double *z, LineRaw<K> &r)
+{
+    const int len = ch.len;
+    const long base = ch.v0 + (long)l * ch.vline, fo = (long)l * len;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int kk = k0 + k;
+        const bool ok = kk < len;
+        r.v[k] = ok ? __ldg(v + base + (long)kk * ch.vstride) : 0.0;
+        r.p[k] = ok ? __ldg(ch.p + fo + kk) : 0.0;
+        r.e[k] = ok ? __ldg(ch.e + fo + kk) : 0.0;
+        r.al[k] = ok ? __ldg(ch.al + fo + kk) : 0.0;
+        r.be[k] = ok ? __ldg(ch.be + fo + kk) : 0.0;
+    }
+    // coupling to the I neighbour of the last element (written by the M_II sweep)
+    r.tI = (k0 <= len - 1 && len - 1 < k0 + K) ? ch.t[l] * z[base + (long)(len - 1) * ch.vstride + ch.istep] : 0.0;
+}
+
+// Line solves of one chunk: lines start..last in order, each T_l z_l = s v_l + C_l z_{l-1} (+ I
+// coupling) by two block-wide affine scans.  The raw operands of line l+1 are loaded while line l
+// is scanned (register double buffer; the loop is unrolled by two so the buffers are static).
+template <int K>
+__global__ void __launch_bounds__(256) k_lines(LineChain cx, LineChain cy, const LineChunk *chunks,
                                                const double *__restrict__ v, double *z)
 {
     __shared__ double sA[32], sB[64];
@@ -84,38 +114,42 @@ __global__ void __launch_bounds__(512) k_lines(LineChain cx, LineChain cy, const
     const LineChain &ch = ck.chain == 0 ? cx : cy;
     const int len = ch.len;
     const int k0 = threadIdx.x * K;
-    double zp[K], al[K], be[K], b[K], y[K], zz[K];
+    double zp[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) zp[k] = 0.0;
-    for (int l = ck.start; l <= ck.last; ++l) {
-        const long base = ch.v0 + (long)l * ch.vline;
-        const long fo = (long)l * len;
-        // prefetch the next line's factors into L2
-        if (l < ck.last && k0 < len) {
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(ch.p + fo + len + k0));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(ch.e + fo + len + k0));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(ch.al + fo + len + k0));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(ch.be + fo + len + k0));
-        }
+    auto solve = [&](int l, const LineRaw<K> &r) {
+        double al[K], be[K], b[K], y[K], zz[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const int kk = k0 + k;
-            if (kk < len) {
-                const double vv = v[base + (long)kk * ch.vstride];
-                double bb = ch.p[fo + kk] * vv + ch.e[fo + kk] * zp[k];
-                if (kk == len - 1) bb += ch.t[l] * z[base + (long)kk * ch.vstride + ch.istep];
-                b[k] = bb; al[k] = ch.al[fo + kk]; be[k] = ch.be[fo + kk];
-            } else {
-                b[k] = 0.0; al[k] = 0.0; be[k] = 0.0;
-            }
+            double bb = r.p[k] * r.v[k] + r.e[k] * zp[k];
+            if (k0 + k == len - 1) bb += r.tI;
+            b[k] = bb; al[k] = r.al[k]; be[k] = r.be[k];
         }
         fwd_scan<K>(al, b, y, sA, sB);
         bwd_scan<K>(be, y, zz, sA, sB);
+        const long base = ch.v0 + (long)l * ch.vline;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             zp[k] = zz[k];
             const int kk = k0 + k;
             if (l >= ck.first && kk < len) z[base + (long)kk * ch.vstride] = zz[k];
+        }
+    };
+    if (K <= 8) {
+        LineRaw<K> ra, rb;
+        line_load<K>(ch, ck.start, k0, v, z, ra);
+        for (int l = ck.start; l <= ck.last; l += 2) {
+            if (l + 1 <= ck.last) line_load<K>(ch, l + 1, k0, v, z, rb);
+            solve(l, ra);
+            if (l + 1 > ck.last) break;
+            if (l + 2 <= ck.last) line_load<K>(ch, l + 2, k0, v, z, ra);
+            solve(l + 1, rb);
+        }
+    } else {                                           // large K: no double buffer (registers)
+        for (int l = ck.start; l <= ck.last; ++l) {
+            LineRaw<K> r;
+            line_load<K>(ch, l, k0, v, z, r);
+            solve(l, r);
         }
     }
 }
@@ -126,7 +160,7 @@ void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double
     c->chunks.clear();
     const int nl = c->n - 1;
     const double target = std::log(1e-20);
-    const int budget = std::max(1, c->sm_count);          // CTAs per chain
+    const int budget = std::max(1, c->sm_count / 2);      // CTAs per chain: one resident CTA per SM
     for (int chain = 0; chain < 2; ++chain) {
         const std::vector<double> &k = chain == 0 ? kx : ky;
         std::vector<double> lg(nl + 1, 0.0);                 // prefix sums of log kappa
@@ -160,13 +194,10 @@ cudaError_t setup_lines(Ctx *c)
     double *xp = base, *xe = base + per, *xa = base + 2 * per, *xb = base + 3 * per;
     double *yp = base + 4 * per, *ye = base + 5 * per, *ya = base + 6 * per, *yb = base + 7 * per;
     const int tpb = 64, nb = (nl + tpb - 1) / tpb;
-    k_line_factor<<<nb, tpb, 0, c->st>>>(0, N, c->P, c->aE, c->aN, c->rr, c->aW, c->aS, c->weighted,
-                                         xp, xe, xa, xb, c->tX);
-    k_line_factor<<<nb, tpb, 0, c->st>>>(1, N, c->P, c->aE, c->aN, c->rr, c->aW, c->aS, c->weighted,
-                                         yp, ye, ya, yb, c->tY);
-    k_line_kappa<<<nb, tpb, 0, c->st>>>(n, nl, xe, xa, xb, c->cbuf, c->kapX);
-    k_line_kappa<<<nb, tpb, 0, c->st>>>(n, nl, ye, ya, yb, c->cbuf + per, c->kapY);
-    c->launches += 4;
+    const LineFactorOut ox{xp, xe, xa, xb, c->tX, c->kapX, c->cbuf};
+    const LineFactorOut oy{yp, ye, ya, yb, c->tY, c->kapY, c->cbuf + per};
+    k_line_factor<<<dim3(nb, 2), tpb, 0, c->st>>>(N, c->P, c->aE, c->aN, c->rr, c->aW, c->aS, c->weighted, ox, oy);
+    c->launches++;
     SPP_CUDA_TRY(cudaGetLastError());
     std::vector<double> kx(nl), ky(nl);
     SPP_CUDA_TRY(cudaMemcpyAsync(kx.data(), c->kapX, sizeof(double) * nl, cudaMemcpyDeviceToHost, c->st));
@@ -186,7 +217,7 @@ cudaError_t setup_lines(Ctx *c)
                                  cudaMemcpyHostToDevice, c->st));
     int T = n / 8;
     if (T < 32) T = 32;
-    if (T > 512) T = 512;
+    if (T > 256) T = 256;
     c->lines_threads = T;
     return cudaStreamSynchronize(c->st);
 }
@@ -201,7 +232,8 @@ void launch_lines(Ctx *c, const double *v, double *z)
     if (K <= 1) k_lines<1><<<nb, T, 0, c->st>>>(c->chX, c->chY, c->d_chunks, v, z);
     else if (K <= 2) k_lines<2><<<nb, T, 0, c->st>>>(c->chX, c->chY, c->d_chunks, v, z);
     else if (K <= 4) k_lines<4><<<nb, T, 0, c->st>>>(c->chX, c->chY, c->d_chunks, v, z);
-    else k_lines<8><<<nb, T, 0, c->st>>>(c->chX, c->chY, c->d_chunks, v, z);
+    else if (K <= 8) k_lines<8><<<nb, T, 0, c->st>>>(c->chX, c->chY, c->d_chunks, v, z);
+    else k_lines<16><<<nb, T, 0, c->st>>>(c->chX, c->chY, c->d_chunks, v, z);
     c->launches++;
 }
 

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a, const __grid_co
         tma_load(dst + WBOX * 8, &m.a1, x, R0, bar);
         tma_load(dst + 2 * WBOX * 8, &m.a2, x, R0, bar);
     };
-    if (lane == 0) {
+    if (lane == 0 && !(a.dbg & 16)) {
         issue(0);
         if (nch > 1) issue(1);
     }
@@ -192,8 +192,10 @@ __global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a, const __grid_co
     const bool rows_all = wtop - 31 >= out_bot;         // all 32 rows of the warp are swept rows
     const bool rows_out_all = rows_all && wtop <= out_top;   // ... and output rows
     double z1 = 0.0, z2 = 0.0;                          // own results of the last two steps
+    long long tp_spin = 0, tp_bar = 0, tp_steps = 0, tp_fast = 0;
+    const long long tp0 = clock64();
     for (int c = 0; c < nch; ++c) {
-        if (lane == 0) {
+        if (lane == 0 && !(a.dbg & 16)) {
             if (c + 2 < nch) issue(c + 2);
             if (c + WPF < nch) {
                 const int x = Xb - (c + WPF) * WCW;
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a, const __grid_co
         // element an output node -- no per-element predicates
         const bool fast = rows_all && c * WCW - WLAG * 31 >= 0 && c * WCW + WCW - 1 < ncols &&
                           (c == 0 || (rows_out_all && (c - 1) * WCW - WLAG * 31 >= right - out_right));
-        stage_cd(c);
+        if (!(a.dbg & 2)) stage_cd(c);
         if (YFORM) asm volatile("cp.async.wait_group 1;" ::: "memory");   // chunk c-1's 1/D band
         const double *cdb = cdband + (size_t)((c + 1) & 1) * WCDB;
         // North inflow of lane 0 for the columns of this chunk (all wait loops warp-uniform: a
@@ -213,6 +215,7 @@ __global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a, const __grid_co
         const int need = min(ncols, c * WCW + WCW);
         const double *ein_src = nullptr;                // inflow row (edge ring) or null = 0
         double ein_g[WCW];
+        const long long ta = clock64();
         if (w > 0) {
             while (*((volatile int *)&prod[w - 1]) < need) { }
             __threadfence_block();
@@ -227,7 +230,8 @@ __global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a, const __grid_co
             const int lim = c * WCW + WCW - WLAG * 31 - WEB;
             if (lim > 0) { while (*((volatile int *)&cons[w + 1]) < lim) { } }
         }
-        mbar_wait((unsigned)__cvta_generic_to_shared(&bars[w][c % WNS]), (unsigned)((c / WNS) & 1));
+        const long long tb = clock64();
+        if (!(a.dbg & 8)) mbar_wait((unsigned)__cvta_generic_to_shared(&bars[w][c % WNS]), (unsigned)((c / WNS) & 1));
         __syncwarp();
         const double *sq = ring + (size_t)(c % WNS) * WSLOT;
         double *zb = zband + (size_t)(c & 1) * WZB;
@@ -271,15 +275,18 @@ __global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a, const __grid_co
                     if (has_consumer) edge[w][idx & (WEB - 1)] = Z[u];
                     if (CHAIN && chain_out) __stcg(a.chain_buf + (long)blockIdx.y * a.chain_ld + idx, Z[u]);
                 }
-                if (c > 0) {                            // interleaved write-back of chunk c-1
+                if (c > 0 && !(a.dbg & 4)) {            // interleaved write-back of chunk c-1
                     const double cdv = YFORM ? cdb[k * 32 + lane] : 1.0;
                     if (F) a.z[wv0 + k * dwv - (c - 1) * WCW] = YFORM ? cdv * YB[u] : YB[u];
                     else wb(c - 1, k, cdv);
                 }
             }
         };
+        const long long tc = clock64();
         if (fast) { group(std::true_type{}, std::integral_constant<int, 0>{}); group(std::true_type{}, std::integral_constant<int, 1>{}); }
         else { group(std::false_type{}, std::integral_constant<int, 0>{}); group(std::false_type{}, std::integral_constant<int, 1>{}); }
+        const long long td = clock64();
+        tp_spin += tb - ta; tp_bar += tc - tb; tp_steps += td - tc; tp_fast += fast;
         const int done = min(ncols, max(0, c * WCW + WCW - WLAG * 31));
         if (lane == 31) {
             if (has_consumer) {
@@ -289,6 +296,11 @@ __global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a, const __grid_co
             if (chain_out) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.chain_flags + blockIdx.y), "r"(done) : "memory");
         }
         __syncwarp();
+    }
+    if ((a.dbg & 64) && lane == 0 && a.prof) {
+        const long long tot = clock64() - tp0;
+        long long *o = a.prof + 8 * ((blockIdx.y * gridDim.x + blockIdx.x) * 4 + w);
+        o[0] = tot; o[1] = tp_spin; o[2] = tp_bar; o[3] = tp_steps; o[4] = tp_fast; o[5] = nch;
     }
     {   // write-back of the last chunk
         const int c = nch - 1;
@@ -367,14 +379,30 @@ void launch_wave(Ctx *c, WaveArgs a, long rows_v, long rows_c, int warps, bool y
     WaveMaps m;
     if (!wave_maps(c, a, rows_v, rows_c, &m)) { c->sticky = cudaErrorInvalidValue; return; }
     static int dbg = -1;
-    if (dbg < 0) { const char *e = getenv("SPP_WAVE_DBG"); dbg = e ? atoi(e) : 0; }
-    a.dbg = dbg;
+    static long long *prof = nullptr;
+    if (dbg < 0) {
+        const char *e = getenv("SPP_WAVE_DBG"); dbg = e ? atoi(e) : 0;
+        if (dbg & 64) cudaMalloc(&prof, sizeof(long long) * 8 * 4 * 4096);
+    }
+    a.dbg = dbg; a.prof = prof;
     const dim3 grid((a.nl + a.cols_out - 1) / a.cols_out, (a.nl + a.rows_out - 1) / a.rows_out);
     const size_t sm = wave_smem(warps);
     ProfScope ps(c, cls, bytes);
+    if (prof) cudaMemsetAsync(prof, 0, sizeof(long long) * 8 * 4 * 4096, c->st);
     if (yform) k_wave<true, false><<<grid, warps * 32, sm, c->st>>>(a, m);
     else k_wave<false, false><<<grid, warps * 32, sm, c->st>>>(a, m);
     c->launches++;
+    if (prof && a.nl >= 2048 && getenv("SPP_WAVE_PROF_DUMP")) {
+        static int dumped = 0;
+        if (!dumped++) {
+            long long h[8 * 4 * 16];
+            cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, c->st);
+            cudaStreamSynchronize(c->st);
+            for (int k = 0; k < 16; ++k)
+                fprintf(stderr, "[wave-prof] cta %d warp %d: total %lld spin %lld bar %lld steps %lld fastchunks %lld nch %lld\n",
+                        k / 4, k % 4, h[8 * k], h[8 * k + 1], h[8 * k + 2], h[8 * k + 3], h[8 * k + 4], h[8 * k + 5]);
+        }
+    }
     dbg_sync(c, "k_wave tiled");
 }
 
@@ -458,6 +486,193 @@ void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, dou
     if (L.tile_warps == 0) { launch_wave_chain(c, a, rows_v, rows_c, true, 3, bytes); return; }
     a.rows_out = L.tile_rows; a.cols_out = L.tile_cols; a.halo_y = L.halo_y; a.halo_x = L.halo_x;
     launch_wave(c, a, rows_v, rows_c, L.tile_warps, true, 3, bytes);
+}
+
+// ------------------------------------------------------------------------------------------
+// Coarse V-cycle (levels with n <= kCoarseMax): one CTA runs the whole
+// V(1,1) cycle of P:1205-1209 / P:1281-1283 for levels lc..L-1 with every level's b, e and
+// residual in shared memory (zero ghost ring); coefficients come from global memory (L2).
+//   down: e_l = GS(b_l) from 0; rho = b_l - A_l e_l; b_{l+1} = S^-1 P^T S rho
+//   coarsest: 4 GS sweeps from 0
+//   up:   e_l += P e_{l+1}; e_l = GS(b_l) from e_l
+// GS is the sequential downstream sweep (j desc, i desc; E/N new, W/S old) done in place by
+// anti-diagonals: the nodes of diagonal d = (n-i) + (n-j) need only diagonal d-1 (new E, N) and
+// diagonal d+1 (old W, S), so each diagonal is one parallel step (then __syncthreads).
+// ------------------------------------------------------------------------------------------
+struct CoarseLev {
+    int n; int cpitch;
+    const double *aE, *aN, *rr, *cd, *aW, *aS, *hb, *kb;
+};
+struct CoarseArgs {
+    int nlev;                       // levels lc .. lc+nlev-1 (the last is the coarsest)
+    CoarseLev lv[8];
+    const double *R; long rpitch;   // rhs of level lc (value layout)
+    double *out; long opitch;       // result e of level lc (value layout)
+};
+
+// ring: 4 slots x 4 coefficients x blockDim doubles of shared memory (per-thread prefetch ring)
+__device__ __forceinline__ void cgs_sweep(const CoarseLev &L, const double *b, double *e, int stride, double *ring)
+{
+    // thread t owns column i = n - t and meets it on diagonals d = t .. t+n-1 at row j = n-(d-t);
+    // its coefficients (column i, rows descending) are staged by cp.async four rows ahead
+    const int n = L.n, t = threadIdx.x, T = blockDim.x;
+    const bool act = t < n;
+    const int i = n - t;
+    const double aw = act ? __ldg(L.aW + i) : 0.0;
+    auto stage = [&](int r) {                          // row j = n - r into slot r & 3
+        const int j = n - r, u = r & 3;
+        const bool ok = act && j >= 1;
+        const int q = ok ? j * L.cpitch + i : 0;
+        double *sl = ring + (size_t)u * 4 * T + t;
+        cp_async8(sl, L.aE + q, ok);
+        cp_async8(sl + T, L.aN + q, ok);
+        cp_async8(sl + 2 * T, L.cd + q, ok);
+        cp_async8(sl + 3 * T, L.aS + (ok ? j : 0), ok);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int r = 0; r < 4; ++r) stage(r);
+    int r = 0;                                         // rows of this column done
+    for (int d = 0; d <= 2 * (n - 1); ++d) {
+        if (act && d >= t && r < n) {
+            asm volatile("cp.async.wait_group 3;" ::: "memory");
+            const double *sl = ring + (size_t)(r & 3) * 4 * T + t;
+            const int j = n - r, s = j * stride + i;
+            const double v = (((b[s] + aw * e[s - 1]) + sl[3 * T] * e[s - stride]) + sl[0] * e[s + 1]) + sl[T] * e[s + stride];
+            e[s] = v * sl[2 * T];
+            stage(r + 4);                              // slot r&3 refilled with row j-4
+            ++r;
+        }
+        __syncthreads();
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
+{
+    extern __shared__ double cs[];
+    // layout: per level b_l, e_l of (n_l+2)^2, then one residual scratch of level lc's size
+    double *B[8], *E[8];
+    int st[8];
+    double *p = cs;
+    for (int l = 0; l < a.nlev; ++l) {
+        st[l] = a.lv[l].n + 2;
+        B[l] = p; p += st[l] * st[l];
+        E[l] = p; p += st[l] * st[l];
+    }
+    double *rho = p;
+    double *cring = rho + st[0] * st[0];               // cgs_sweep prefetch ring, 16 * blockDim doubles
+    const int tot = (int)(p - cs) + st[0] * st[0];
+    for (int k = threadIdx.x; k < tot; k += blockDim.x) cs[k] = 0.0;
+    __syncthreads();
+    {   // level lc rhs
+        const int n = a.lv[0].n;
+        for (int k = threadIdx.x; k < n * n; k += blockDim.x) {
+            const int j = k / n + 1, i = k % n + 1;
+            B[0][j * st[0] + i] = a.R[(long)j * a.rpitch + i];
+        }
+        __syncthreads();
+    }
+    const int last = a.nlev - 1;
+    // ---- down ----
+    for (int l = 0; l < last; ++l) {
+        const CoarseLev &F = a.lv[l], &C = a.lv[l + 1];
+        const int n = F.n, sf = st[l], sc = st[l + 1];
+        cgs_sweep(F, B[l], E[l], sf, cring);                           // pre-smoothing from zero
+        for (int k = threadIdx.x; k < n * n; k += blockDim.x) {        // S-scaled residual
+            const int j = k / n + 1, i = k % n + 1;
+            const int s = j * sf + i, q = j * F.cpitch + i;
+            const double ec = E[l][s];
+            const double Ae = __ldg(F.aW + i) * (ec - E[l][s - 1]) + __ldg(F.aE + q) * (ec - E[l][s + 1]) +
+                              __ldg(F.aS + j) * (ec - E[l][s - sf]) + __ldg(F.aN + q) * (ec - E[l][s + sf]) +
+                              __ldg(F.rr + q) * ec;
+            rho[s] = (__ldg(F.hb + i) * __ldg(F.kb + j)) * (B[l][s] - Ae);
+        }
+        __syncthreads();
+        const int nc = C.n;
+        for (int k = threadIdx.x; k < nc * nc; k += blockDim.x) {      // b_c = S_c^-1 P^T (S rho)
+            const int J = k / nc + 1, I = k % nc + 1;
+            double acc = 0.0;
+#pragma unroll
+            for (int bb = -1; bb <= 1; ++bb) {
+                const int j = 2 * J + bb;
+                if (j < 1 || j > n) continue;
+                const double *r = rho + j * sf + 2 * I;
+                double rs = r[0];
+                if (2 * I - 1 >= 1) rs = 0.5 * r[-1] + rs;
+                if (2 * I + 1 <= n) rs = rs + 0.5 * r[1];
+                acc += (bb == 0 ? 1.0 : 0.5) * rs;
+            }
+            B[l + 1][J * sc + I] = acc / (__ldg(C.hb + I) * __ldg(C.kb + J));
+        }
+        __syncthreads();
+    }
+    // ---- coarsest: four sweeps from zero ----
+    for (int s4 = 0; s4 < 4; ++s4) cgs_sweep(a.lv[last], B[last], E[last], st[last], cring);
+    // ---- up ----
+    for (int l = last - 1; l >= 0; --l) {
+        const int n = a.lv[l].n, sf = st[l], sc = st[l + 1];
+        const double *ec = E[l + 1];
+        for (int k = threadIdx.x; k < n * n; k += blockDim.x) {        // e += P e_c
+            const int j = k / n + 1, i = k % n + 1;
+            const int I0 = i >> 1, J0 = j >> 1;
+            const bool oi = i & 1, oj = j & 1;
+            double v;
+            if (!oi && !oj) v = ec[J0 * sc + I0];
+            else if (oi && !oj) v = 0.5 * (ec[J0 * sc + I0] + ec[J0 * sc + I0 + 1]);
+            else if (!oi && oj) v = 0.5 * (ec[J0 * sc + I0] + ec[(J0 + 1) * sc + I0]);
+            else v = 0.25 * ((ec[J0 * sc + I0] + ec[J0 * sc + I0 + 1]) + (ec[(J0 + 1) * sc + I0] + ec[(J0 + 1) * sc + I0 + 1]));
+            E[l][j * sf + i] += v;
+        }
+        __syncthreads();
+        cgs_sweep(a.lv[l], B[l], E[l], sf, cring);                     // post-smoothing
+    }
+    {   // result of level lc
+        const int n = a.lv[0].n;
+        for (int k = threadIdx.x; k < n * n; k += blockDim.x) {
+            const int j = k / n + 1, i = k % n + 1;
+            a.out[(long)j * a.opitch + i] = E[0][j * st[0] + i];
+        }
+    }
+}
+
+static size_t coarse_smem(const Ctx *c, int lc)
+{
+    size_t tot = 0;
+    for (int l = lc; l < c->L; ++l) tot += 2 * (size_t)(c->lev[l].n + 2) * (c->lev[l].n + 2);
+    tot += (size_t)(c->lev[lc].n + 2) * (c->lev[lc].n + 2) + 16 * 256;
+    return tot * sizeof(double);
+}
+
+// V-cycle of levels lc..L-1 in one launch; result in lev[lc].q.  Returns false when the levels
+// do not fit (the caller then recurses level by level).
+bool launch_coarse_vcycle(Ctx *c, int lc, const double *R)
+{
+    if (c->L - lc > 8 || c->lev[lc].n > c->tune.coarse_max) return false;
+    const size_t sm = coarse_smem(c, lc);
+    if (sm > 200 * 1024) return false;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_coarse_vcycle, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess)
+            return false;
+        attr = true;
+    }
+    CoarseArgs a{};
+    a.nlev = c->L - lc;
+    for (int l = lc; l < c->L; ++l) {
+        const Level &L = c->lev[l];
+        a.lv[l - lc] = CoarseLev{L.n, (int)L.cpitch, L.aE, L.aN, L.rr, L.cd, L.aW, L.aS, L.hb, L.kb};
+    }
+    a.R = R; a.rpitch = c->lev[lc].pitch;
+    a.out = c->lev[lc].q; a.opitch = c->lev[lc].pitch;
+    double nn = 0;
+    for (int l = lc; l < c->L; ++l) nn += (double)c->lev[l].n * c->lev[l].n;
+    ProfScope ps(c, 10, nn * 96.0);   // b read; aE, aN, 1/D, r read by two sweeps + residual; e written
+    const int threads = std::max(256, (c->lev[lc].n + 31) / 32 * 32);   // >= n: one column per thread in the sweeps
+    if (threads > 256) return false;
+    k_coarse_vcycle<<<1, threads, sm, c->st>>>(a);
+    c->launches++;
+    return true;
 }
 
 // ------------------------------------------------------------------------------------------

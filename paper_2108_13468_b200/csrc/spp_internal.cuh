@@ -67,6 +67,7 @@ struct WaveArgs {
     int rows_out, cols_out, halo_y, halo_x;
     int *chain_flags; double *chain_buf; long chain_ld;   // exact chained mode
     int dbg;                             // debugging switches (0 in production)
+    long long *prof;                     // dbg & 64: per-warp cycle counters
 };
 
 // tunables (defaults in spp_create; overridable through SPP_TUNE="key=val,..." for experiments)
@@ -75,6 +76,7 @@ struct Tune {
     int gs_tile_cols = 512;    // output columns per GS tile
     int gs_max_halo = 128;     // no certified halo below this -> exact chained sweep
     int sweep_warps = 4;       // warps per CTA of the exact chained sweep (M_II)
+    int coarse_max = 64;       // levels with n <= this run as one fused single-CTA V-cycle
 };
 
 struct ProfRec { int64_t launches = 0; double ms = 0, bytes = 0; };
@@ -150,6 +152,7 @@ void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e);
 void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew, const double *b, double *rho,
                          double *part);
 cudaError_t setup_mg_tiles(Ctx *c);
+bool launch_coarse_vcycle(Ctx *c, int lc, const double *R);
 
 // profiling helpers
 struct ProfScope {
