@@ -48,20 +48,17 @@
 namespace spp {
 
 constexpr int WCW = 16;          // columns per chunk (box width, 128 bytes)
-constexpr int WNS = 3;           // staging ring slots (one consumed, two in flight)
-constexpr int WNA = 3;           // staged arrays: q, a1, a2
-constexpr int WBOX = 32 * WCW;   // doubles per box
-constexpr int WSLOT = WNA * WBOX;             // doubles per staging slot (12 KB)
-constexpr int WZP = WCW + 1;                  // padded result band row stride
-constexpr int WZB = 32 * WZP;                 // doubles per result band
-constexpr int WCDB = 16 * 32;                 // doubles per write-back scale band (1/D of one chunk)
-constexpr int WWARP = (WNS * WSLOT + 2 * WZB + 2 * WCDB + 127) / 128 * 128;   // doubles per warp (1 KB multiple)
-constexpr int WMAXW = 4;         // warps per CTA (max)
+constexpr int WNS = 3;           // staging ring slots
+constexpr int WNA = 4;           // boxes per slot: q (overwritten in place by y), a1, a2, 1/D
+constexpr int WBOX = 32 * WCW;   // doubles per box (4 KB)
+constexpr int WSLOT = WNA * WBOX;             // doubles per staging slot (16 KB)
+constexpr int WWARP = WNS * WSLOT;            // doubles per warp (48 KB, a 1 KB multiple)
+constexpr int WMAXW = 4;         // sweeping warps per CTA (max); +1 TMA producer warp
 constexpr int WEB = 128;         // edge ring (columns)
 constexpr int WPF = 4;           // L2 prefetch distance (chunks)
 constexpr int WLAG = 2;          // lane-to-lane skew (columns)
 
-struct WaveMaps { CUtensorMap q, a1, a2, cd; };   // cd: L2 prefetch only
+struct WaveMaps { CUtensorMap q, a1, a2, cd; };
 
 __device__ __forceinline__ void cp_async8(double *dst, const double *src, bool valid)
 {
@@ -91,17 +88,22 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity)
 }
 
 template <bool YFORM, bool CHAIN>
-__global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a, const __grid_constant__ WaveMaps m)
+__global__ void __launch_bounds__((WMAXW + 1) * 32) k_wave(WaveArgs a, const __grid_constant__ WaveMaps m)
 {
     extern __shared__ double smem_raw[];
     __shared__ double edge[WMAXW][WEB];
     __shared__ int prod[WMAXW], cons[WMAXW];
-    __shared__ __align__(8) unsigned long long bars[WMAXW][WNS];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
+    // full: the TMA of (warp, slot) landed; empty: the warp is done with the slot (steps and the
+    // write-back of its results, which happens one chunk later)
+    __shared__ __align__(8) unsigned long long bars[WMAXW][WNS], ebars[WMAXW][WNS];
+    // warps 0..W-1 sweep 32-row strips; warp W is the TMA producer (lane w serves warp w)
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = (blockDim.x >> 5) - 1;
     if (threadIdx.x < WMAXW) { prod[threadIdx.x] = 0; cons[threadIdx.x] = 0; }
-    if (lane == 0)
-        for (int s = 0; s < WNS; ++s)
+    if (w < W && lane == 0)
+        for (int s = 0; s < WNS; ++s) {
             asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&bars[w][s])));
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&ebars[w][s])));
+        }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     const int nl = a.nl;
@@ -118,104 +120,91 @@ __global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a, const __grid_co
     const int right0 = min(nl, out_right + a.halo_x);
     const int right = ((right0 + a.ioff) & 1) ? right0 : right0 + 1;
     const int ncols = right - out_left + 1;
+    const int nch = (ncols + WLAG * 31 + WCW - 1) / WCW;
+    // 128B-swizzled TMA boxes need 1 KB aligned shared memory (pointer arithmetic on the shared
+    // array keeps the accesses in the shared state space: LDS/STS, not generic LD/ST)
+    double *smem = smem_raw + (((1024u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u) >> 3);
+    if (w == W) {                                       // ---- TMA producer warp ----
+        const int pw = lane;
+        const int pwtop = top - 32 * pw;
+        if (pw >= W || pwtop < out_bot) return;
+        const unsigned ring_s = (unsigned)__cvta_generic_to_shared(smem + (size_t)pw * WWARP);
+        // box origin in the sheared view: X = col + 2R (array coordinates), rows wtop-31..wtop
+        const int Xb = right + a.ioff + WLAG * (pwtop + a.joff) - (WCW - 1);
+        const int R0 = pwtop - 31 + a.joff;
+        const unsigned bytes = (YFORM ? 4 : 3) * WBOX * 8;
+        for (int c = 0; c < nch; ++c) {
+            const int sl = c % WNS;
+            if (c >= WNS) mbar_wait((unsigned)__cvta_generic_to_shared(&ebars[pw][sl]), (unsigned)(((c / WNS) - 1) & 1));
+            const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[pw][sl]);
+            const unsigned dst = ring_s + (unsigned)(sl * WSLOT * 8);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+            const int x = Xb - c * WCW;
+            tma_load(dst, &m.q, x, R0, bar);
+            tma_load(dst + WBOX * 8, &m.a1, x, R0, bar);
+            tma_load(dst + 2 * WBOX * 8, &m.a2, x, R0, bar);
+            if (YFORM) tma_load(dst + 3 * WBOX * 8, &m.cd, x, R0, bar);
+            if (c + WPF < nch) {
+                const int xp = Xb - (c + WPF) * WCW;
+                tma_prefetch(&m.q, xp, R0); tma_prefetch(&m.a1, xp, R0); tma_prefetch(&m.a2, xp, R0);
+                if (YFORM) tma_prefetch(&m.cd, xp, R0);
+            }
+        }
+        return;
+    }
     const int wtop = top - 32 * w;
     if (wtop < out_bot) return;                         // no rows for this warp
     const int nwa = min(W, (top - out_bot) / 32 + 1);
     const bool has_consumer = w + 1 < nwa;
     const bool chain_in = CHAIN && w == 0 && blockIdx.y > 0;
     const bool chain_out = CHAIN && w == nwa - 1 && (int)blockIdx.y + 1 < (int)gridDim.y;
-    const int nsteps = ncols + WLAG * 31;
-    const int nch = (nsteps + WCW - 1) / WCW;
-    // 128B-swizzled TMA boxes need 1 KB aligned shared memory (pointer arithmetic on the shared
-    // array keeps the accesses in the shared state space: LDS/STS, not generic LD/ST)
-    double *smem = smem_raw + (((1024u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u) >> 3);
     double *ring = smem + (size_t)w * WWARP;
-    double *zband = ring + WNS * WSLOT;
-    double *cdband = zband + 2 * WZB;                   // [chunk & 1][e][lane]: 1/D of the write-back elements
-    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
-    // box origin in the sheared view: X = col + 2R (array coordinates), rows wtop-31..wtop
-    const int Xb = right + a.ioff + WLAG * (wtop + a.joff) - (WCW - 1);   // X0 of chunk 0
-    const int R0 = wtop - 31 + a.joff;
-    auto issue = [&](int c) {                           // lane 0 only
-        const int s = c % WNS;
-        const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[w][s]);
-        const unsigned dst = ring_s + (unsigned)(s * WSLOT * 8);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(WSLOT * 8) : "memory");
-        const int x = Xb - c * WCW;
-        tma_load(dst, &m.q, x, R0, bar);
-        tma_load(dst + WBOX * 8, &m.a1, x, R0, bar);
-        tma_load(dst + 2 * WBOX * 8, &m.a2, x, R0, bar);
-    };
-    if (lane == 0 && !(a.dbg & 16)) {
-        issue(0);
-        if (nch > 1) issue(1);
-    }
-    // this lane's row and swizzled box offsets: element (row 31-t, column x') lives at byte
-    // (31-t)*128 + ((x'/2) ^ ((31-t)&7))*16 + (x'&1)*8
-    const int br = 31 - lane;
-    const int rowoff = br * WCW;                         // doubles
-    const int sw = br & 7;
+    // this lane's row; element (box row 31-t, column x') lives at double offset
+    // (31-t)*16 + ((x'/2) ^ ((31-t)&7))*2 + (x'&1)   (128B swizzle)
+    const int rowoff = (31 - lane) * WCW, sw = (31 - lane) & 7;
     const int row = wtop - lane;
     const bool rvalid = row >= out_bot;
-    // write-back mapping: element e -> band row t = 2e + lane/16, step k = 15 - lane%16
+    // write-back mapping: element e -> band row t = 2e + lane/16, box column x' = lane%16
+    // (chunk column k = 15 - x'), grid row wtop - t, column right - 16c - 15 + x' + 2t
     const int th = lane >> 4, kk = lane & 15;
     const int tmax = wtop - out_bot;
-    const int pv = (int)a.pv, pc = (int)a.pc;
-    // offset of (row wtop - th, col right - 15 + kk + 2 th) for chunk 0, element 0; per element
-    // e: row -2, col +4; per chunk: col -16
+    const int pv = (int)a.pv;
     const int wv0 = (wtop - th + a.joff) * pv + right - (WCW - 1) + kk + WLAG * th + a.ioff;
-    const int wc0 = (wtop - th + a.joff) * pc + right - (WCW - 1) + kk + WLAG * th + a.ioff;
-    const int dwv = 2 * WLAG - 2 * pv, dwc = 2 * WLAG - 2 * pc;
-    auto wb = [&](int c, int e, double cdv) {
-        const double *zb = zband + (size_t)(c & 1) * WZB;
-        const int t = 2 * e + th, k = WCW - 1 - kk, idx = c * WCW + k - WLAG * t;
-        const int col = right - idx;
-        if (t <= tmax && wtop - t <= out_top && idx >= 0 && idx < ncols && col <= out_right) {
-            const double y = zb[t * WZP + k];
-            a.z[wv0 + e * dwv - c * WCW] = YFORM ? cdv * y : y;
-        }
+    const int dwv = 2 * WLAG - 2 * pv;
+    auto wb_off = [&](int e) {                          // swizzled box offset of element e
+        const int br = 31 - (2 * e + th);
+        return br * WCW + ((((kk >> 1) ^ (br & 7))) << 1) + (kk & 1);
     };
-    // 1/D of the write-back elements of chunk c, staged by cp.async one chunk ahead of use
-    auto stage_cd = [&](int c) {
-        if (!YFORM) return;
-        double *cb = cdband + (size_t)(c & 1) * WCDB;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int t = 2 * e + th, k = WCW - 1 - kk, idx = c * WCW + k - WLAG * t;
-            const bool ok = t <= tmax && idx >= 0 && idx < ncols;
-            cp_async8(cb + e * 32 + lane, a.cd + (ok ? wc0 + e * dwc - c * WCW : 0), ok);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-
     const bool rows_all = wtop - 31 >= out_bot;         // all 32 rows of the warp are swept rows
     const bool rows_out_all = rows_all && wtop <= out_top;   // ... and output rows
-    double z1 = 0.0, z2 = 0.0;                          // own results of the last two steps
-    long long tp_spin = 0, tp_bar = 0, tp_steps = 0, tp_fast = 0;
-    const long long tp0 = clock64();
-    for (int c = 0; c < nch; ++c) {
-        if (lane == 0 && !(a.dbg & 16)) {
-            if (c + 2 < nch) issue(c + 2);
-            if (c + WPF < nch) {
-                const int x = Xb - (c + WPF) * WCW;
-                tma_prefetch(&m.q, x, R0); tma_prefetch(&m.a1, x, R0); tma_prefetch(&m.a2, x, R0);
-                if (YFORM) tma_prefetch(&m.cd, x, R0);
+    double z1 = 0.0, z2 = 0.0;                          // own results of the last step (pair)
+    // write-back of chunk cw (results in place of q in its slot): 16 elements per lane
+    auto writeback = [&](int cw, bool fastwb) {
+        const double *sl = ring + (size_t)(cw % WNS) * WSLOT;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int o = wb_off(e);
+            const double y = sl[o];
+            const double v = YFORM ? sl[3 * WBOX + o] * y : y;
+            if (fastwb) a.z[wv0 + e * dwv - cw * WCW] = v;
+            else {
+                const int t = 2 * e + th, idx = cw * WCW + (WCW - 1 - kk) - WLAG * t, col = right - idx;
+                if (t <= tmax && wtop - t <= out_top && idx >= 0 && idx < ncols && col <= out_right)
+                    a.z[wv0 + e * dwv - cw * WCW] = v;
             }
         }
-        // interior chunks (warp-uniform test): every lane's element valid, every written-back
-        // element an output node -- no per-element predicates
-        const bool fast = rows_all && c * WCW - WLAG * 31 >= 0 && c * WCW + WCW - 1 < ncols &&
-                          (c == 0 || (rows_out_all && (c - 1) * WCW - WLAG * 31 >= right - out_right));
-        if (!(a.dbg & 2)) stage_cd(c);
-        if (YFORM) asm volatile("cp.async.wait_group 1;" ::: "memory");   // chunk c-1's 1/D band
-        const double *cdb = cdband + (size_t)((c + 1) & 1) * WCDB;
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(&ebars[w][cw % WNS])) : "memory");
+    };
+    for (int c = 0; c < nch; ++c) {
+        // interior chunks (warp-uniform test): every lane's element valid
+        const bool fast = rows_all && c * WCW - WLAG * 31 >= 0 && c * WCW + WCW - 1 < ncols;
         // North inflow of lane 0 for the columns of this chunk (all wait loops warp-uniform: a
         // lane-divergent spin sends the shuffles below down the slow emulation path)
         const int need = min(ncols, c * WCW + WCW);
-        const double *ein_src = nullptr;                // inflow row (edge ring) or null = 0
+        const double *ein_src = nullptr;
         double ein_g[WCW];
-        const long long ta = clock64();
         if (w > 0) {
             while (*((volatile int *)&prod[w - 1]) < need) { }
             __threadfence_block();
@@ -230,64 +219,67 @@ __global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a, const __grid_co
             const int lim = c * WCW + WCW - WLAG * 31 - WEB;
             if (lim > 0) { while (*((volatile int *)&cons[w + 1]) < lim) { } }
         }
-        const long long tb = clock64();
-        if (!(a.dbg & 8)) mbar_wait((unsigned)__cvta_generic_to_shared(&bars[w][c % WNS]), (unsigned)((c / WNS) & 1));
+        mbar_wait((unsigned)__cvta_generic_to_shared(&bars[w][c % WNS]), (unsigned)((c / WNS) & 1));
         __syncwarp();
-        const double *sq = ring + (size_t)(c % WNS) * WSLOT;
-        double *zb = zband + (size_t)(c & 1) * WZB;
-        const double *zbp = zband + (size_t)((c + 1) & 1) * WZB;   // chunk c-1's results
-        // Steps in two groups of 8: all shared-memory operands of a group are loaded before its
-        // dependent FMA chain runs (stores to the result band would otherwise pin every load
-        // behind the previous step's store), results are stored after the group.
+        double *sq = ring + (size_t)(c % WNS) * WSLOT;
+        // Two columns per step (the lane skew is two columns, so lane t-1 finished this pair one
+        // step earlier, and the pair shares one 16-byte swizzle unit: one 128-bit load per array);
+        // two groups of 4 steps, operands of a group loaded before its dependent FMA chain.
         auto group = [&](auto fast_tag, auto g_tag) {
             constexpr bool F = decltype(fast_tag)::value;
             constexpr int G = decltype(g_tag)::value;
-            double Q[8], A1[8], A2[8], E[8], YB[8];
+            double2 Q[4], A1[4], A2[4], E[4];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int k = 8 * G + u;
-                const int xo = rowoff + ((((WCW - 1 - k) >> 1) ^ sw) << 1) + ((WCW - 1 - k) & 1);
-                Q[u] = sq[xo]; A1[u] = sq[WBOX + xo]; A2[u] = sq[2 * WBOX + xo];
-                E[u] = ein_src ? ein_src[(c * WCW + k) & (WEB - 1)] : (chain_in ? ein_g[k] : 0.0);
-                if (c > 0) YB[u] = zbp[(2 * k + th) * WZP + WCW - 1 - kk];
+            for (int u = 0; u < 4; ++u) {
+                const int st = 4 * G + u;                           // columns 2st, 2st+1 of the chunk
+                const int xo = rowoff + (((7 - st) ^ sw) << 1);     // unit holding (2st+1, 2st) as (lo, hi)
+                Q[u] = *reinterpret_cast<const double2 *>(sq + xo);
+                A1[u] = *reinterpret_cast<const double2 *>(sq + WBOX + xo);
+                A2[u] = *reinterpret_cast<const double2 *>(sq + 2 * WBOX + xo);
+                if (ein_src) E[u] = *reinterpret_cast<const double2 *>(ein_src + ((c * WCW + 2 * st) & (WEB - 1)));
+                else if (chain_in) E[u] = make_double2(ein_g[2 * st], ein_g[2 * st + 1]);
+                else E[u] = make_double2(0.0, 0.0);
             }
             if (G == 1 && w > 0 && lane == 0) *((volatile int *)&cons[w]) = need;
             double Z[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int k = 8 * G + u;
-                double zN = __shfl_up_sync(0xffffffffu, z2, 1);
-                if (lane == 0) zN = E[u];
-                double z = fma(A2[u], zN, fma(A1[u], z1, Q[u]));
+            for (int u = 0; u < 4; ++u) {
+                const int st = 4 * G + u;
+                double n0 = __shfl_up_sync(0xffffffffu, z2, 1);     // lane t-1's pair of the last step
+                double n1 = __shfl_up_sync(0xffffffffu, z1, 1);
+                if (lane == 0) { n0 = E[u].x; n1 = E[u].y; }
+                double za = fma(A1[u].y, z1, fma(A2[u].y, n0, Q[u].y));   // column 2st   (east one first)
+                double zc = fma(A1[u].x, za, fma(A2[u].x, n1, Q[u].x));   // column 2st+1
                 if (!F) {
-                    const int idx = c * WCW + k - WLAG * lane;
-                    z = (rvalid && idx >= 0 && idx < ncols) ? z : 0.0;
+                    const int idx = c * WCW + 2 * st - WLAG * lane;
+                    za = (rvalid && idx >= 0 && idx < ncols) ? za : 0.0;
+                    zc = (rvalid && idx + 1 >= 0 && idx + 1 < ncols) ? zc : 0.0;
                 }
-                Z[u] = z;
-                z2 = z1; z1 = z;
+                Z[2 * u] = za; Z[2 * u + 1] = zc;
+                z2 = za; z1 = zc;
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int k = 8 * G + u;
-                const int idx = c * WCW + k - WLAG * lane;
-                zb[lane * WZP + k] = Z[u];
-                if (lane == 31 && idx >= 0 && idx < ncols) {
-                    if (has_consumer) edge[w][idx & (WEB - 1)] = Z[u];
-                    if (CHAIN && chain_out) __stcg(a.chain_buf + (long)blockIdx.y * a.chain_ld + idx, Z[u]);
-                }
-                if (c > 0 && !(a.dbg & 4)) {            // interleaved write-back of chunk c-1
-                    const double cdv = YFORM ? cdb[k * 32 + lane] : 1.0;
-                    if (F) a.z[wv0 + k * dwv - (c - 1) * WCW] = YFORM ? cdv * YB[u] : YB[u];
-                    else wb(c - 1, k, cdv);
+            for (int u = 0; u < 4; ++u) {
+                const int st = 4 * G + u;
+                const int xo = rowoff + (((7 - st) ^ sw) << 1);
+                *reinterpret_cast<double2 *>(sq + xo) = make_double2(Z[2 * u + 1], Z[2 * u]);   // y in place of q
+                const int idx = c * WCW + 2 * st - WLAG * lane;
+                if (lane == 31 && idx >= 0 && idx + 1 < ncols) {
+                    if (has_consumer) *reinterpret_cast<double2 *>(&edge[w][idx & (WEB - 1)]) = make_double2(Z[2 * u], Z[2 * u + 1]);
+                    if (CHAIN && chain_out) {
+                        __stcg(a.chain_buf + (long)blockIdx.y * a.chain_ld + idx, Z[2 * u]);
+                        __stcg(a.chain_buf + (long)blockIdx.y * a.chain_ld + idx + 1, Z[2 * u + 1]);
+                    }
+                } else if (lane == 31 && idx >= 0 && idx < ncols) {  // last odd column
+                    if (has_consumer) edge[w][idx & (WEB - 1)] = Z[2 * u];
+                    if (CHAIN && chain_out) __stcg(a.chain_buf + (long)blockIdx.y * a.chain_ld + idx, Z[2 * u]);
                 }
             }
         };
-        const long long tc = clock64();
         if (fast) { group(std::true_type{}, std::integral_constant<int, 0>{}); group(std::true_type{}, std::integral_constant<int, 1>{}); }
         else { group(std::false_type{}, std::integral_constant<int, 0>{}); group(std::false_type{}, std::integral_constant<int, 1>{}); }
-        const long long td = clock64();
-        tp_spin += tb - ta; tp_bar += tc - tb; tp_steps += td - tc; tp_fast += fast;
         const int done = min(ncols, max(0, c * WCW + WCW - WLAG * 31));
+        __syncwarp();
         if (lane == 31) {
             if (has_consumer) {
                 __threadfence_block();
@@ -295,21 +287,14 @@ __global__ void __launch_bounds__(WMAXW * 32) k_wave(WaveArgs a, const __grid_co
             }
             if (chain_out) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.chain_flags + blockIdx.y), "r"(done) : "memory");
         }
-        __syncwarp();
+        // write-back of chunk c-1 (its slot is released afterwards)
+        if (c > 0) {
+            const int cw = c - 1;
+            const bool fastwb = rows_out_all && cw * WCW - WLAG * 31 >= right - out_right && cw * WCW + WCW - 1 < ncols;
+            writeback(cw, fastwb);
+        }
     }
-    if ((a.dbg & 64) && lane == 0 && a.prof) {
-        const long long tot = clock64() - tp0;
-        long long *o = a.prof + 8 * ((blockIdx.y * gridDim.x + blockIdx.x) * 4 + w);
-        o[0] = tot; o[1] = tp_spin; o[2] = tp_bar; o[3] = tp_steps; o[4] = tp_fast; o[5] = nch;
-    }
-    {   // write-back of the last chunk
-        const int c = nch - 1;
-        if (YFORM) asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncwarp();
-        const double *cdb = cdband + (size_t)(c & 1) * WCDB;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) wb(c, e, YFORM ? cdb[e * 32 + lane] : 1.0);
-    }
+    writeback(nch - 1, false);
 }
 
 static size_t wave_smem(int warps) { return sizeof(double) * (size_t)warps * WWARP + 1024; }
@@ -378,31 +363,12 @@ void launch_wave(Ctx *c, WaveArgs a, long rows_v, long rows_c, int warps, bool y
 {
     WaveMaps m;
     if (!wave_maps(c, a, rows_v, rows_c, &m)) { c->sticky = cudaErrorInvalidValue; return; }
-    static int dbg = -1;
-    static long long *prof = nullptr;
-    if (dbg < 0) {
-        const char *e = getenv("SPP_WAVE_DBG"); dbg = e ? atoi(e) : 0;
-        if (dbg & 64) cudaMalloc(&prof, sizeof(long long) * 8 * 4 * 4096);
-    }
-    a.dbg = dbg; a.prof = prof;
     const dim3 grid((a.nl + a.cols_out - 1) / a.cols_out, (a.nl + a.rows_out - 1) / a.rows_out);
     const size_t sm = wave_smem(warps);
     ProfScope ps(c, cls, bytes);
-    if (prof) cudaMemsetAsync(prof, 0, sizeof(long long) * 8 * 4 * 4096, c->st);
-    if (yform) k_wave<true, false><<<grid, warps * 32, sm, c->st>>>(a, m);
-    else k_wave<false, false><<<grid, warps * 32, sm, c->st>>>(a, m);
+    if (yform) k_wave<true, false><<<grid, (warps + 1) * 32, sm, c->st>>>(a, m);
+    else k_wave<false, false><<<grid, (warps + 1) * 32, sm, c->st>>>(a, m);
     c->launches++;
-    if (prof && a.nl >= 2048 && getenv("SPP_WAVE_PROF_DUMP")) {
-        static int dumped = 0;
-        if (!dumped++) {
-            long long h[8 * 4 * 16];
-            cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, c->st);
-            cudaStreamSynchronize(c->st);
-            for (int k = 0; k < 16; ++k)
-                fprintf(stderr, "[wave-prof] cta %d warp %d: total %lld spin %lld bar %lld steps %lld fastchunks %lld nch %lld\n",
-                        k / 4, k % 4, h[8 * k], h[8 * k + 1], h[8 * k + 2], h[8 * k + 3], h[8 * k + 4], h[8 * k + 5]);
-        }
-    }
     dbg_sync(c, "k_wave tiled");
 }
 
@@ -422,8 +388,8 @@ void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform,
     const size_t sm = wave_smem(W);
     void *args[] = {(void *)&a, (void *)&m};
     ProfScope ps(c, cls, bytes);
-    if (yform) cudaLaunchCooperativeKernel((void *)k_wave<true, true>, dim3(1, ncta), dim3(32 * W), args, sm, c->st);
-    else cudaLaunchCooperativeKernel((void *)k_wave<false, true>, dim3(1, ncta), dim3(32 * W), args, sm, c->st);
+    if (yform) cudaLaunchCooperativeKernel((void *)k_wave<true, true>, dim3(1, ncta), dim3(32 * (W + 1)), args, sm, c->st);
+    else cudaLaunchCooperativeKernel((void *)k_wave<false, true>, dim3(1, ncta), dim3(32 * (W + 1)), args, sm, c->st);
     c->launches++;
     dbg_sync(c, "k_wave chain");
 }
@@ -682,18 +648,18 @@ bool launch_coarse_vcycle(Ctx *c, int lc, const double *R)
 // (2RT+1)^2 fine nodes it needs is formed once into shared memory, then gathered.  rho is never
 // written to HBM.
 // ------------------------------------------------------------------------------------------
-constexpr int RT = 32;
-constexpr int RFW = 2 * RT + 1;
-
+template <int RT>
 __global__ void __launch_bounds__(256) k_resid_restrict(int nf, long pv, long pc, const double *__restrict__ e,
     const double *__restrict__ R, const double *__restrict__ aE, const double *__restrict__ aN,
     const double *__restrict__ rr, const double *__restrict__ aW, const double *__restrict__ aS,
     const double *__restrict__ hbf, const double *__restrict__ kbf, int nc, long pvc,
     const double *__restrict__ hbc, const double *__restrict__ kbc, double *bc)
 {
+    constexpr int RFW = 2 * RT + 1;
     __shared__ double s[RFW * RFW];
     const int I0 = (int)blockIdx.x * RT + 1, J0 = (int)blockIdx.y * RT + 1;
     const int fi0 = 2 * I0 - 1, fj0 = 2 * J0 - 1;
+#pragma unroll 4
     for (int p = threadIdx.x; p < RFW * RFW; p += blockDim.x) {
         const int di = p % RFW, dj = p / RFW;
         const int i = fi0 + di, j = fj0 + dj;
@@ -726,10 +692,16 @@ __global__ void __launch_bounds__(256) k_resid_restrict(int nf, long pv, long pc
 void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e)
 {
     Level &F = c->lev[l], &C = c->lev[l + 1];
-    dim3 grid((C.n + RT - 1) / RT, (C.n + RT - 1) / RT);
     ProfScope ps(c, 4, (double)F.n * F.n * 40.0 + 8.0 * C.n * (double)C.n);
-    k_resid_restrict<<<grid, 256, 0, c->st>>>(F.n, F.pitch, F.cpitch, e, R, F.aE, F.aN, F.rr, F.aW, F.aS, F.hb,
-                                               F.kb, C.n, C.pitch, C.hb, C.kb, C.b);
+    // coarse tile edge: enough CTAs to fill the GPU on the small levels
+    const int RTn = C.n >= 512 ? 32 : (C.n >= 128 ? 16 : 8);
+    const dim3 grid((C.n + RTn - 1) / RTn, (C.n + RTn - 1) / RTn);
+#define SPP_RR(T) k_resid_restrict<T><<<grid, T >= 32 ? 256 : (T >= 16 ? 256 : 128), 0, c->st>>>(F.n, F.pitch, \
+        F.cpitch, e, R, F.aE, F.aN, F.rr, F.aW, F.aS, F.hb, F.kb, C.n, C.pitch, C.hb, C.kb, C.b)
+    if (RTn == 32) SPP_RR(32);
+    else if (RTn == 16) SPP_RR(16);
+    else SPP_RR(8);
+#undef SPP_RR
     c->launches++;
 }
 
@@ -864,7 +836,15 @@ cudaError_t setup_mg_tiles(Ctx *c)
             L.halo_y = halo;
             L.tile_rows = rows_cta - halo;
             L.halo_x = halo;
-            L.tile_cols = std::min(n, T.gs_tile_cols);
+            // column tiles: the time of a tile grows with its width (wavefront chunks), so use as
+            // many column tiles as fit one wave of one CTA per SM (>= 64 columns each)
+            const int nrt = (n + L.tile_rows - 1) / L.tile_rows;
+            int nct = std::max(1, c->sm_count / nrt);
+            nct = std::min(nct, std::max(1, n / 64));
+            int tc = (n + nct - 1) / nct;
+            tc = (tc + 15) / 16 * 16;
+            if (T.gs_tile_cols > 0) tc = std::min(n, T.gs_tile_cols);
+            L.tile_cols = std::min(n, tc);
             if (L.tile_cols >= n) { L.tile_cols = n; L.halo_x = 0; }
         }
     }

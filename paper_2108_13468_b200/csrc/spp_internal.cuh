@@ -66,14 +66,13 @@ struct WaveArgs {
     double *z;
     int rows_out, cols_out, halo_y, halo_x;
     int *chain_flags; double *chain_buf; long chain_ld;   // exact chained mode
-    int dbg;                             // debugging switches (0 in production)
-    long long *prof;                     // dbg & 64: per-warp cycle counters
+
 };
 
 // tunables (defaults in spp_create; overridable through SPP_TUNE="key=val,..." for experiments)
 struct Tune {
     int gs_warps = 4;          // warps (32-row strips) per GS tile
-    int gs_tile_cols = 512;    // output columns per GS tile
+    int gs_tile_cols = 0;      // output columns per GS tile (0: one wave of CTAs per level)
     int gs_max_halo = 128;     // no certified halo below this -> exact chained sweep
     int sweep_warps = 4;       // warps per CTA of the exact chained sweep (M_II)
     int coarse_max = 64;       // levels with n <= this run as one fused single-CTA V-cycle

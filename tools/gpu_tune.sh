@@ -2,7 +2,7 @@
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1
 tail -3 gpurun_out/gpu_tests.log
-for t in ""; do
+for t in "" "gs_tile_cols=512" "gs_tile_cols=256"; do
   echo "=== SPP_TUNE=$t" >> gpurun_out/tune.log
   SPP_TUNE="$t" timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --profile-all >> gpurun_out/tune.log 2>&1
 done
