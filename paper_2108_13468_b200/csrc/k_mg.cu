@@ -66,11 +66,18 @@ __device__ __forceinline__ void cp_async8(double *dst, const double *src, bool v
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
 }
 
-__device__ __forceinline__ int ld_acquire(const int *p)
+// chain inflow slots are preset to this NaN (all bits set); the sweep only produces values by
+// fma/select, whose NaNs are canonical (0x7fff...), never this pattern
+constexpr unsigned long long kChainSentinel = ~0ull;
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p)
 {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ void st_relaxed(double *p, double v)
+{
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
 }
 __device__ __forceinline__ void tma_load(unsigned dst, const CUtensorMap *tm, int x, int y, unsigned bar)
 {
@@ -93,6 +100,7 @@ __global__ void __launch_bounds__((WMAXW + 1) * 32) k_wave(WaveArgs a, const __g
     extern __shared__ double smem_raw[];
     __shared__ double edge[WMAXW][WEB];
     __shared__ int prod[WMAXW], cons[WMAXW];
+    __shared__ __align__(16) double cin[WCW];          // chain inflow of the chunk (warp 0)
     // full: the TMA of (warp, slot) landed; empty: the warp is done with the slot (steps and the
     // write-back of its results, which happens one chunk later)
     __shared__ __align__(8) unsigned long long bars[WMAXW][WNS], ebars[WMAXW][WNS];
@@ -168,32 +176,44 @@ __global__ void __launch_bounds__((WMAXW + 1) * 32) k_wave(WaveArgs a, const __g
     // write-back mapping: element e -> band row t = 2e + lane/16, box column x' = lane%16
     // (chunk column k = 15 - x'), grid row wtop - t, column right - 16c - 15 + x' + 2t
     const int th = lane >> 4, kk = lane & 15;
-    const int tmax = wtop - out_bot;
     const int pv = (int)a.pv;
-    const int wv0 = (wtop - th + a.joff) * pv + right - (WCW - 1) + kk + WLAG * th + a.ioff;
+    double *const zw = a.z + ((wtop - th + a.joff) * pv + right - (WCW - 1) + kk + WLAG * th + a.ioff);
     const int dwv = 2 * WLAG - 2 * pv;
+    unsigned rowmask = 0;                               // elements whose row is an output row
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const int t = 2 * e + th;
+        if (wtop - t >= out_bot && wtop - t <= out_top) rowmask |= 1u << e;
+    }
+    // element e of chunk cw has sweep index idx = cw*16 + 15 - kk - WLAG*th - 2*WLAG*e; it is an
+    // output column when lo <= idx < ncols (lo = right - out_right): a contiguous range of e
+    const int wb_lo = right - out_right;
+    const int wb_b0 = (WCW - 1) - kk - WLAG * th;
+    auto wb_mask = [&](int cw) -> unsigned {
+        const int base = cw * WCW + wb_b0;
+        const int emax = (base - wb_lo) >> 2;           // floor division (2*WLAG = 4)
+        const int emin = ((base - ncols) >> 2) + 1;
+        if (emax < 0 || emin > 15) return 0u;
+        const unsigned hi = emax >= 15 ? 0xffffu : ((2u << emax) - 1u);
+        const unsigned lo = emin <= 0 ? 0u : ((1u << emin) - 1u);
+        return rowmask & hi & ~lo;
+    };
     auto wb_off = [&](int e) {                          // swizzled box offset of element e
         const int br = 31 - (2 * e + th);
         return br * WCW + ((((kk >> 1) ^ (br & 7))) << 1) + (kk & 1);
     };
+    static_assert(WLAG == 2, "wb_mask divides by 2*WLAG with a shift");
+    unsigned long long vin = kChainSentinel;            // chain inflow value in flight (warp 0)
     const bool rows_all = wtop - 31 >= out_bot;         // all 32 rows of the warp are swept rows
-    const bool rows_out_all = rows_all && wtop <= out_top;   // ... and output rows
     double z1 = 0.0, z2 = 0.0;                          // own results of the last step (pair)
-    // write-back of chunk cw (results in place of q in its slot): 16 elements per lane
-    auto writeback = [&](int cw, bool fastwb) {
-        const double *sl = ring + (size_t)(cw % WNS) * WSLOT;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int o = wb_off(e);
-            const double y = sl[o];
-            const double v = YFORM ? sl[3 * WBOX + o] * y : y;
-            if (fastwb) a.z[wv0 + e * dwv - cw * WCW] = v;
-            else {
-                const int t = 2 * e + th, idx = cw * WCW + (WCW - 1 - kk) - WLAG * t, col = right - idx;
-                if (t <= tmax && wtop - t <= out_top && idx >= 0 && idx < ncols && col <= out_right)
-                    a.z[wv0 + e * dwv - cw * WCW] = v;
-            }
-        }
+#ifdef SPP_WAVE_PROF
+    long long tp_spin = 0, tp_bar = 0, tp_steps = 0, tp_wb = 0;
+    const long long tp0 = clock64();
+#define SPP_TP(v) const long long v = clock64()
+#else
+#define SPP_TP(v)
+#endif
+    auto release = [&](int cw) {                        // the warp is done with slot cw % WNS
         __syncwarp();
         if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(&ebars[w][cw % WNS])) : "memory");
     };
@@ -202,82 +222,122 @@ __global__ void __launch_bounds__((WMAXW + 1) * 32) k_wave(WaveArgs a, const __g
         const bool fast = rows_all && c * WCW - WLAG * 31 >= 0 && c * WCW + WCW - 1 < ncols;
         // North inflow of lane 0 for the columns of this chunk (all wait loops warp-uniform: a
         // lane-divergent spin sends the shuffles below down the slow emulation path)
+        SPP_TP(ta);
         const int need = min(ncols, c * WCW + WCW);
-        const double *ein_src = nullptr;
-        double ein_g[WCW];
         if (w > 0) {
-            while (*((volatile int *)&prod[w - 1]) < need) { }
+            while (*((volatile int *)&prod[w - 1]) < need) __nanosleep(32);   // back off: spinning loads slow the working warps' smem traffic
             __threadfence_block();
-            ein_src = &edge[w - 1][0];
         } else if (chain_in) {
-            while (ld_acquire(a.chain_flags + blockIdx.y - 1) < need) { }
-            const double *src = a.chain_buf + (long)(blockIdx.y - 1) * a.chain_ld;
-#pragma unroll
-            for (int k = 0; k < WCW; ++k) ein_g[k] = (c * WCW + k < ncols) ? __ldcg(src + c * WCW + k) : 0.0;
+            // the strip above publishes its bottom row value by value into a buffer preset to the
+            // sentinel (no fence on the producer side): lanes 0..15 poll the chunk's 16 columns
+            // (the load for chunk c was issued during chunk c-1: vin, so the L2 round trip overlaps
+            // the steps; only a value not yet published is polled again)
+            const unsigned long long *src = reinterpret_cast<const unsigned long long *>(
+                a.chain_buf + (long)(blockIdx.y - 1) * a.chain_ld) + c * WCW + (lane & 15);
+            const bool mine = lane < 16 && c * WCW + lane < ncols;
+            if (c == 0 && mine) vin = ld_relaxed_u64(src);
+            for (unsigned spins = 0; !__all_sync(0xffffffffu, !mine || vin != kChainSentinel); ++spins) {
+                if (spins > (1u << 26)) __trap();       // a lost value: fail the launch, never hang
+                __nanosleep(32);
+                if (mine) vin = ld_relaxed_u64(src);
+            }
+            if (lane < 16) cin[lane] = mine ? __longlong_as_double((long long)vin) : 0.0;
+            __syncwarp();
+            if (lane < 16 && (c + 1) * WCW + lane < ncols) vin = ld_relaxed_u64(src + WCW);   // chunk c+1
         }
         if (has_consumer) {                             // back-pressure on the edge ring
             const int lim = c * WCW + WCW - WLAG * 31 - WEB;
-            if (lim > 0) { while (*((volatile int *)&cons[w + 1]) < lim) { } }
+            if (lim > 0) { while (*((volatile int *)&cons[w + 1]) < lim) __nanosleep(32); }
         }
+        SPP_TP(tb);
         mbar_wait((unsigned)__cvta_generic_to_shared(&bars[w][c % WNS]), (unsigned)((c / WNS) & 1));
         __syncwarp();
+        SPP_TP(tc);
         double *sq = ring + (size_t)(c % WNS) * WSLOT;
         // Two columns per step (the lane skew is two columns, so lane t-1 finished this pair one
-        // step earlier, and the pair shares one 16-byte swizzle unit: one 128-bit load per array);
-        // two groups of 4 steps, operands of a group loaded before its dependent FMA chain.
-        auto group = [&](auto fast_tag, auto g_tag) {
+        // step earlier, and the pair shares one 16-byte swizzle unit: one 128-bit load per array).
+        // Every shared-memory load of the chunk (operands, inflow, and the results of chunk c-1
+        // for the write-back) is issued before the first store: a store ahead of a possibly
+        // aliasing load would serialise the load behind it. The write-back of chunk c-1 is
+        // branch-free (predicated stores) and shares the basic block of the step chain, so its
+        // instructions fill the chain's latency bubbles.
+        double2 Q[8], A1[8], A2[8], E[8];
+#pragma unroll
+        for (int st = 0; st < 8; ++st) {                        // columns 2st, 2st+1 of the chunk
+            const int xo = rowoff + (((7 - st) ^ sw) << 1);     // unit holding (2st+1, 2st) as (lo, hi)
+            Q[st] = *reinterpret_cast<const double2 *>(sq + xo);
+            A1[st] = *reinterpret_cast<const double2 *>(sq + WBOX + xo);
+            A2[st] = *reinterpret_cast<const double2 *>(sq + 2 * WBOX + xo);
+        }
+        if (w > 0) {
+#pragma unroll
+            for (int st = 0; st < 8; ++st) E[st] = *reinterpret_cast<const double2 *>(&edge[w - 1][(c * WCW + 2 * st) & (WEB - 1)]);
+        } else if (chain_in) {
+#pragma unroll
+            for (int st = 0; st < 8; ++st) E[st] = *reinterpret_cast<const double2 *>(&cin[2 * st]);
+        } else {
+#pragma unroll
+            for (int st = 0; st < 8; ++st) E[st] = make_double2(0.0, 0.0);
+        }
+        if (w > 0 && lane == 0) *((volatile int *)&cons[w]) = need;
+        // results (y) and cd of chunk c-1 for the write-back
+        const int cw = c - 1;
+        const unsigned wmask = c > 0 ? wb_mask(cw) : 0u;
+        const double *sl = ring + (size_t)((c + WNS - 1) % WNS) * WSLOT;
+        double Y[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int o = wb_off(e);
+            Y[e] = YFORM ? sl[3 * WBOX + o] * sl[o] : sl[o];
+        }
+        if (c > 0) release(cw);                         // chunk c-1's slot is free once Y is in registers
+        double *const zc_ = zw - cw * WCW;
+        auto steps = [&](auto fast_tag) {
             constexpr bool F = decltype(fast_tag)::value;
-            constexpr int G = decltype(g_tag)::value;
-            double2 Q[4], A1[4], A2[4], E[4];
+            double Z[16];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int st = 4 * G + u;                           // columns 2st, 2st+1 of the chunk
-                const int xo = rowoff + (((7 - st) ^ sw) << 1);     // unit holding (2st+1, 2st) as (lo, hi)
-                Q[u] = *reinterpret_cast<const double2 *>(sq + xo);
-                A1[u] = *reinterpret_cast<const double2 *>(sq + WBOX + xo);
-                A2[u] = *reinterpret_cast<const double2 *>(sq + 2 * WBOX + xo);
-                if (ein_src) E[u] = *reinterpret_cast<const double2 *>(ein_src + ((c * WCW + 2 * st) & (WEB - 1)));
-                else if (chain_in) E[u] = make_double2(ein_g[2 * st], ein_g[2 * st + 1]);
-                else E[u] = make_double2(0.0, 0.0);
-            }
-            if (G == 1 && w > 0 && lane == 0) *((volatile int *)&cons[w]) = need;
-            double Z[8];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int st = 4 * G + u;
-                double n0 = __shfl_up_sync(0xffffffffu, z2, 1);     // lane t-1's pair of the last step
+            for (int st = 0; st < 8; ++st) {
+                double n0 = __shfl_up_sync(0xffffffffu, z2, 1);    // lane t-1's pair of the last step
                 double n1 = __shfl_up_sync(0xffffffffu, z1, 1);
-                if (lane == 0) { n0 = E[u].x; n1 = E[u].y; }
-                double za = fma(A1[u].y, z1, fma(A2[u].y, n0, Q[u].y));   // column 2st   (east one first)
-                double zc = fma(A1[u].x, za, fma(A2[u].x, n1, Q[u].x));   // column 2st+1
+                if (lane == 0) { n0 = E[st].x; n1 = E[st].y; }
+                double za = fma(A1[st].y, z1, fma(A2[st].y, n0, Q[st].y));   // column 2st   (east one first)
+                double zc = fma(A1[st].x, za, fma(A2[st].x, n1, Q[st].x));   // column 2st+1
                 if (!F) {
                     const int idx = c * WCW + 2 * st - WLAG * lane;
                     za = (rvalid && idx >= 0 && idx < ncols) ? za : 0.0;
                     zc = (rvalid && idx + 1 >= 0 && idx + 1 < ncols) ? zc : 0.0;
                 }
-                Z[2 * u] = za; Z[2 * u + 1] = zc;
+                Z[2 * st] = za; Z[2 * st + 1] = zc;
                 z2 = za; z1 = zc;
+                // interleave two write-back stores of chunk c-1 per step
+#pragma unroll
+                for (int e = 2 * st; e < 2 * st + 2; ++e)
+                    if (wmask & (1u << e)) zc_[e * dwv] = Y[e];
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int st = 4 * G + u;
+            for (int st = 0; st < 8; ++st) {
                 const int xo = rowoff + (((7 - st) ^ sw) << 1);
-                *reinterpret_cast<double2 *>(sq + xo) = make_double2(Z[2 * u + 1], Z[2 * u]);   // y in place of q
-                const int idx = c * WCW + 2 * st - WLAG * lane;
-                if (lane == 31 && idx >= 0 && idx + 1 < ncols) {
-                    if (has_consumer) *reinterpret_cast<double2 *>(&edge[w][idx & (WEB - 1)]) = make_double2(Z[2 * u], Z[2 * u + 1]);
-                    if (CHAIN && chain_out) {
-                        __stcg(a.chain_buf + (long)blockIdx.y * a.chain_ld + idx, Z[2 * u]);
-                        __stcg(a.chain_buf + (long)blockIdx.y * a.chain_ld + idx + 1, Z[2 * u + 1]);
+                *reinterpret_cast<double2 *>(sq + xo) = make_double2(Z[2 * st + 1], Z[2 * st]);   // y in place of q
+            }
+            if (lane == 31) {                                   // hand the bottom row to the next strip
+                double *eo = &edge[w][0];
+                double *co = CHAIN ? a.chain_buf + (long)blockIdx.y * a.chain_ld : nullptr;
+#pragma unroll
+                for (int st = 0; st < 8; ++st) {
+                    const int idx = c * WCW + 2 * st - WLAG * 31;
+                    if (F || (idx >= 0 && idx + 1 < ncols)) {
+                        if (has_consumer) *reinterpret_cast<double2 *>(eo + (idx & (WEB - 1))) = make_double2(Z[2 * st], Z[2 * st + 1]);
+                        if (CHAIN && chain_out) { st_relaxed(co + idx, Z[2 * st]); st_relaxed(co + idx + 1, Z[2 * st + 1]); }
+                    } else if (idx >= 0 && idx < ncols) {   // last odd column
+                        if (has_consumer) eo[idx & (WEB - 1)] = Z[2 * st];
+                        if (CHAIN && chain_out) st_relaxed(co + idx, Z[2 * st]);
                     }
-                } else if (lane == 31 && idx >= 0 && idx < ncols) {  // last odd column
-                    if (has_consumer) edge[w][idx & (WEB - 1)] = Z[2 * u];
-                    if (CHAIN && chain_out) __stcg(a.chain_buf + (long)blockIdx.y * a.chain_ld + idx, Z[2 * u]);
                 }
             }
         };
-        if (fast) { group(std::true_type{}, std::integral_constant<int, 0>{}); group(std::true_type{}, std::integral_constant<int, 1>{}); }
-        else { group(std::false_type{}, std::integral_constant<int, 0>{}); group(std::false_type{}, std::integral_constant<int, 1>{}); }
+        if (fast) steps(std::true_type{});
+        else steps(std::false_type{});
+        SPP_TP(td);
         const int done = min(ncols, max(0, c * WCW + WCW - WLAG * 31));
         __syncwarp();
         if (lane == 31) {
@@ -285,19 +345,53 @@ __global__ void __launch_bounds__((WMAXW + 1) * 32) k_wave(WaveArgs a, const __g
                 __threadfence_block();
                 *((volatile int *)&prod[w]) = done;
             }
-            if (chain_out) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.chain_flags + blockIdx.y), "r"(done) : "memory");
         }
-        // write-back of chunk c-1 (its slot is released afterwards)
-        if (c > 0) {
-            const int cw = c - 1;
-            const bool fastwb = rows_out_all && cw * WCW - WLAG * 31 >= right - out_right && cw * WCW + WCW - 1 < ncols;
-            writeback(cw, fastwb);
-        }
+#ifdef SPP_WAVE_PROF
+        SPP_TP(te);
+        tp_spin += tb - ta; tp_bar += tc - tb; tp_steps += td - tc; tp_wb += te - td;
+#endif
     }
-    writeback(nch - 1, false);
+    {                                                   // write-back of the last chunk
+        const int cw = nch - 1;
+        const unsigned wmask = wb_mask(cw);
+        const double *sl = ring + (size_t)(cw % WNS) * WSLOT;
+        double *const zc_ = zw - cw * WCW;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int o = wb_off(e);
+            const double y = YFORM ? sl[3 * WBOX + o] * sl[o] : sl[o];
+            if (wmask & (1u << e)) zc_[e * dwv] = y;
+        }
+        release(cw);
+    }
+#ifdef SPP_WAVE_PROF
+    if (lane == 0 && a.prof) {
+        long long *o = a.prof + 8 * ((blockIdx.y * gridDim.x + blockIdx.x) * 4 + w);
+        o[0] = clock64() - tp0; o[1] = tp_spin; o[2] = tp_bar; o[3] = tp_steps; o[4] = tp_wb; o[5] = nch;
+    }
+#endif
 }
 
 static size_t wave_smem(int warps) { return sizeof(double) * (size_t)warps * WWARP + 1024; }
+
+#ifdef SPP_WAVE_PROF
+// debugging build only: per-warp cycle breakdown of the first launch of each kind
+static void wave_prof_dump(Ctx *c, long long *prof, const char *what, int nctas)
+{
+    static int done_tiled = 0, done_chain = 0;
+    if (!what) return;
+    int &d = what[0] == 'c' ? done_chain : done_tiled;
+    if (d++) return;
+    const int nw = std::min(nctas, 16) * 4;
+    long long h[8 * 64];
+    cudaMemcpyAsync(h, prof, sizeof(long long) * 8 * nw, cudaMemcpyDeviceToHost, c->st);
+    cudaStreamSynchronize(c->st);
+    for (int k = 0; k < nw; ++k)
+        if (h[8 * k])
+            fprintf(stderr, "[wave-prof] %s cta %d warp %d: total %lld spin %lld bar %lld steps %lld wb %lld nch %lld\n",
+                    what, k / 4, k % 4, h[8 * k], h[8 * k + 1], h[8 * k + 2], h[8 * k + 3], h[8 * k + 4], h[8 * k + 5]);
+}
+#endif
 
 // SPP_DEBUG_SYNC=1: synchronise and report after every launch of this file (debugging aid)
 static void dbg_sync(Ctx *c, const char *what)
@@ -366,9 +460,17 @@ void launch_wave(Ctx *c, WaveArgs a, long rows_v, long rows_c, int warps, bool y
     const dim3 grid((a.nl + a.cols_out - 1) / a.cols_out, (a.nl + a.rows_out - 1) / a.rows_out);
     const size_t sm = wave_smem(warps);
     ProfScope ps(c, cls, bytes);
+#ifdef SPP_WAVE_PROF
+    static long long *prof = nullptr;
+    if (!prof) cudaMalloc(&prof, sizeof(long long) * 8 * 4 * 8192);
+    a.prof = prof;
+#endif
     if (yform) k_wave<true, false><<<grid, (warps + 1) * 32, sm, c->st>>>(a, m);
     else k_wave<false, false><<<grid, (warps + 1) * 32, sm, c->st>>>(a, m);
     c->launches++;
+#ifdef SPP_WAVE_PROF
+    wave_prof_dump(c, prof, a.nl >= c->n ? "tiled level 0" : nullptr, grid.x * grid.y);
+#endif
     dbg_sync(c, "k_wave tiled");
 }
 
@@ -384,13 +486,21 @@ void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform,
     a.chain_flags = c->chain_flags;
     a.chain_buf = c->chain;
     a.chain_ld = c->chain_ld;
-    cudaMemsetAsync(c->chain_flags, 0, sizeof(int) * (ncta + 1), c->st);
+    cudaMemsetAsync(c->chain, 0xff, sizeof(double) * (size_t)ncta * c->chain_ld, c->st);   // kChainSentinel
     const size_t sm = wave_smem(W);
     void *args[] = {(void *)&a, (void *)&m};
     ProfScope ps(c, cls, bytes);
+#ifdef SPP_WAVE_PROF
+    static long long *prof = nullptr;
+    if (!prof) cudaMalloc(&prof, sizeof(long long) * 8 * 4 * 8192);
+    a.prof = prof;
+#endif
     if (yform) cudaLaunchCooperativeKernel((void *)k_wave<true, true>, dim3(1, ncta), dim3(32 * (W + 1)), args, sm, c->st);
     else cudaLaunchCooperativeKernel((void *)k_wave<false, true>, dim3(1, ncta), dim3(32 * (W + 1)), args, sm, c->st);
     c->launches++;
+#ifdef SPP_WAVE_PROF
+    wave_prof_dump(c, prof, "chain", ncta);
+#endif
     dbg_sync(c, "k_wave chain");
 }
 

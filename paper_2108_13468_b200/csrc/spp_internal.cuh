@@ -66,6 +66,7 @@ struct WaveArgs {
     double *z;
     int rows_out, cols_out, halo_y, halo_x;
     int *chain_flags; double *chain_buf; long chain_ld;   // exact chained mode
+    long long *prof;                     // SPP_WAVE_PROF builds only
 
 };
 
