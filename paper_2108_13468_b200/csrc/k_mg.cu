@@ -75,6 +75,12 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int ld_acquire_cta(const int *p)
+{
+    int v;
+    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_relaxed(double *p, double v)
 {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
@@ -95,22 +101,24 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity)
 }
 
 template <bool YFORM, bool CHAIN>
-__global__ void __launch_bounds__((WMAXW + 1) * 32) k_wave(WaveArgs a, const __grid_constant__ WaveMaps m)
+__global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const __grid_constant__ WaveMaps m)
 {
     extern __shared__ double smem_raw[];
     __shared__ double edge[WMAXW][WEB];
     __shared__ int prod[WMAXW], cons[WMAXW];
     __shared__ __align__(16) double cin[WCW];          // chain inflow of the chunk (warp 0)
-    // full: the TMA of (warp, slot) landed; empty: the warp is done with the slot (steps and the
-    // write-back of its results, which happens one chunk later)
-    __shared__ __align__(8) unsigned long long bars[WMAXW][WNS], ebars[WMAXW][WNS];
-    // warps 0..W-1 sweep 32-row strips; warp W is the TMA producer (lane w serves warp w)
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = (blockDim.x >> 5) - 1;
+    // Per (sweeping warp, slot): full = the TMA boxes landed; ready = the sweeping warp stored its
+    // results in the slot; empty = the write-back warp stored them to global memory (slot free).
+    __shared__ __align__(8) unsigned long long bars[WMAXW][WNS], rbars[WMAXW][WNS], ebars[WMAXW][WNS];
+    // warps 0..W-1 sweep 32-row strips; warp W+w writes back the results of warp w; warp 2W is
+    // the TMA producer (lane w serves warp w)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = ((blockDim.x >> 5) - 1) / 2;
     if (threadIdx.x < WMAXW) { prod[threadIdx.x] = 0; cons[threadIdx.x] = 0; }
-    if (w < W && lane == 0)
+    if (wid < W && lane == 0)
         for (int s = 0; s < WNS; ++s) {
-            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&bars[w][s])));
-            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&ebars[w][s])));
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&bars[wid][s])));
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&rbars[wid][s])));
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&ebars[wid][s])));
         }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
@@ -132,7 +140,7 @@ __global__ void __launch_bounds__((WMAXW + 1) * 32) k_wave(WaveArgs a, const __g
     // 128B-swizzled TMA boxes need 1 KB aligned shared memory (pointer arithmetic on the shared
     // array keeps the accesses in the shared state space: LDS/STS, not generic LD/ST)
     double *smem = smem_raw + (((1024u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u) >> 3);
-    if (w == W) {                                       // ---- TMA producer warp ----
+    if (wid == 2 * W) {                                 // ---- TMA producer warp ----
         const int pw = lane;
         const int pwtop = top - 32 * pw;
         if (pw >= W || pwtop < out_bot) return;
@@ -161,51 +169,78 @@ __global__ void __launch_bounds__((WMAXW + 1) * 32) k_wave(WaveArgs a, const __g
         }
         return;
     }
+    const bool wbw = wid >= W;                          // write-back warp
+    const int w = wbw ? wid - W : wid;                  // the sweeping warp (strip) served
     const int wtop = top - 32 * w;
-    if (wtop < out_bot) return;                         // no rows for this warp
+    if (wtop < out_bot) return;                         // no rows for this strip
+    double *ring = smem + (size_t)w * WWARP;
+    if (wbw) {                                          // ---- write-back warp ----
+        // element e -> band row t = 2e + lane/16, box column x' = lane%16 (chunk column
+        // k = 15 - x'), grid row wtop - t, column right - 16c - 15 + x' + 2t: two coalesced
+        // 128-byte row segments per instruction
+        const int th = lane >> 4, kk = lane & 15;
+        const int pv = (int)a.pv;
+        double *const zw = a.z + ((wtop - th + a.joff) * pv + right - (WCW - 1) + kk + WLAG * th + a.ioff);
+        const int dwv = 2 * WLAG - 2 * pv;
+        unsigned rowmask = 0;                           // elements whose row is an output row
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int t = 2 * e + th;
+            if (wtop - t >= out_bot && wtop - t <= out_top) rowmask |= 1u << e;
+        }
+        // element e of chunk c has sweep index idx = 16c + 15 - kk - WLAG*th - 2*WLAG*e; it is
+        // an output column when lo <= idx < ncols (lo = right - out_right): a contiguous e range
+        static_assert(WLAG == 2, "the write-back mask divides by 2*WLAG with a shift");
+        const int wb_lo = right - out_right;
+        const int wb_b0 = (WCW - 1) - kk - WLAG * th;
+        int offs[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const int br = 31 - (2 * e + th);
+            offs[e] = br * WCW + ((((kk >> 1) ^ (br & 7))) << 1) + (kk & 1);
+        }
+        for (int c = 0; c < nch; ++c) {
+            const int base = c * WCW + wb_b0;
+            const int emax = (base - wb_lo) >> 2;       // floor division (2*WLAG = 4)
+            const int emin = ((base - ncols) >> 2) + 1;
+            unsigned msk = 0u;
+            if (emax >= 0 && emin <= 15) {
+                const unsigned hi = emax >= 15 ? 0xffffu : ((2u << emax) - 1u);
+                const unsigned lo = emin <= 0 ? 0u : ((1u << emin) - 1u);
+                msk = rowmask & hi & ~lo;
+            }
+            mbar_wait((unsigned)__cvta_generic_to_shared(&rbars[w][c % WNS]), (unsigned)((c / WNS) & 1));
+            const double *sl = ring + (size_t)(c % WNS) * WSLOT;
+            double *zp = zw - c * WCW;
+            double v[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = YFORM ? sl[3 * WBOX + offs[e]] * sl[offs[e]] : sl[offs[e]];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                if (msk & (1u << e)) *zp = v[e];
+                zp += dwv;
+            }
+            __syncwarp();                               // every lane's loads of the slot consumed
+            if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(&ebars[w][c % WNS])) : "memory");
+        }
+        return;
+    }
+    // ---- sweeping warp ----
     const int nwa = min(W, (top - out_bot) / 32 + 1);
     const bool has_consumer = w + 1 < nwa;
     const bool chain_in = CHAIN && w == 0 && blockIdx.y > 0;
     const bool chain_out = CHAIN && w == nwa - 1 && (int)blockIdx.y + 1 < (int)gridDim.y;
-    double *ring = smem + (size_t)w * WWARP;
     // this lane's row; element (box row 31-t, column x') lives at double offset
     // (31-t)*16 + ((x'/2) ^ ((31-t)&7))*2 + (x'&1)   (128B swizzle)
     const int rowoff = (31 - lane) * WCW, sw = (31 - lane) & 7;
     const int row = wtop - lane;
     const bool rvalid = row >= out_bot;
-    // write-back mapping: element e -> band row t = 2e + lane/16, box column x' = lane%16
-    // (chunk column k = 15 - x'), grid row wtop - t, column right - 16c - 15 + x' + 2t
-    const int th = lane >> 4, kk = lane & 15;
-    const int pv = (int)a.pv;
-    double *const zw = a.z + ((wtop - th + a.joff) * pv + right - (WCW - 1) + kk + WLAG * th + a.ioff);
-    const int dwv = 2 * WLAG - 2 * pv;
-    unsigned rowmask = 0;                               // elements whose row is an output row
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-        const int t = 2 * e + th;
-        if (wtop - t >= out_bot && wtop - t <= out_top) rowmask |= 1u << e;
-    }
-    // element e of chunk cw has sweep index idx = cw*16 + 15 - kk - WLAG*th - 2*WLAG*e; it is an
-    // output column when lo <= idx < ncols (lo = right - out_right): a contiguous range of e
-    const int wb_lo = right - out_right;
-    const int wb_b0 = (WCW - 1) - kk - WLAG * th;
-    auto wb_mask = [&](int cw) -> unsigned {
-        const int base = cw * WCW + wb_b0;
-        const int emax = (base - wb_lo) >> 2;           // floor division (2*WLAG = 4)
-        const int emin = ((base - ncols) >> 2) + 1;
-        if (emax < 0 || emin > 15) return 0u;
-        const unsigned hi = emax >= 15 ? 0xffffu : ((2u << emax) - 1u);
-        const unsigned lo = emin <= 0 ? 0u : ((1u << emin) - 1u);
-        return rowmask & hi & ~lo;
-    };
-    auto wb_off = [&](int e) {                          // swizzled box offset of element e
-        const int br = 31 - (2 * e + th);
-        return br * WCW + ((((kk >> 1) ^ (br & 7))) << 1) + (kk & 1);
-    };
-    static_assert(WLAG == 2, "wb_mask divides by 2*WLAG with a shift");
-    unsigned long long vin = kChainSentinel;            // chain inflow value in flight (warp 0)
     const bool rows_all = wtop - 31 >= out_bot;         // all 32 rows of the warp are swept rows
+    unsigned long long vin = kChainSentinel;            // chain inflow value in flight (warp 0)
     double z1 = 0.0, z2 = 0.0;                          // own results of the last step (pair)
+    int xo[8];                                          // swizzled offsets of this lane's pairs
+#pragma unroll
+    for (int st = 0; st < 8; ++st) xo[st] = rowoff + (((7 - st) ^ sw) << 1);
 #ifdef SPP_WAVE_PROF
     long long tp_spin = 0, tp_bar = 0, tp_steps = 0, tp_wb = 0;
     const long long tp0 = clock64();
@@ -213,10 +248,6 @@ __global__ void __launch_bounds__((WMAXW + 1) * 32) k_wave(WaveArgs a, const __g
 #else
 #define SPP_TP(v)
 #endif
-    auto release = [&](int cw) {                        // the warp is done with slot cw % WNS
-        __syncwarp();
-        if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(&ebars[w][cw % WNS])) : "memory");
-    };
     for (int c = 0; c < nch; ++c) {
         // interior chunks (warp-uniform test): every lane's element valid
         const bool fast = rows_all && c * WCW - WLAG * 31 >= 0 && c * WCW + WCW - 1 < ncols;
@@ -225,8 +256,7 @@ __global__ void __launch_bounds__((WMAXW + 1) * 32) k_wave(WaveArgs a, const __g
         SPP_TP(ta);
         const int need = min(ncols, c * WCW + WCW);
         if (w > 0) {
-            while (*((volatile int *)&prod[w - 1]) < need) __nanosleep(32);   // back off: spinning loads slow the working warps' smem traffic
-            __threadfence_block();
+            while (ld_acquire_cta(&prod[w - 1]) < need) __nanosleep(32);   // back off: spinning loads slow the working warps' smem traffic
         } else if (chain_in) {
             // the strip above publishes its bottom row value by value into a buffer preset to the
             // sentinel (no fence on the producer side): lanes 0..15 poll the chunk's 16 columns
@@ -256,18 +286,14 @@ __global__ void __launch_bounds__((WMAXW + 1) * 32) k_wave(WaveArgs a, const __g
         double *sq = ring + (size_t)(c % WNS) * WSLOT;
         // Two columns per step (the lane skew is two columns, so lane t-1 finished this pair one
         // step earlier, and the pair shares one 16-byte swizzle unit: one 128-bit load per array).
-        // Every shared-memory load of the chunk (operands, inflow, and the results of chunk c-1
-        // for the write-back) is issued before the first store: a store ahead of a possibly
-        // aliasing load would serialise the load behind it. The write-back of chunk c-1 is
-        // branch-free (predicated stores) and shares the basic block of the step chain, so its
-        // instructions fill the chain's latency bubbles.
+        // Every shared-memory load of the chunk is issued before the first store: a store ahead
+        // of a possibly aliasing load would serialise the load behind it.
         double2 Q[8], A1[8], A2[8], E[8];
 #pragma unroll
         for (int st = 0; st < 8; ++st) {                        // columns 2st, 2st+1 of the chunk
-            const int xo = rowoff + (((7 - st) ^ sw) << 1);     // unit holding (2st+1, 2st) as (lo, hi)
-            Q[st] = *reinterpret_cast<const double2 *>(sq + xo);
-            A1[st] = *reinterpret_cast<const double2 *>(sq + WBOX + xo);
-            A2[st] = *reinterpret_cast<const double2 *>(sq + 2 * WBOX + xo);
+            Q[st] = *reinterpret_cast<const double2 *>(sq + xo[st]);     // (2st+1, 2st) as (lo, hi)
+            A1[st] = *reinterpret_cast<const double2 *>(sq + WBOX + xo[st]);
+            A2[st] = *reinterpret_cast<const double2 *>(sq + 2 * WBOX + xo[st]);
         }
         if (w > 0) {
 #pragma unroll
@@ -280,18 +306,6 @@ __global__ void __launch_bounds__((WMAXW + 1) * 32) k_wave(WaveArgs a, const __g
             for (int st = 0; st < 8; ++st) E[st] = make_double2(0.0, 0.0);
         }
         if (w > 0 && lane == 0) *((volatile int *)&cons[w]) = need;
-        // results (y) and cd of chunk c-1 for the write-back
-        const int cw = c - 1;
-        const unsigned wmask = c > 0 ? wb_mask(cw) : 0u;
-        const double *sl = ring + (size_t)((c + WNS - 1) % WNS) * WSLOT;
-        double Y[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int o = wb_off(e);
-            Y[e] = YFORM ? sl[3 * WBOX + o] * sl[o] : sl[o];
-        }
-        if (c > 0) release(cw);                         // chunk c-1's slot is free once Y is in registers
-        double *const zc_ = zw - cw * WCW;
         auto steps = [&](auto fast_tag) {
             constexpr bool F = decltype(fast_tag)::value;
             double Z[16];
@@ -309,16 +323,10 @@ __global__ void __launch_bounds__((WMAXW + 1) * 32) k_wave(WaveArgs a, const __g
                 }
                 Z[2 * st] = za; Z[2 * st + 1] = zc;
                 z2 = za; z1 = zc;
-                // interleave two write-back stores of chunk c-1 per step
-#pragma unroll
-                for (int e = 2 * st; e < 2 * st + 2; ++e)
-                    if (wmask & (1u << e)) zc_[e * dwv] = Y[e];
             }
 #pragma unroll
-            for (int st = 0; st < 8; ++st) {
-                const int xo = rowoff + (((7 - st) ^ sw) << 1);
-                *reinterpret_cast<double2 *>(sq + xo) = make_double2(Z[2 * st + 1], Z[2 * st]);   // y in place of q
-            }
+            for (int st = 0; st < 8; ++st)
+                *reinterpret_cast<double2 *>(sq + xo[st]) = make_double2(Z[2 * st + 1], Z[2 * st]);   // y in place of q
             if (lane == 31) {                                   // hand the bottom row to the next strip
                 double *eo = &edge[w][0];
                 double *co = CHAIN ? a.chain_buf + (long)blockIdx.y * a.chain_ld : nullptr;
@@ -340,29 +348,13 @@ __global__ void __launch_bounds__((WMAXW + 1) * 32) k_wave(WaveArgs a, const __g
         SPP_TP(td);
         const int done = min(ncols, max(0, c * WCW + WCW - WLAG * 31));
         __syncwarp();
-        if (lane == 31) {
-            if (has_consumer) {
-                __threadfence_block();
-                *((volatile int *)&prod[w]) = done;
-            }
-        }
+        if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(&rbars[w][c % WNS])) : "memory");
+        if (lane == 31 && has_consumer)                 // release: the edge values before the count
+            asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(&prod[w])), "r"(done) : "memory");
 #ifdef SPP_WAVE_PROF
         SPP_TP(te);
         tp_spin += tb - ta; tp_bar += tc - tb; tp_steps += td - tc; tp_wb += te - td;
 #endif
-    }
-    {                                                   // write-back of the last chunk
-        const int cw = nch - 1;
-        const unsigned wmask = wb_mask(cw);
-        const double *sl = ring + (size_t)(cw % WNS) * WSLOT;
-        double *const zc_ = zw - cw * WCW;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int o = wb_off(e);
-            const double y = YFORM ? sl[3 * WBOX + o] * sl[o] : sl[o];
-            if (wmask & (1u << e)) zc_[e * dwv] = y;
-        }
-        release(cw);
     }
 #ifdef SPP_WAVE_PROF
     if (lane == 0 && a.prof) {
@@ -465,8 +457,8 @@ void launch_wave(Ctx *c, WaveArgs a, long rows_v, long rows_c, int warps, bool y
     if (!prof) cudaMalloc(&prof, sizeof(long long) * 8 * 4 * 8192);
     a.prof = prof;
 #endif
-    if (yform) k_wave<true, false><<<grid, (warps + 1) * 32, sm, c->st>>>(a, m);
-    else k_wave<false, false><<<grid, (warps + 1) * 32, sm, c->st>>>(a, m);
+    if (yform) k_wave<true, false><<<grid, (2 * warps + 1) * 32, sm, c->st>>>(a, m);
+    else k_wave<false, false><<<grid, (2 * warps + 1) * 32, sm, c->st>>>(a, m);
     c->launches++;
 #ifdef SPP_WAVE_PROF
     wave_prof_dump(c, prof, a.nl >= c->n ? "tiled level 0" : nullptr, grid.x * grid.y);
@@ -495,8 +487,8 @@ void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform,
     if (!prof) cudaMalloc(&prof, sizeof(long long) * 8 * 4 * 8192);
     a.prof = prof;
 #endif
-    if (yform) cudaLaunchCooperativeKernel((void *)k_wave<true, true>, dim3(1, ncta), dim3(32 * (W + 1)), args, sm, c->st);
-    else cudaLaunchCooperativeKernel((void *)k_wave<false, true>, dim3(1, ncta), dim3(32 * (W + 1)), args, sm, c->st);
+    if (yform) cudaLaunchCooperativeKernel((void *)k_wave<true, true>, dim3(1, ncta), dim3(32 * (2 * W + 1)), args, sm, c->st);
+    else cudaLaunchCooperativeKernel((void *)k_wave<false, true>, dim3(1, ncta), dim3(32 * (2 * W + 1)), args, sm, c->st);
     c->launches++;
 #ifdef SPP_WAVE_PROF
     wave_prof_dump(c, prof, "chain", ncta);
