@@ -28,53 +28,115 @@
 namespace spp {
 
 // ------------------------------------------------------------------------------ setup
-// One thread per line, both chains in one launch (blockIdx.y = chain): chain 0 = X (lines of
-// constant y, j = N-1-l; element k -> i = k+1), chain 1 = Y (lines of constant x, i = N-1-l;
-// element k -> j = k+1).  The Thomas forward sweep (a dependent chain of reciprocals) runs with
-// the coefficient loads of 8 elements issued ahead; the certified contraction
-// kappa_l = max_k (T_l^{-1} c_l)_k is formed in the same kernel (forward part y = al y + e
-// alongside the factorisation, backward part from the scratch copy of y).
+// One lane per line, 32 lines per warp (one warp per CTA), both chains in one launch
+// (blockIdx.y = chain): chain 0 = X (lines of constant y, j = N-1-l; element k -> i = k+1),
+// chain 1 = Y (lines of constant x, i = N-1-l; element k -> j = k+1).  The Thomas forward sweep
+// (a dependent chain of reciprocals) runs 8 elements per block with the coefficient loads of the
+// next block in flight; the outputs of 32 consecutive elements are staged in shared memory and
+// stored as coalesced line segments (the factor arrays are line-major, as the apply reads them).
+// The certified contraction kappa_l = max_k (T_l^{-1} c_l)_k is formed in the same kernel:
+// forward part y = al y + e alongside the factorisation, backward part over the staged blocks of
+// the scratch copy of y, last block first.
 struct LineFactorOut { double *p, *e, *al, *be, *t, *kap, *scratch; };
 
-__global__ void __launch_bounds__(64) k_line_factor(int N, long P, const double *__restrict__ aE,
+constexpr int LFB = 32;   // elements per staged block
+
+__global__ void __launch_bounds__(32) k_line_factor(int N, long P, const double *__restrict__ aE,
     const double *__restrict__ aN, const double *__restrict__ rr, const double *__restrict__ aW,
     const double *__restrict__ aS, int weighted, LineFactorOut ox, LineFactorOut oy)
 {
+    __shared__ double buf[5][32][LFB + 1];
     const int chain = blockIdx.y;
     const LineFactorOut &o = chain == 0 ? ox : oy;
     const int n = N / 2, nl = n - 1;
-    const int l = blockIdx.x * blockDim.x + threadIdx.x;
-    if (l >= nl) return;
+    const int lane = threadIdx.x, l0 = blockIdx.x * 32;
+    const int l = min(l0 + lane, nl - 1);               // idle lanes redo the last line (not stored)
     const int line = N - 1 - l;
+    // element k of this lane's line: coefficient address g0 + k*gs, 1D indices
+    const long g0 = chain == 0 ? (long)line * P + 1 : P + line, gs = chain == 0 ? 1 : P;
+    const double wsub = chain == 0 ? 0.0 : __ldg(aW + line);   // per-line 1D coefficients
+    const double ssub = chain == 0 ? __ldg(aS + line) : 0.0;
     double gprev = 0.0, supprev = 0.0, y = 0.0;
-    const long base = (long)l * n;
-#pragma unroll 8
-    for (int k = 0; k < n; ++k) {
-        int i, j;
-        if (chain == 0) { i = k + 1; j = line; } else { i = line; j = k + 1; }
-        const long g = (long)j * P + i;
-        const double vE = __ldg(aE + g), vN = __ldg(aN + g), vr = __ldg(rr + g), vw = __ldg(aW + i), vs = __ldg(aS + j);
-        const double D = ((vw + vE) + (vs + vN)) + vr;
-        const double sub = chain == 0 ? vw : vs, sup = chain == 0 ? vE : vN, cE = chain == 0 ? vN : vE;
-        const double den = (k == 0) ? D : D - sub * (supprev * gprev);
-        const double gk = 1.0 / den;
-        const double alk = (k == 0) ? 0.0 : sub * gk, ek = cE * gk;
-        o.p[base + k] = (weighted ? D : 1.0) * gk;
-        o.e[base + k] = ek;
-        o.al[base + k] = alk;
-        o.be[base + k] = (k == n - 1) ? 0.0 : sup * gk;
-        if (k == n - 1) o.t[l] = sup * gk;    // coupling to the I neighbour of the last element
-        y = alk * y + ek;                     // forward part of T^{-1} c
-        o.scratch[base + k] = y;
-        gprev = gk; supprev = sup;
+    struct Raw { double E[8], Nn[8], R[8], w[8], s[8]; };
+    auto load = [&](int k0, Raw &r) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = min(k0 + u, n - 1);
+            const long g = g0 + (long)k * gs;
+            r.E[u] = __ldg(aE + g); r.Nn[u] = __ldg(aN + g); r.R[u] = __ldg(rr + g);
+            r.w[u] = chain == 0 ? __ldg(aW + k + 1) : wsub;
+            r.s[u] = chain == 0 ? ssub : __ldg(aS + k + 1);
+        }
+    };
+    auto factor8 = [&](int k0, const Raw &r) {          // elements k0..k0+7 (k0 % LFB + 8 <= LFB)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = k0 + u;
+            if (k < n) {
+                const double vE = r.E[u], vN = r.Nn[u], vw = r.w[u], vs = r.s[u];
+                const double D = ((vw + vE) + (vs + vN)) + r.R[u];
+                const double sub = chain == 0 ? vw : vs, sup = chain == 0 ? vE : vN, cE = chain == 0 ? vN : vE;
+                const double den = (k == 0) ? D : D - sub * (supprev * gprev);
+                const double gk = 1.0 / den;
+                const double alk = (k == 0) ? 0.0 : sub * gk, ek = cE * gk;
+                const int kk = k % LFB;
+                buf[0][lane][kk] = (weighted ? D : 1.0) * gk;
+                buf[1][lane][kk] = ek;
+                buf[2][lane][kk] = alk;
+                buf[3][lane][kk] = (k == n - 1) ? 0.0 : sup * gk;
+                y = alk * y + ek;                       // forward part of T^{-1} c
+                buf[4][lane][kk] = y;
+                if (k == n - 1 && l0 + lane < nl) o.t[l] = sup * gk;   // coupling to the I neighbour
+                gprev = gk; supprev = sup;
+            }
+        }
+    };
+    auto flush = [&](int kb) {                          // block kb..kb+LFB-1 of the 32 lines
+        __syncwarp();
+        const int k = kb + lane;
+        for (int r = 0; r < 32 && l0 + r < nl; ++r) {
+            if (k < n) {
+                const long q = (long)(l0 + r) * n + k;
+                o.p[q] = buf[0][r][lane]; o.e[q] = buf[1][r][lane]; o.al[q] = buf[2][r][lane];
+                o.be[q] = buf[3][r][lane]; o.scratch[q] = buf[4][r][lane];
+            }
+        }
+        __syncwarp();
+    };
+    Raw ra, rb;
+    load(0, ra);
+    for (int k0 = 0; k0 < n; k0 += 16) {                // two blocks of 8 per iteration (static buffers)
+        load(k0 + 8, rb);
+        factor8(k0, ra);
+        if ((k0 + 8) % LFB == 0) flush(k0 + 8 - LFB);
+        load(k0 + 16, ra);
+        factor8(k0 + 8, rb);
+        if ((k0 + 16) % LFB == 0 || k0 + 16 >= n) flush((k0 + 16 - 1) / LFB * LFB);
     }
+    // backward part of T^{-1} c: z_k = y_k + be_k z_{k+1}; kappa = max z (blocks staged in buf)
     double z = 0.0, mx = 0.0;
-#pragma unroll 8
-    for (int k = n - 1; k >= 0; --k) {
-        z = o.scratch[base + k] + o.be[base + k] * z;
-        mx = fmax(mx, z);
+    for (int kb = (n - 1) / LFB * LFB; kb >= 0; kb -= LFB) {
+        __syncwarp();
+        const int k = kb + lane;
+#pragma unroll
+        for (int r0 = 0; r0 < 32; r0 += 16) {           // 32 loads in flight per round
+            double vb[16], vy[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const bool ok = k < n && l0 + r0 + r < nl;
+                const long q = (long)(l0 + r0 + r) * n + k;
+                vb[r] = ok ? o.be[q] : 0.0; vy[r] = ok ? o.scratch[q] : 0.0;
+            }
+#pragma unroll
+            for (int r = 0; r < 16; ++r) { buf[3][r0 + r][lane] = vb[r]; buf[4][r0 + r][lane] = vy[r]; }
+        }
+        __syncwarp();
+        for (int kk = min(LFB, n - kb) - 1; kk >= 0; --kk) {
+            z = buf[4][lane][kk] + buf[3][lane][kk] * z;
+            mx = fmax(mx, z);
+        }
     }
-    o.kap[l] = mx;
+    if (l0 + lane < nl) o.kap[l] = mx;
 }
 
 // ------------------------------------------------------------------------------ apply
@@ -193,10 +255,10 @@ cudaError_t setup_lines(Ctx *c)
     double *base = c->fac;
     double *xp = base, *xe = base + per, *xa = base + 2 * per, *xb = base + 3 * per;
     double *yp = base + 4 * per, *ye = base + 5 * per, *ya = base + 6 * per, *yb = base + 7 * per;
-    const int tpb = 64, nb = (nl + tpb - 1) / tpb;
+    const int nb = (nl + 31) / 32;
     const LineFactorOut ox{xp, xe, xa, xb, c->tX, c->kapX, c->cbuf};
     const LineFactorOut oy{yp, ye, ya, yb, c->tY, c->kapY, c->cbuf + per};
-    k_line_factor<<<dim3(nb, 2), tpb, 0, c->st>>>(N, c->P, c->aE, c->aN, c->rr, c->aW, c->aS, c->weighted, ox, oy);
+    k_line_factor<<<dim3(nb, 2), 32, 0, c->st>>>(N, c->P, c->aE, c->aN, c->rr, c->aW, c->aS, c->weighted, ox, oy);
     c->launches++;
     SPP_CUDA_TRY(cudaGetLastError());
     std::vector<double> kx(nl), ky(nl);
