@@ -168,6 +168,136 @@ static int corner_solve(Ctx *c, const double *bc, double b0sq, int *cap_hit, cud
     return cycles;
 }
 
+// ------------------------------------------------------------------------------------------ corner graph
+// The stationary iteration of corner_solve as one CUDA graph: an init kernel, then a device-side
+// while loop whose body is one V-cycle (every level's launches), the update z' = z + e with
+// rho = b_C - A_CC z', and a check kernel that makes exactly corner_solve's decision (same
+// partial sums in the same order, same tests) and sets the loop condition.  No host round trip
+// per cycle; the cycle count is read back at the FGMRES iteration's own synchronisation.
+__device__ __forceinline__ double ordered_sum(const double *p)
+{
+    double s = 0.0;
+    for (int i = 0; i < kRedBlocks; ++i) s += p[i];   // host_sum's order
+    return s;
+}
+__device__ __forceinline__ int mg_continue(MGState *s, double red, int maxc, int fixed)
+{
+    if (fixed > 0) return s->cycles < fixed;
+    if (s->res <= red * s->b0) return 0;
+    if (s->cycles >= maxc) { s->cap = 1; return 0; }
+    return 1;
+}
+__global__ void k_mg_init(const double *part_b, MGState *s, double *za, double *zb, double red, int maxc, int fixed,
+                          cudaGraphConditionalHandle h)
+{
+    s->b0 = fixed > 0 ? 0.0 : sqrt(ordered_sum(part_b));
+    s->res = s->b0;
+    s->cycles = 0; s->cap = 0;
+    s->zcur = nullptr; s->za = za; s->zb = zb; s->znext = za;
+    cudaGraphSetConditional(h, mg_continue(s, red, maxc, fixed));
+}
+__global__ void k_mg_check(const double *part_r, MGState *s, double red, int maxc, int fixed,
+                           cudaGraphConditionalHandle h)
+{
+    s->cycles++;
+    if (fixed <= 0) s->res = sqrt(ordered_sum(part_r));
+    s->zcur = s->znext;
+    s->znext = s->znext == s->za ? s->zb : s->za;
+    cudaGraphSetConditional(h, mg_continue(s, red, maxc, fixed));
+}
+
+// what the captured launches depend on besides fixed buffers: the level plans and MG options
+static std::vector<long> corner_signature(const Ctx *c)
+{
+    std::vector<long> v{c->N, c->L, c->tune.coarse_max, c->opt.mg_fixed_cycles, c->opt.mg_max_cycles,
+                        (long)(c->opt.mg_reduction * 1e15)};
+    for (int l = 0; l < c->L; ++l) {
+        const Level &L = c->lev[l];
+        for (long x : {(long)L.n, L.pitch, L.cpitch, (long)L.tile_warps, (long)L.tile_rows, (long)L.tile_cols,
+                       (long)L.halo_x, (long)L.halo_y})
+            v.push_back(x);
+    }
+    return v;
+}
+
+static void corner_graph_destroy(Ctx *c)
+{
+    if (c->cg_exec) cudaGraphExecDestroy(c->cg_exec);
+    if (c->cg) cudaGraphDestroy(c->cg);
+    c->cg_exec = nullptr; c->cg = nullptr; c->cg_sig.clear();
+}
+
+static cudaError_t corner_graph_build(Ctx *c)
+{
+    corner_graph_destroy(c);
+    if (!c->cap_st) SPP_CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_st, cudaStreamNonBlocking));
+    Level &L0 = c->lev[0];
+    const double red = c->opt.mg_reduction;
+    const int maxc = c->opt.mg_max_cycles, fixed = c->opt.mg_fixed_cycles;
+    cudaGraph_t g = nullptr;
+    SPP_CUDA_TRY(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    SPP_CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+    cudaStream_t user = c->st;
+    const int prof = c->prof_on;
+    const int64_t l0 = c->launches;
+    c->st = c->cap_st; c->prof_on = 0; c->capturing = true;
+    cudaError_t e = cudaStreamBeginCaptureToGraph(c->st, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        k_mg_init<<<1, 1, 0, c->st>>>(part_slot(c, 1), c->mgs, c->Zc, c->Zc2, red, maxc, fixed, h);
+        cudaStreamCaptureStatus cs;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t nd = 0;
+        e = cudaStreamGetCaptureInfo(c->st, &cs, nullptr, nullptr, &deps, &nd);
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t wn = nullptr;
+        if (e == cudaSuccess) e = cudaGraphAddNode(&wn, g, deps, nd, &cp);
+        if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(c->st, &wn, 1, cudaStreamSetCaptureDependencies);
+        cudaGraph_t tmp = nullptr;
+        const cudaError_t e2 = cudaStreamEndCapture(c->st, &tmp);
+        if (e == cudaSuccess) e = e2;
+        if (e == cudaSuccess) {                         // the loop body: one cycle
+            cudaGraph_t body = cp.conditional.phGraph_out[0];
+            e = cudaStreamBeginCaptureToGraph(c->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+            if (e == cudaSuccess) {
+                const int64_t b0 = c->launches;
+                const double *ev = vcycle(c, 0, L0.rho);
+                launch_cycle_update(c, nullptr, ev, nullptr, c->Bc, L0.rho, part_slot(c, 0), c->mgs);
+                k_mg_check<<<1, 1, 0, c->st>>>(part_slot(c, 0), c->mgs, red, maxc, fixed, h);
+                c->launches++;
+                c->cg_body_launches = c->launches - b0;
+                const cudaError_t e3 = cudaStreamEndCapture(c->st, &tmp);
+                e = e3 != cudaSuccess ? e3 : cudaGetLastError();
+            }
+        }
+    }
+    c->st = user; c->prof_on = prof; c->capturing = false;
+    c->launches = l0;
+    if (e == cudaSuccess && c->sticky != cudaSuccess) { e = c->sticky; c->sticky = cudaSuccess; }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&c->cg_exec, g, 0);
+    if (e != cudaSuccess) { cudaGraphDestroy(g); c->cg_exec = nullptr; return e; }
+    c->cg = g;
+    c->cg_sig = corner_signature(c);
+    if (getenv("SPP_DEBUG_GRAPH")) fprintf(stderr, "[spp] corner graph captured: %lld kernels per cycle\n", (long long)c->cg_body_launches);
+    return cudaSuccess;
+}
+
+// corner solve through the graph (b_C in c->Bc and L0.rho, ||S0 b_C||^2 partials in part slot 1);
+// the result is read through c->mgs (k_corner_out)
+static cudaError_t corner_solve_graph(Ctx *c)
+{
+    if (!c->cg_exec || c->cg_sig != corner_signature(c)) SPP_CUDA_TRY(corner_graph_build(c));
+    SPP_CUDA_TRY(cudaGraphLaunch(c->cg_exec, c->st));
+    c->launches += 1;                                   // k_mg_init (the body is counted per cycle)
+    return cudaSuccess;
+}
+
+static bool graph_mode(const Ctx *c) { return c->use_graph && c->prof_on == 0; }
+
 // M_II solve on region I = [n+1, N-1]^2: z = (D - E - N)^{-1} (s v), s = 1/D
 // (scaled, unweighted mode) or 1 (Jacobi mode: the input is already D v, reading R11); the exact
 // chained row-scan sweep of k_mg.cu with the level origin at (n, n) of the global grid.
@@ -193,11 +323,19 @@ static int apply_precond(Ctx *c, const double *v, double *z, int *cap_hit, cudaE
     launch_lines(c, v, z);
     // corner
     Level &L0 = c->lev[0];
+    const bool gm = graph_mode(c);
     {
         ProfScope ps(c, 9, 40.0 * (double)n * n);
         k_corner_rhs<<<kRedBlocks, kRedThreads, 0, c->st>>>(N, c->P, L0.pitch, v, z, c->aE, c->aN, c->rr, c->aW,
-                                                            c->aS, L0.hb, L0.kb, c->weighted, c->Bc, part_slot(c, 1));
+                                                            c->aS, L0.hb, L0.kb, c->weighted, c->Bc, part_slot(c, 1),
+                                                            gm ? L0.rho : nullptr);
         c->launches++;
+    }
+    if (gm) {                                           // cycles known after the caller's next sync
+        *err = corner_solve_graph(c);
+        k_corner_out<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, nullptr, c->P, z, c->mgs);
+        c->launches++;
+        return -1;
     }
     double b0sq = 0;
     if (c->opt.mg_fixed_cycles <= 0) {
@@ -210,7 +348,7 @@ static int apply_precond(Ctx *c, const double *v, double *z, int *cap_hit, cudaE
         *err = cudaMemsetAsync(c->Zc, 0, sizeof(double) * L0.elems, c->st);
         zc = c->Zc;
     }
-    k_corner_out<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, zc, c->P, z);
+    k_corner_out<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, zc, c->P, z, nullptr);
     c->launches++;
     return cyc;
 }
@@ -339,6 +477,12 @@ static spp_status alloc_all(Ctx *c)
                                                                       (size_t)kMaxLevels * kRedBlocks)));
     CK(c, cudaMalloc(&c->flags, sizeof(int) * 256));
     CK(c, cudaMemsetAsync(c->flags, 0, sizeof(int) * 256, c->st));
+    CK(c, cudaMalloc(&c->mgs, sizeof(MGState)));
+    CK(c, cudaMallocHost(&c->hmgs, sizeof(MGState)));
+    {
+        const char *ng = getenv("SPP_NO_GRAPH");
+        c->use_graph = !(ng && ng[0] == '1');
+    }
     {   // exact chained sweep: one progress flag and one inflow row per CTA
         const int W = std::max(1, std::min(c->tune.sweep_warps, 8));
         const long ncta = (n + 32L * W - 1) / (32L * W) + 1;
@@ -524,6 +668,10 @@ void spp_destroy(spp_ctx *cx)
     cudaFree(c->chain); cudaFree(c->chain_flags);
     cudaFree(c->d_chunks); cudaFree(c->d1);
     if (c->hpin) cudaFreeHost(c->hpin);
+    corner_graph_destroy(c);
+    if (c->cap_st) cudaStreamDestroy(c->cap_st);
+    cudaFree(c->mgs);
+    if (c->hmgs) cudaFreeHost(c->hmgs);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     delete c;
 }
@@ -610,10 +758,12 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
             CK(c, ensure_vectors(c, k + 1));
             int cap = 0;
             cudaError_t err = cudaSuccess;
-            const int cyc = apply_precond(c, c->V[k], c->Z[k], &cap, &err);
+            int cyc = apply_precond(c, c->V[k], c->Z[k], &cap, &err);
             CK(c, err);
-            if (cap && c->opt.mg_strict) FAIL(c, SPP_E_MG_CAP, "corner multigrid hit the cycle cap (%d)", c->opt.mg_max_cycles);
-            mg_tot += cyc; mg_min = std::min(mg_min, cyc); mg_max = std::max(mg_max, cyc); caps += cap;
+            if (cyc >= 0) {
+                if (cap && c->opt.mg_strict) FAIL(c, SPP_E_MG_CAP, "corner multigrid hit the cycle cap (%d)", c->opt.mg_max_cycles);
+                mg_tot += cyc; mg_min = std::min(mg_min, cyc); mg_max = std::max(mg_max, cyc); caps += cap;
+            }
             // w = W A z_k, with <w, v_0>
             {
                 ProfScope ps(c, 0, 48.0 * mm);
@@ -636,8 +786,15 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
                                                                    c->V[k + 1]);
                 c->launches += 2;
             }
+            if (cyc < 0) CK(c, cudaMemcpyAsync(c->hmgs, c->mgs, sizeof(MGState), cudaMemcpyDeviceToHost, c->st));
             CK(c, cudaMemcpyAsync(c->hpin, c->dscal, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, c->st));
             CK(c, cudaStreamSynchronize(c->st));
+            if (cyc < 0) {                              // corner graph: this apply's cycle count
+                cyc = c->hmgs->cycles; cap = c->hmgs->cap;
+                c->launches += (int64_t)cyc * c->cg_body_launches;
+                if (cap && c->opt.mg_strict) FAIL(c, SPP_E_MG_CAP, "corner multigrid hit the cycle cap (%d)", c->opt.mg_max_cycles);
+                mg_tot += cyc; mg_min = std::min(mg_min, cyc); mg_max = std::max(mg_max, cyc); caps += cap;
+            }
             double *h = &H[(size_t)k * (maxit + 1)];
             for (int j = 0; j <= k + 1; ++j) h[j] = c->hpin[j];
             // Givens (Saad 2003)
@@ -762,6 +919,12 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
         c->weighted = w;
         if (w) CK(c, setup_lines(c));
         CK(c, err);
+        if (k < 0) {                                    // corner graph: read the cycle count
+            CK(c, cudaMemcpyAsync(c->hmgs, c->mgs, sizeof(MGState), cudaMemcpyDeviceToHost, c->st));
+            CK(c, cudaStreamSynchronize(c->st));
+            k = c->hmgs->cycles;
+            c->launches += (int64_t)k * c->cg_body_launches;
+        }
         if (cyc) *cyc = k;
         up(B, out);
     } else if (s == SPP_STAGE_MII || s == SPP_STAGE_MYY || s == SPP_STAGE_MXX) {
@@ -790,7 +953,7 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
         pk(in + mm, B);
         Level &L0 = c->lev[0];
         k_corner_rhs<<<kRedBlocks, kRedThreads, 0, c->st>>>(c->N, c->P, L0.pitch, A, B, c->aE, c->aN, c->rr, c->aW,
-                                                            c->aS, L0.hb, L0.kb, 0, c->Bc, part_slot(c, 0));
+                                                            c->aS, L0.hb, L0.kb, 0, c->Bc, part_slot(c, 0), nullptr);
         k_unpack_level<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, c->Bc, out);
     } else if (s == SPP_STAGE_CORNER_SOLVE) {
         Level &L0 = c->lev[0];

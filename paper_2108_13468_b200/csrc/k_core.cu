@@ -319,7 +319,7 @@ __global__ void k_update_x(long n2, int k, const double *const *Z, const double 
 // written to the level-0 value grid; partial ||S_0 b_C||^2 (S_0 = diag(hbar_i kbar_j)).
 __global__ void __launch_bounds__(kRedThreads) k_corner_rhs(int N, long P, long P0, const double *v,
     const double *z, const double *aE, const double *aN, const double *rr, const double *aW,
-    const double *aS, const double *hb, const double *kb, int weighted, double *bc, double *part)
+    const double *aS, const double *hb, const double *kb, int weighted, double *bc, double *part, double *bc2)
 {
     __shared__ double sm[32];
     const int n = N / 2;
@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(kRedThreads) k_corner_rhs(int N, long P, long 
         if (j == n) b += aN[g] * z[g + P];
         if (i == n) b += aE[g] * z[g + 1];
         bc[(long)j * P0 + i] = b;
+        if (bc2) bc2[(long)j * P0 + i] = b;           // corner graph: the first cycle's residual
         const double t = (hb[i] * kb[j]) * b;
         acc += t * t;
     }
@@ -398,12 +399,13 @@ __global__ void k_prolong_add(int nl, long Pv, double *e, const double *ec, long
 }
 
 // copy the corner iterate into the global preconditioned vector
-__global__ void k_corner_out(int n, long P0, const double *zc, long P, double *z)
+__global__ void k_corner_out(int n, long P0, const double *zc, long P, double *z, const MGState *ms)
 {
+    if (ms) zc = ms->zcur;                          // corner graph: nullptr when no cycle ran (z = 0)
     const long tot = (long)n * n;
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
         const int j = (int)(p / n) + 1, i = (int)(p % n) + 1;
-        z[(long)j * P + i] = zc[(long)j * P0 + i];
+        z[(long)j * P + i] = zc ? zc[(long)j * P0 + i] : 0.0;
     }
 }
 

@@ -390,7 +390,7 @@ static void dbg_sync(Ctx *c, const char *what)
 {
     static int on = -1;
     if (on < 0) { const char *e = getenv("SPP_DEBUG_SYNC"); on = (e && e[0] == '1') ? 1 : 0; }
-    if (!on) return;
+    if (!on || c->capturing) return;
     cudaError_t e = cudaStreamSynchronize(c->st);
     if (e == cudaSuccess) e = cudaGetLastError();
     fprintf(stderr, "[spp-debug] %s: %s\n", what, cudaGetErrorString(e));
@@ -817,9 +817,10 @@ __global__ void __launch_bounds__(kRedThreads) k_cycle_update(int nl, long pv, l
     const double *__restrict__ e, double *znew, const double *__restrict__ b, const double *__restrict__ aE,
     const double *__restrict__ aN, const double *__restrict__ rr, const double *__restrict__ aW,
     const double *__restrict__ aS, const double *__restrict__ hb, const double *__restrict__ kb, double *rho,
-    double *part)
+    double *part, const MGState *ms)
 {
     __shared__ double sm[32];
+    if (ms) { z = ms->zcur; znew = ms->znext; }        // corner graph: buffers from the device state
     double acc = 0.0;
     const long tot = (long)nl * nl;
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
@@ -848,13 +849,13 @@ __global__ void __launch_bounds__(kRedThreads) k_cycle_update(int nl, long pv, l
 }
 
 void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew, const double *b, double *rho,
-                         double *part)
+                         double *part, const MGState *ms)
 {
     Level &L = c->lev[0];
     const double nn = (double)L.n * L.n;
     ProfScope ps(c, 6, nn * (z ? 64.0 : 56.0));
     k_cycle_update<<<kRedBlocks, kRedThreads, 0, c->st>>>(L.n, L.pitch, L.cpitch, z, e, znew, b, L.aE, L.aN, L.rr,
-                                                          L.aW, L.aS, L.hb, L.kb, rho, part);
+                                                          L.aW, L.aS, L.hb, L.kb, rho, part, ms);
     c->launches++;
 }
 

@@ -35,13 +35,13 @@ __global__ void k_update_x(long n2, int k, const double *const *Z, const double 
 __global__ void k_corner_rhs(int N, long P, long P0, const double *v, const double *z,
                              const double *aE, const double *aN, const double *rr, const double *aW,
                              const double *aS, const double *hb, const double *kb, int weighted,
-                             double *bc, double *part);
+                             double *bc, double *part, double *bc2);
 __global__ void k_mg_resid(int nl, long Pv, long Pc, double *z, const double *e, const double *b,
                            const double *aE, const double *aN, const double *rr, const double *aW,
                            const double *aS, const double *hb, const double *kb, double *rho,
                            double *part);
 __global__ void k_prolong_add(int nl, long Pv, double *e, const double *ec, long Pcv);
-__global__ void k_corner_out(int n, long P0, const double *zc, long P, double *z);
+__global__ void k_corner_out(int n, long P0, const double *zc, long P, double *z, const MGState *ms);
 __global__ void k_pack_level(int nl, long Pv, const double *src, double *dst);
 __global__ void k_unpack_level(int nl, long Pv, const double *src, double *dst);
 

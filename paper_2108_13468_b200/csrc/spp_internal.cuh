@@ -81,6 +81,16 @@ struct Tune {
 
 struct ProfRec { int64_t launches = 0; double ms = 0, bytes = 0; };
 
+// device-resident state of the corner stationary iteration when it runs as a CUDA graph with a
+// device-side while loop (capi.cu "corner graph")
+struct MGState {
+    const double *zcur;     // current iterate z (nullptr: z = 0, no cycle ran yet)
+    double *znext;          // buffer the next cycle writes
+    double *za, *zb;        // the two iterate buffers
+    double b0, res;         // ||S0 b_C||, ||S0 rho||
+    int cycles, cap;        // cycles run, cycle cap hit
+};
+
 struct Ctx {
     int dim = 0, N = 0, n = 0, m = 0;    // N intervals, n = N/2, m = N-1
     double eps = 0;
@@ -136,6 +146,15 @@ struct Ctx {
     std::vector<PendingProf> pend;
     float setup_ms = 0;
     int sm_count = 148;
+    // corner graph: the stationary V-cycle iteration as one CUDA graph with a while node
+    MGState *mgs = nullptr;                // device state
+    MGState *hmgs = nullptr;               // pinned host copy
+    cudaStream_t cap_st = nullptr;         // private capture stream
+    cudaGraph_t cg = nullptr; cudaGraphExec_t cg_exec = nullptr;
+    std::vector<long> cg_sig;              // plan signature the graph was captured for
+    int64_t cg_body_launches = 0;          // kernels per loop iteration
+    bool capturing = false;
+    int use_graph = 1;
 };
 
 // kernels / launchers (defined in the .cu files)
@@ -150,7 +169,7 @@ void launch_ycoef(Ctx *c, int nl, long pc, const double *aE, const double *aN, c
 cudaError_t wave_init();
 void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e);
 void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew, const double *b, double *rho,
-                         double *part);
+                         double *part, const MGState *ms = nullptr);
 cudaError_t setup_mg_tiles(Ctx *c);
 bool launch_coarse_vcycle(Ctx *c, int lc, const double *R);
 
