@@ -795,8 +795,9 @@ void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e)
 {
     Level &F = c->lev[l], &C = c->lev[l + 1];
     ProfScope ps(c, 4, (double)F.n * F.n * 40.0 + 8.0 * C.n * (double)C.n);
-    // coarse tile edge: enough CTAs to fill the GPU on the small levels
-    const int RTn = C.n >= 512 ? 32 : (C.n >= 128 ? 16 : 8);
+    // coarse tile edge: enough CTAs to fill the GPU on the small levels, and several waves of
+    // CTAs on the large ones (one wave plus a small remainder leaves most SMs idle in the tail)
+    const int RTn = C.n >= 128 ? 16 : 8;
     const dim3 grid((C.n + RTn - 1) / RTn, (C.n + RTn - 1) / RTn);
 #define SPP_RR(T) k_resid_restrict<T><<<grid, T >= 32 ? 256 : (T >= 16 ? 256 : 128), 0, c->st>>>(F.n, F.pitch, \
         F.cpitch, e, R, F.aE, F.aN, F.rr, F.aW, F.aS, F.hb, F.kb, C.n, C.pitch, C.hb, C.kb, C.b)
