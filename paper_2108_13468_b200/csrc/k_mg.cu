@@ -55,7 +55,7 @@ constexpr int WSLOT = WNA * WBOX;             // doubles per staging slot (16 KB
 constexpr int WWARP = WNS * WSLOT;            // doubles per warp (48 KB, a 1 KB multiple)
 constexpr int WMAXW = 4;         // sweeping warps per CTA (max); +1 TMA producer warp
 constexpr int WEB = 128;         // edge ring (columns)
-constexpr int WPF = 4;           // L2 prefetch distance (chunks)
+constexpr int WPF = 8;           // L2 prefetch distance (chunks)
 constexpr int WLAG = 2;          // lane-to-lane skew (columns)
 
 struct WaveMaps { CUtensorMap q, a1, a2, cd; };
