@@ -482,6 +482,8 @@ static spp_status alloc_all(Ctx *c)
     {
         const char *ng = getenv("SPP_NO_GRAPH");
         c->use_graph = !(ng && ng[0] == '1');
+        const char *nl = getenv("SPP_NO_LINES_TMA");
+        c->no_lines_tma = (nl && nl[0] == '1') ? 1 : 0;
     }
     {   // exact chained sweep: one progress flag and one inflow row per CTA
         const int W = std::max(1, std::min(c->tune.sweep_warps, 8));

@@ -20,10 +20,13 @@
 // rounding).  Each line is solved by the CTA with two
 // block-wide affine scans (warp shuffles + one shared-memory level).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 
 #include "spp_internal.cuh"
 #include "scan.cuh"
+#include "tma.cuh"
 
 namespace spp {
 
@@ -150,18 +153,20 @@ __device__ __forceinline__ void line_load(const LineChain &ch, int l, int k0, co
 {
     const int len = ch.len;
     const long base = ch.v0 + (long)l * ch.vline, fo = (long)l * len;
+    // unpredicated loads from a clamped index (elements past the line end are masked where they
+    // are used): a predicated load with a zero fill makes the next write of the register wait for
+    // the load, which serialised the prefetch of line l+1 behind the scans of line l
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        const int kk = k0 + k;
-        const bool ok = kk < len;
-        r.v[k] = ok ? __ldg(v + base + (long)kk * ch.vstride) : 0.0;
-        r.p[k] = ok ? __ldg(ch.p + fo + kk) : 0.0;
-        r.e[k] = ok ? __ldg(ch.e + fo + kk) : 0.0;
-        r.al[k] = ok ? __ldg(ch.al + fo + kk) : 0.0;
-        r.be[k] = ok ? __ldg(ch.be + fo + kk) : 0.0;
+        const int kk = min(k0 + k, len - 1);
+        r.v[k] = __ldg(v + base + (long)kk * ch.vstride);
+        r.p[k] = __ldg(ch.p + fo + kk);
+        r.e[k] = __ldg(ch.e + fo + kk);
+        r.al[k] = __ldg(ch.al + fo + kk);
+        r.be[k] = __ldg(ch.be + fo + kk);
     }
     // coupling to the I neighbour of the last element (written by the M_II sweep)
-    r.tI = (k0 <= len - 1 && len - 1 < k0 + K) ? ch.t[l] * z[base + (long)(len - 1) * ch.vstride + ch.istep] : 0.0;
+    r.tI = ch.t[l] * z[base + (long)(len - 1) * ch.vstride + ch.istep];   // used by the owner of element len-1 only
 }
 
 // Line solves of one chunk: lines start..last in order, each T_l z_l = s v_l + C_l z_{l-1} (+ I
@@ -183,9 +188,10 @@ __global__ void __launch_bounds__(256) k_lines(LineChain cx, LineChain cy, const
         double al[K], be[K], b[K], y[K], zz[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
+            const bool in = k0 + k < len;
             double bb = r.p[k] * r.v[k] + r.e[k] * zp[k];
             if (k0 + k == len - 1) bb += r.tI;
-            b[k] = bb; al[k] = r.al[k]; be[k] = r.be[k];
+            b[k] = in ? bb : 0.0; al[k] = in ? r.al[k] : 0.0; be[k] = in ? r.be[k] : 0.0;
         }
         fwd_scan<K>(al, b, y, sA, sB);
         bwd_scan<K>(be, y, zz, sA, sB);
@@ -214,6 +220,156 @@ __global__ void __launch_bounds__(256) k_lines(LineChain cx, LineChain cy, const
             solve(l, r);
         }
     }
+}
+
+// TMA-staged variant (line length a multiple of 64, K elements per thread): the four factor
+// arrays of a line are one 2D box each (the line viewed as len/16 rows of 16, 128B swizzle), the
+// operand v is one box of its row (X lines) or len/256 boxes of a 2-column strip (Y lines,
+// columns i&~1, i&~1 + 1); all land in a shared-memory stage with one mbarrier.  Each thread reads
+// its K values from the stage, the block syncs, and thread 0 refills the stage for a later line
+// while the scans of this line run.  Loading through the LSU (one 8-byte element per lane per
+// row/column of the grid) had left the line chains waiting on the L1 tag stage and on load
+// latency (ncu: stall_long_sb + stall_lg ~57% of samples).
+struct LineMaps { CUtensorMap f[2][4]; CUtensorMap vx, vy; };
+
+__device__ __forceinline__ int swz16(int o)            // 128B-swizzled offset of element o (16 per row)
+{
+    const int r = o >> 4, c = o & 15;
+    return (r << 4) + ((((c >> 1) ^ (r & 7))) << 1) + (c & 1);
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) k_lines_tma(LineChain cx, LineChain cy, const LineChunk *chunks,
+                                                   double *z, double *ysc, int N, long P, int nst,
+                                                   const __grid_constant__ LineMaps m)
+{
+    extern __shared__ double lsm_raw[];
+    __shared__ double sA[32], sB[64];
+    __shared__ __align__(8) unsigned long long full[2];
+    const LineChunk ck = chunks[blockIdx.x];
+    const int chain = ck.chain;
+    const LineChain &ch = chain == 0 ? cx : cy;
+    const int len = ch.len;
+    const int k0 = threadIdx.x * K;
+    double *sm = lsm_raw + (((1024u - ((unsigned)__cvta_generic_to_shared(lsm_raw) & 1023u)) & 1023u) >> 3);
+    const int stage = 6 * len;                          // doubles: 4 factor boxes + v (<= 2 len)
+    const int vxr = len / 16 + 1, nvx = (vxr + 255) / 256, vxb = ((vxr + nvx - 1) / nvx + 7) / 8 * 8;   // X: row boxes (1 KB multiples)
+    const unsigned vbytes = chain == 0 ? (unsigned)(nvx * vxb * 16) * 8u : (unsigned)len * 16u;
+    const unsigned bytes = 4u * (unsigned)len * 8u + vbytes;
+    const int vrows = len < 256 ? len : 256;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nst; ++s)
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&full[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int l, int s) {                    // thread 0: all boxes of line l into stage s
+        const unsigned bar = (unsigned)__cvta_generic_to_shared(&full[s]);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(sm + (size_t)s * stage);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+#pragma unroll
+        for (int f = 0; f < 4; ++f) tma_load(dst + (unsigned)(f * len * 8), &m.f[chain][f], 0, l * (len >> 4), bar);
+        const long g0 = ch.v0 + (long)l * ch.vline;     // grid index of element 0 of the line
+        if (chain == 0) {
+            for (int b = 0; b < nvx; ++b)
+                tma_load(dst + (unsigned)((4 * len + 16 * vxb * b) * 8), &m.vx, 0, (int)((g0 - 1) >> 4) + vxb * b, bar);
+        }
+        else {
+            const int i = (int)(g0 % P), x = i & ~1;
+            for (int r0 = 0; r0 < len; r0 += vrows)
+                tma_load(dst + (unsigned)((4 * len + 2 * r0) * 8), &m.vy, x, 1 + r0, bar);
+        }
+    };
+    double zp[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) zp[k] = 0.0;
+    const int nlines = ck.last - ck.start + 1;
+    if (threadIdx.x == 0)
+        for (int s = 0; s < nst && s < nlines; ++s) issue(ck.start + s, s);
+    const bool owner = k0 <= len - 1 && len - 1 < k0 + K;   // holds the element coupled to I
+    double tnext = 0.0;
+    if (owner) {
+        const long g0 = ch.v0 + (long)ck.start * ch.vline;
+        tnext = ch.t[ck.start] * z[g0 + (long)(len - 1) * ch.vstride + ch.istep];
+    }
+#ifdef SPP_LINES_PROF
+    long long q0 = 0, q1 = 0, q2 = 0, q3 = 0, q4 = 0;
+#define LP(v) long long v; asm volatile("mov.u64 %0, %%clock64;" : "=l"(v) :: "memory")
+#else
+#define LP(v)
+#endif
+    for (int it = 0; it < nlines; ++it) {
+        const int l = ck.start + it, s = it % nst;
+        LP(ta);
+        mbar_wait((unsigned)__cvta_generic_to_shared(&full[s]), (unsigned)((it / nst) & 1));
+        LP(tb);
+        const double *st = sm + (size_t)s * stage;
+        double p[K], e[K], al[K], be[K], vv[K];
+#pragma unroll
+        for (int k = 0; k < K; k += 2) {                // pairs share a 16-byte swizzle unit
+            const int o = swz16(k0 + k);
+            const double2 a0 = *reinterpret_cast<const double2 *>(st + o);
+            const double2 a1 = *reinterpret_cast<const double2 *>(st + len + o);
+            const double2 a2 = *reinterpret_cast<const double2 *>(st + 2 * len + o);
+            const double2 a3 = *reinterpret_cast<const double2 *>(st + 3 * len + o);
+            p[k] = a0.x; p[k + 1] = a0.y; e[k] = a1.x; e[k + 1] = a1.y;
+            al[k] = a2.x; al[k + 1] = a2.y; be[k] = a3.x; be[k + 1] = a3.y;
+        }
+        const long g0 = ch.v0 + (long)l * ch.vline;
+        if (chain == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) vv[k] = st[4 * len + swz16(k0 + k + 1)];
+        } else {
+            const int ic = (int)(g0 % P) & 1;
+#pragma unroll
+            for (int k = 0; k < K; ++k) vv[k] = st[4 * len + 2 * (k0 + k) + ic];
+        }
+        const double tI = tnext;
+        LP(tc);
+        __syncthreads();                                // stage s fully read
+        LP(td);
+        if (threadIdx.x == 0 && it + nst < nlines) issue(l + nst, s);
+        if (owner && it + 1 < nlines) {                 // I coupling of the next line, one line ahead
+            const long g1 = g0 + ch.vline;
+            tnext = ch.t[l + 1] * z[g1 + (long)(len - 1) * ch.vstride + ch.istep];
+        }
+        double b[K], y[K], zz[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const bool in = k0 + k < len;
+            double bb = p[k] * vv[k] + e[k] * zp[k];
+            if (k0 + k == len - 1) bb += tI;
+            b[k] = in ? bb : 0.0;
+            if (!in) { al[k] = 0.0; be[k] = 0.0; }
+        }
+        fwd_scan<K>(al, b, y, sA, sB);
+        bwd_scan<K>(be, y, zz, sA, sB);
+        LP(te);
+        // the line's results leave as coalesced segments through shared memory: X lines are row
+        // segments of z, Y lines (columns of z) go line-major to the scratch (k_ysc_transpose)
+        double *zs = sm + (size_t)nst * stage;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            zp[k] = zz[k];
+            const int kk = k0 + k;
+            zs[kk + (kk >> 5)] = zz[k];                 // one pad per 32: conflict-light
+        }
+        __syncthreads();
+        if (l >= ck.first) {
+            double *out = chain == 0 ? z + g0 : ysc + (long)l * len;
+            for (int kk = threadIdx.x; kk < len; kk += blockDim.x) out[kk] = zs[kk + (kk >> 5)];
+        }
+#ifdef SPP_LINES_PROF
+        LP(tf);
+        q0 += tb - ta; q1 += tc - tb; q2 += td - tc; q3 += te - td; q4 += tf - te;
+#endif
+    }
+#ifdef SPP_LINES_PROF
+    if ((threadIdx.x == 0 || threadIdx.x == 255) && (blockIdx.x == 0 || blockIdx.x == 70))
+        printf("[lines-prof] cta %d thr %d lines %d per line: wait %lld read %lld relsync %lld scans %lld store %lld\n",
+               blockIdx.x, threadIdx.x, nlines, q0 / nlines, q1 / nlines, q2 / nlines, q3 / nlines, q4 / nlines);
+#endif
 }
 
 // ------------------------------------------------------------------------------ host
@@ -245,6 +401,10 @@ void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double
         }
         for (int f = 0; f < nl; f += bestG)
             c->chunks.push_back({chain, f, std::min(nl - 1, f + bestG - 1), warm(f)});
+        if (getenv("SPP_DEBUG_LINES"))
+            fprintf(stderr, "[spp] line chain %d: %d lines, chunk %d lines, %d chunks, worst %ld lines (kappa %.6g .. %.6g)\n",
+                    chain, nl, bestG, (nl + bestG - 1) / bestG, bestCost, *std::min_element(k.begin(), k.end()),
+                    *std::max_element(k.begin(), k.end()));
     }
 }
 
@@ -284,6 +444,70 @@ cudaError_t setup_lines(Ctx *c)
     return cudaStreamSynchronize(c->st);
 }
 
+static size_t lines_tma_smem(int len, int nst)
+{
+    return ((size_t)nst * 6 * len + len + len / 32 + 32) * sizeof(double) + 1024;   // stages + z staging
+}
+
+// z (Y region) <- scratch: line l (column i = N-1-l), element k (row j = k+1); 32x32 tiles
+__global__ void k_ysc_transpose(int nl, int len, long P, int N, const double *__restrict__ ysc, double *z)
+{
+    __shared__ double t[32][33];
+    const int l0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int l = l0 + r, k = k0 + threadIdx.x;
+        if (l < nl && k < len) t[r][threadIdx.x] = ysc[(long)l * len + k];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int k = k0 + r, l = l0 + 31 - threadIdx.x;   // consecutive lanes: consecutive columns i
+        if (k < len && l < nl && l >= l0) z[(long)(k + 1) * P + (N - 1 - l)] = t[31 - threadIdx.x][r];
+    }
+}
+
+// the TMA-staged line kernel, when the line length allows it (multiple of 64, at most 4096)
+static bool launch_lines_tma(Ctx *c, const double *v, double *z)
+{
+    const int len = c->n, T = c->lines_threads, K = (len + T - 1) / T;
+    // 1 KB aligned boxes (the 128B swizzle phase) need len % 128 == 0
+    if (len % 128 != 0 || len > 4096 || (K != 8 && K != 16) || T * K != len || c->no_lines_tma) return false;
+    const int nst = lines_tma_smem(len, 2) <= 227 * 1024 - 2048 ? 2 : 1;
+    if (lines_tma_smem(len, nst) > 227 * 1024 - 2048) return false;
+    const size_t sm = lines_tma_smem(len, nst);
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_lines_tma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 2048) != cudaSuccess ||
+            cudaFuncSetAttribute(k_lines_tma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 2048) != cudaSuccess)
+            return false;
+        attr = true;
+    }
+    LineMaps m;
+    const int nl = c->n - 1;
+    const unsigned long long rows = (unsigned long long)nl * len / 16;
+    const LineChain *chs[2] = {&c->chX, &c->chY};
+    for (int ci = 0; ci < 2; ++ci) {
+        const double *fa[4] = {chs[ci]->p, chs[ci]->e, chs[ci]->al, chs[ci]->be};
+        for (int f = 0; f < 4; ++f) {
+            const CUtensorMap *t = tmap2d(c, fa[f], 16, rows, 128, 16, (unsigned)(len / 16), true);
+            if (!t) return false;
+            m.f[ci][f] = *t;
+        }
+    }
+    const int vxr = len / 16 + 1, nvx = (vxr + 255) / 256, vxb = ((vxr + nvx - 1) / nvx + 7) / 8 * 8;
+    const CUtensorMap *tx = tmap2d(c, v, 16, (unsigned long long)c->G / 16, 128, 16, (unsigned)vxb, true);
+    const CUtensorMap *ty = tmap2d(c, v, (unsigned long long)c->P, (unsigned long long)c->N + 1,
+                                   (unsigned long long)c->P * 8, 2, (unsigned)std::min(len, 256), false);
+    if (!tx || !ty) return false;
+    m.vx = *tx; m.vy = *ty;
+    const int nb = (int)c->chunks.size();
+    double *ysc = c->cbuf;                              // free during the FGMRES iterations
+    if (K == 8) k_lines_tma<8><<<nb, T, sm, c->st>>>(c->chX, c->chY, c->d_chunks, z, ysc, c->N, c->P, nst, m);
+    else k_lines_tma<16><<<nb, T, sm, c->st>>>(c->chX, c->chY, c->d_chunks, z, ysc, c->N, c->P, nst, m);
+    k_ysc_transpose<<<dim3((nl + 31) / 32, (len + 31) / 32), dim3(32, 8), 0, c->st>>>(nl, len, c->P, c->N, ysc, z);
+    c->launches += 2;
+    return true;
+}
+
 void launch_lines(Ctx *c, const double *v, double *z)
 {
     const int T = c->lines_threads, K = (c->n + T - 1) / T;
@@ -291,6 +515,7 @@ void launch_lines(Ctx *c, const double *v, double *z)
     double bytes = 0;   // algorithmic: v + 4 factors read, z written, per node of X and Y
     bytes = 2.0 * (c->n - 1) * c->n * 48.0;
     ProfScope ps(c, 2, bytes);
+    if (launch_lines_tma(c, v, z)) return;
     if (K <= 1) k_lines<1><<<nb, T, 0, c->st>>>(c->chX, c->chY, c->d_chunks, v, z);
     else if (K <= 2) k_lines<2><<<nb, T, 0, c->st>>>(c->chX, c->chY, c->d_chunks, v, z);
     else if (K <= 4) k_lines<4><<<nb, T, 0, c->st>>>(c->chX, c->chY, c->d_chunks, v, z);

@@ -44,6 +44,7 @@
 #include <type_traits>
 
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace spp {
 
@@ -84,20 +85,6 @@ __device__ __forceinline__ int ld_acquire_cta(const int *p)
 __device__ __forceinline__ void st_relaxed(double *p, double v)
 {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
-}
-__device__ __forceinline__ void tma_load(unsigned dst, const CUtensorMap *tm, int x, int y, unsigned bar)
-{
-    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-                 ::"r"(dst), "l"(tm), "r"(x), "r"(y), "r"(bar) : "memory");
-}
-__device__ __forceinline__ void tma_prefetch(const CUtensorMap *tm, int x, int y)
-{
-    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(tm), "r"(x), "r"(y) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity)
-{
-    asm volatile("{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W%=;\n}"
-                 ::"r"(bar), "r"(parity) : "memory");
 }
 
 template <bool YFORM, bool CHAIN>
@@ -430,6 +417,24 @@ static const CUtensorMap *sheared_map(Ctx *c, const double *base, long pitch, lo
                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (rc != CUDA_SUCCESS) return nullptr;
     return &(c->tmaps[key] = tm);
+}
+
+// Generic 2D fp64 tensor map (dims d0 x d1 elements, row stride in bytes, box b0 x b1), cached.
+const CUtensorMap *tmap2d(Ctx *c, const void *base, unsigned long long d0, unsigned long long d1,
+                          unsigned long long stride_bytes, unsigned b0, unsigned b1, bool swz128)
+{
+    auto key = std::make_tuple(base, d0, d1, stride_bytes, b0, b1, swz128);
+    auto it = c->tmaps2.find(key);
+    if (it != c->tmaps2.end()) return &it->second;
+    CUtensorMap tm;
+    cuuint64_t dim[2] = {(cuuint64_t)d0, (cuuint64_t)d1};
+    cuuint64_t str[1] = {(cuuint64_t)stride_bytes};
+    cuuint32_t box[2] = {b0, b1}, es[2] = {1, 1};
+    CUresult rc = g_encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)base, dim, str, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) return nullptr;
+    return &(c->tmaps2[key] = tm);
 }
 
 static bool wave_maps(Ctx *c, const WaveArgs &a, long rows_v, long rows_c, WaveMaps *m)

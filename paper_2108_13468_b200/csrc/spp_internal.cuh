@@ -130,6 +130,8 @@ struct Ctx {
     int *chain_flags = nullptr;
     Tune tune;
     std::map<std::tuple<const void *, long, long>, CUtensorMap> tmaps;   // sheared TMA maps (k_mg.cu)
+    std::map<std::tuple<const void *, unsigned long long, unsigned long long, unsigned long long, unsigned, unsigned, bool>,
+             CUtensorMap> tmaps2;          // generic 2D maps (tmap2d)
     cudaError_t sticky = cudaSuccess;      // first launch-configuration error of a solve
     double *mg_block = nullptr;
     int *flags = nullptr; int epoch = 0;
@@ -155,6 +157,7 @@ struct Ctx {
     int64_t cg_body_launches = 0;          // kernels per loop iteration
     bool capturing = false;
     int use_graph = 1;
+    int no_lines_tma = 0;                  // SPP_NO_LINES_TMA=1: LSU-loaded line kernel
 };
 
 // kernels / launchers (defined in the .cu files)
@@ -167,6 +170,8 @@ void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, dou
 void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform, int cls, double bytes);
 void launch_ycoef(Ctx *c, int nl, long pc, const double *aE, const double *aN, const double *cd, double *ya, double *yn);
 cudaError_t wave_init();
+const CUtensorMap *tmap2d(Ctx *c, const void *base, unsigned long long d0, unsigned long long d1,
+                          unsigned long long stride_bytes, unsigned b0, unsigned b1, bool swz128);
 void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e);
 void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew, const double *b, double *rho,
                          double *part, const MGState *ms = nullptr);
