@@ -934,28 +934,50 @@ cudaError_t setup_mg_tiles(Ctx *c)
             for (int h = 8; h <= T.gs_max_halo; h += 8)
                 if (h * std::log(rho) <= std::log(1e-17)) { halo = h; break; }
         const int n = L.n;
-        const int rows_cta = 32 * Wt;
-        if (n <= rows_cta) {                                   // one CTA, exact
-            L.tile_warps = (n + 31) / 32;
-            L.tile_rows = n; L.tile_cols = n; L.halo_x = 0; L.halo_y = 0;
-        } else if (halo < 0 || halo + 16 > rows_cta) {         // no certified halo: exact chain
-            L.tile_warps = 0;
-        } else {
-            L.tile_warps = Wt;
-            L.halo_y = halo;
-            L.tile_rows = rows_cta - halo;
-            L.halo_x = halo;
-            // column tiles: the time of a tile grows with its width (wavefront chunks), so use as
-            // many column tiles as fit one wave of one CTA per SM (>= 64 columns each)
-            const int nrt = (n + L.tile_rows - 1) / L.tile_rows;
-            int nct = std::max(1, c->sm_count / nrt);
-            nct = std::min(nct, std::max(1, n / 64));
-            int tc = (n + nct - 1) / nct;
-            tc = (tc + 15) / 16 * 16;
-            if (T.gs_tile_cols > 0) tc = std::min(n, T.gs_tile_cols);
-            L.tile_cols = std::min(n, tc);
-            if (L.tile_cols >= n) { L.tile_cols = n; L.halo_x = 0; }
+        // A tile's sweep takes about (chunks + 5 (W - 1)) chunk-times: each of its W warps starts
+        // 5 chunks after the one above (62-column lane skew + one chunk of granularity), and a
+        // warp sweeps (tile columns + halo + 62) / 16 chunks.  Pick the warps per tile (3 or 4;
+        // the halo rows are part of the tile) and the column tiling with the smallest such time
+        // among the plans that run as one wave of one CTA per SM.
+        auto cost = [](int W, int cols) { return (cols + WLAG * 31 + WCW - 1) / WCW + 5 * (W - 1); };
+        if (halo < 0 || halo + 16 > 32 * Wt) {
+            if (n <= 32 * Wt) {                                // one CTA, exact
+                L.tile_warps = (n + 31) / 32;
+                L.tile_rows = n; L.tile_cols = n; L.halo_x = 0; L.halo_y = 0;
+            } else L.tile_warps = 0;                           // no certified halo: exact chain
+            continue;
         }
+        int bestW = 0, bestRows = 0, bestCols = 0, bestT = 1 << 30, bestN = 1 << 30;
+        if (n <= 32 * Wt) {                                    // candidate: one exact CTA
+            bestW = (n + 31) / 32; bestRows = n; bestCols = n; bestT = cost(bestW, n); bestN = 1;
+        }
+        for (int W = std::min(3, Wt); W <= Wt; ++W) {
+            const int rows_out = 32 * W - halo;
+            if (rows_out < 16 || rows_out >= n) continue;
+            const int nrt = (n + rows_out - 1) / rows_out;
+            if (nrt > c->sm_count) continue;
+            const int maxct = std::max(1, std::min(c->sm_count / nrt, n / 64));
+            for (int nct = 1; nct <= maxct; ++nct) {
+                int tc = (n + nct - 1) / nct;
+                tc = (tc + 15) / 16 * 16;
+                if (T.gs_tile_cols > 0) tc = std::min(n, T.gs_tile_cols);
+                const bool full = tc >= n;
+                const int t = cost(W, (full ? n : tc + halo));
+                const int ncta = nrt * ((n + tc - 1) / tc);
+                if (t < bestT || (t == bestT && ncta < bestN)) {
+                    bestT = t; bestN = ncta; bestW = W; bestRows = rows_out; bestCols = full ? n : tc;
+                }
+            }
+        }
+        L.tile_warps = bestW;
+        L.tile_rows = bestRows;
+        L.tile_cols = bestCols;
+        const bool exact1 = bestRows >= n;
+        L.halo_y = exact1 ? 0 : halo;
+        L.halo_x = bestCols >= n ? 0 : halo;
+        if (getenv("SPP_DEBUG_TILES"))
+            fprintf(stderr, "[spp] level %d n=%d rho=%.4f halo=%d: warps %d tile %dx%d (+%d,%d) cost %d chunks, %d CTAs\n",
+                    l, n, rho, halo, L.tile_warps, L.tile_rows, L.tile_cols, L.halo_y, L.halo_x, bestT, bestN);
     }
     return cudaSuccess;
 }
