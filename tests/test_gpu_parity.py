@@ -285,3 +285,45 @@ def test_table2_on_gpu():
             res, ores = _solve1d("ex1d", N, eps, spp.SPP_LEFT, spp.SPP_STOP_ABS_MAX, np.log(N) / N)
             assert res.stats["iters"] == int(row[col]) == ores["iters"], (eps, N)
             assert rel(host(res.u), ores["u"]) <= 1e-9
+
+
+# ------------------------------------------------------------------ execution-path equivalence
+def _with_env(var, fn):
+    import os
+    old = os.environ.get(var)
+    os.environ[var] = "1"
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ[var]
+        else:
+            os.environ[var] = old
+
+
+@pytest.mark.parametrize("name,N,eps,opt", [("cfg4", 512, 1e-8, {}), ("cfg5", 256, 1e-2, {}),
+                                           ("cfg4", 256, 1e-8, {"mg_max_cycles": 2})])
+def test_corner_graph_matches_host_loop(name, N, eps, opt):
+    """The corner solve as a CUDA graph with a device-side while loop (DESIGN.md "The corner
+    solve as a CUDA graph") makes the same per-cycle decisions as the host-driven loop: same
+    cycle counts, cap hits and iterates, bit for bit; and both match the oracle."""
+    cfg, x, y, f, r_graph, ores, u_graph = _solve_pair(name, N, eps, **opt)
+    _, _, _, _, r_host, _, u_host = _with_env("SPP_NO_GRAPH", lambda: _solve_pair(name, N, eps, **opt))
+    for k in ("iters", "mg_cycles_total", "mg_cycles_min", "mg_cycles_max", "mg_cap_hits"):
+        assert r_graph.stats[k] == r_host.stats[k], k
+    assert np.array_equal(u_graph, u_host)
+    assert r_graph.stats["mg_cycles_total"] == ores["mg_cycles_total"]
+    assert rel(u_graph, ores["u"]) <= 1e-9
+    if opt.get("mg_max_cycles"):
+        assert r_graph.stats["mg_cap_hits"] == r_graph.stats["iters"] > 0
+
+
+@pytest.mark.parametrize("name,N,eps", [("cfg3", 1024, None), ("cfg4", 512, 1e-8)])
+def test_tma_line_kernel_matches_lsu_kernel(name, N, eps):
+    """The TMA-staged line-chain kernel (k_lines_tma, line length a multiple of 128) computes the
+    same arithmetic in the same order as the LSU-loaded one: identical results."""
+    cfg, x, y, f, r_tma, ores, u_tma = _solve_pair(name, N, eps)
+    _, _, _, _, r_lsu, _, u_lsu = _with_env("SPP_NO_LINES_TMA", lambda: _solve_pair(name, N, eps))
+    assert r_tma.stats["iters"] == r_lsu.stats["iters"]
+    assert np.array_equal(u_tma, u_lsu)
+    assert rel(u_tma, ores["u"]) <= 1e-9
