@@ -57,7 +57,33 @@ constexpr int WWARP = WNS * WSLOT;            // doubles per warp (48 KB, a 1 KB
 constexpr int WMAXW = 4;         // sweeping warps per CTA (max); +1 TMA producer warp
 constexpr int WEB = 128;         // edge ring (columns)
 constexpr int WPF = 8;           // L2 prefetch distance (chunks)
-constexpr int WLAG = 2;          // lane-to-lane skew (columns)
+constexpr int WLAG = 2;
+// timing experiments only (wrong results): compile with -DEXP_...
+#ifdef EXP_NOSPIN
+constexpr bool EXPF_NOSPIN = true;
+#else
+constexpr bool EXPF_NOSPIN = false;
+#endif
+#ifdef EXP_NOMBAR
+constexpr bool EXPF_NOMBAR = true;
+#else
+constexpr bool EXPF_NOMBAR = false;
+#endif
+#ifdef EXP_NOE
+constexpr bool EXPF_NOE = true;
+#else
+constexpr bool EXPF_NOE = false;
+#endif
+#ifdef EXP_NOSTS
+constexpr bool EXPF_NOSTS = true;
+#else
+constexpr bool EXPF_NOSTS = false;
+#endif
+#ifdef EXP_NOEDGE
+constexpr bool EXPF_NOEDGE = true;
+#else
+constexpr bool EXPF_NOEDGE = false;
+#endif          // lane-to-lane skew (columns)
 
 struct WaveMaps { CUtensorMap q, a1, a2, cd; };
 
@@ -84,7 +110,14 @@ __device__ __forceinline__ int ld_acquire_cta(const int *p)
 }
 __device__ __forceinline__ void st_relaxed(double *p, double v)
 {
-    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)));
+}
+// two consecutive values (16-byte aligned p); each 8-byte element is single-copy atomic, which is
+// all the value-polling consumer needs
+__device__ __forceinline__ void st_relaxed2(double *p, double v0, double v1)
+{
+    asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(__double_as_longlong(v0)),
+                 "l"(__double_as_longlong(v1)));
 }
 
 template <bool YFORM, bool CHAIN>
@@ -242,9 +275,13 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
         // lane-divergent spin sends the shuffles below down the slow emulation path)
         SPP_TP(ta);
         const int need = min(ncols, c * WCW + WCW);
+#ifdef EXP_NOSPIN
+        if (false) {
+#else
         if (w > 0) {
+#endif
             while (ld_acquire_cta(&prod[w - 1]) < need) __nanosleep(32);   // back off: spinning loads slow the working warps' smem traffic
-        } else if (chain_in) {
+        } else if (chain_in && !EXPF_NOSPIN) {
             // the strip above publishes its bottom row value by value into a buffer preset to the
             // sentinel (no fence on the producer side): lanes 0..15 poll the chunk's 16 columns
             // (the load for chunk c was issued during chunk c-1: vin, so the L2 round trip overlaps
@@ -262,12 +299,12 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
             __syncwarp();
             if (lane < 16 && (c + 1) * WCW + lane < ncols) vin = ld_relaxed_u64(src + WCW);   // chunk c+1
         }
-        if (has_consumer) {                             // back-pressure on the edge ring
+        if (has_consumer && !EXPF_NOSPIN) {             // back-pressure on the edge ring
             const int lim = c * WCW + WCW - WLAG * 31 - WEB;
             if (lim > 0) { while (*((volatile int *)&cons[w + 1]) < lim) __nanosleep(32); }
         }
         SPP_TP(tb);
-        mbar_wait((unsigned)__cvta_generic_to_shared(&bars[w][c % WNS]), (unsigned)((c / WNS) & 1));
+        if (!EXPF_NOMBAR) mbar_wait((unsigned)__cvta_generic_to_shared(&bars[w][c % WNS]), (unsigned)((c / WNS) & 1));
         __syncwarp();
         SPP_TP(tc);
         double *sq = ring + (size_t)(c % WNS) * WSLOT;
@@ -282,10 +319,10 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
             A1[st] = *reinterpret_cast<const double2 *>(sq + WBOX + xo[st]);
             A2[st] = *reinterpret_cast<const double2 *>(sq + 2 * WBOX + xo[st]);
         }
-        if (w > 0) {
+        if (w > 0 && !EXPF_NOE) {
 #pragma unroll
             for (int st = 0; st < 8; ++st) E[st] = *reinterpret_cast<const double2 *>(&edge[w - 1][(c * WCW + 2 * st) & (WEB - 1)]);
-        } else if (chain_in) {
+        } else if (chain_in && !EXPF_NOE) {
 #pragma unroll
             for (int st = 0; st < 8; ++st) E[st] = *reinterpret_cast<const double2 *>(&cin[2 * st]);
         } else {
@@ -311,18 +348,31 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
                 Z[2 * st] = za; Z[2 * st + 1] = zc;
                 z2 = za; z1 = zc;
             }
+            if (!EXPF_NOSTS) {
 #pragma unroll
             for (int st = 0; st < 8; ++st)
                 *reinterpret_cast<double2 *>(sq + xo[st]) = make_double2(Z[2 * st + 1], Z[2 * st]);   // y in place of q
-            if (lane == 31) {                                   // hand the bottom row to the next strip
-                double *eo = &edge[w][0];
-                double *co = CHAIN ? a.chain_buf + (long)blockIdx.y * a.chain_ld : nullptr;
+            }
+            // hand the bottom row to the next strip (lane 31's pairs): branch-free predicated
+            // stores on interior chunks, element-wise checks at the edges
+            double *eo = &edge[w][0];
+            double *co = CHAIN ? a.chain_buf + (long)blockIdx.y * a.chain_ld : nullptr;
+            if (F) {
+                const bool e31 = lane == 31 && has_consumer && !EXPF_NOEDGE;
+                const bool c31 = CHAIN && lane == 31 && chain_out && !EXPF_NOEDGE;
 #pragma unroll
                 for (int st = 0; st < 8; ++st) {
                     const int idx = c * WCW + 2 * st - WLAG * 31;
-                    if (F || (idx >= 0 && idx + 1 < ncols)) {
+                    if (e31) *reinterpret_cast<double2 *>(eo + (idx & (WEB - 1))) = make_double2(Z[2 * st], Z[2 * st + 1]);
+                    if (c31) st_relaxed2(co + idx, Z[2 * st], Z[2 * st + 1]);
+                }
+            } else if (lane == 31 && !EXPF_NOEDGE) {
+#pragma unroll
+                for (int st = 0; st < 8; ++st) {
+                    const int idx = c * WCW + 2 * st - WLAG * 31;
+                    if (idx >= 0 && idx + 1 < ncols) {
                         if (has_consumer) *reinterpret_cast<double2 *>(eo + (idx & (WEB - 1))) = make_double2(Z[2 * st], Z[2 * st + 1]);
-                        if (CHAIN && chain_out) { st_relaxed(co + idx, Z[2 * st]); st_relaxed(co + idx + 1, Z[2 * st + 1]); }
+                        if (CHAIN && chain_out) st_relaxed2(co + idx, Z[2 * st], Z[2 * st + 1]);
                     } else if (idx >= 0 && idx < ncols) {   // last odd column
                         if (has_consumer) eo[idx & (WEB - 1)] = Z[2 * st];
                         if (CHAIN && chain_out) st_relaxed(co + idx, Z[2 * st]);
