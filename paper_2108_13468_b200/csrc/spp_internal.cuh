@@ -75,7 +75,7 @@ struct Tune {
     int gs_warps = 4;          // warps (32-row strips) per GS tile
     int gs_tile_cols = 0;      // output columns per GS tile (0: one wave of CTAs per level)
     int gs_max_halo = 128;     // no certified halo below this -> exact chained sweep
-    int sweep_warps = 4;       // warps per CTA of the exact chained sweep (M_II)
+    int sweep_warps = 2;       // warps per CTA of the exact chained sweep (M_II; 2 measured best)
     int coarse_max = 64;       // levels with n <= this run as one fused single-CTA V-cycle
 };
 
