@@ -327,3 +327,23 @@ def test_tma_line_kernel_matches_lsu_kernel(name, N, eps):
     assert r_tma.stats["iters"] == r_lsu.stats["iters"]
     assert np.array_equal(u_tma, u_lsu)
     assert rel(u_tma, ores["u"]) <= 1e-9
+
+
+@pytest.mark.parametrize("eps", [1e-6, 1e-10])
+def test_cfg5_at_2048(eps):
+    """cfg5's data (B:11: c = (1,2), r = 1, seeded random f) at N = 2048 (4.2M unknowns): the
+    tiled corner levels, the TMA line kernel (lines of 1024) and the 2-warp M_II chain at a size
+    between the proxies and the bench, against the oracle."""
+    cfg, x, y, f, res, ores, u = _solve_pair("cfg5", 2048, eps)
+    assert res.stats["iters"] == ores["iters"]
+    assert res.stats["mg_cycles_total"] == ores["mg_cycles_total"]
+    assert rel(u, ores["u"]) <= 1e-9
+
+
+def test_full_size_cfg5_eps_1e10():
+    """cfg5 (B:11) at its BASELINE size, 8192^2 (67M unknowns), eps = 1e-10: full parity with the
+    oracle (the largest single-GPU configuration; 3 iterations)."""
+    cfg, x, y, f, res, ores, u = _solve_pair("cfg5", 8192, 1e-10)
+    assert res.stats["iters"] == ores["iters"]
+    assert res.stats["mg_cycles_total"] == ores["mg_cycles_total"]
+    assert rel(u, ores["u"]) <= 1e-9
