@@ -347,3 +347,15 @@ def test_full_size_cfg5_eps_1e10():
     assert res.stats["iters"] == ores["iters"]
     assert res.stats["mg_cycles_total"] == ores["mg_cycles_total"]
     assert rel(u, ores["u"]) <= 1e-9
+
+
+@pytest.mark.parametrize("name,N,eps", [("cfg4", 512, 1e-8), ("cfg5", 256, 1e-2)])
+def test_scan_line_factorisation_matches_sequential(name, N, eps):
+    """The block-scan Thomas factorisation (2x2 matrix prefix products) and the sequential
+    per-line sweep give the same preconditioner up to rounding: same iterations, solutions within
+    the parity bar of each other and of the oracle."""
+    cfg, x, y, f, r_scan, ores, u_scan = _solve_pair(name, N, eps)
+    _, _, _, _, r_seq, _, u_seq = _with_env("SPP_SEQ_LINE_FACTOR", lambda: _solve_pair(name, N, eps))
+    assert r_scan.stats["iters"] == r_seq.stats["iters"] == ores["iters"]
+    assert rel(u_scan, u_seq) <= 1e-12
+    assert rel(u_scan, ores["u"]) <= 1e-9
