@@ -571,14 +571,12 @@ static spp_status do_setup_2d(Ctx *c, const double *c1, const double *c2, const 
     }
     int *bad = c->flags + 200;
     CK(c, cudaMemsetAsync(bad, 0, sizeof(int), c->st));
-    k_validate<<<nblk((long)mm), 256, 0, c->st>>>((long)mm, d1, d2, d3, bad);
     k_coef_1d<<<nblk(N + 1), 256, 0, c->st>>>(N, c->eps, c->hx, c->Hx, c->hy, c->Hy, c->aW, c->aS);
     k_coef_2d<<<nblk((long)mm), 256, 0, c->st>>>(N, c->P, c->eps, c->hx, c->Hx, c->hy, c->Hy, d1, d2, d3, c->aW,
-                                                c->aS, c->aE, c->aN, c->rr, c->ca, c->cn, c->cd);
+                                                c->aS, c->aE, c->aN, c->rr, c->ca, c->cn, c->cd, c->ya, c->yn, bad);
     Level &L0 = c->lev[0];
     k_level0_1d<<<1, 256, 0, c->st>>>(N, c->hx, c->Hx, c->hy, c->Hy, c->aW, c->aS, L0.aW, L0.aS, L0.hb, L0.kb);
-    c->launches += 4;
-    launch_ycoef(c, m, c->P, c->aE, c->aN, c->cd, c->ya, c->yn);
+    c->launches += 3;
     for (int l = 1; l < c->L; ++l) {
         Level &Lv = c->lev[l];
         // (k_coef_level writes aE/D, aN/D into ya, yn; launch_ycoef then replaces them by the

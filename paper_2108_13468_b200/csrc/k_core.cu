@@ -24,27 +24,42 @@ __global__ void k_coef_1d(int N, double eps, double hx, double Hx, double hy, do
     }
 }
 
-// aE, aN, r, and the sweep coefficients aE/D, aN/D, 1/D on the padded global grid.
-// c1, c2, r are compact ((N-1)^2, x fastest).
+// aE, aN, r, the sweep coefficients aE/D, aN/D, 1/D and the y-form couplings aE/D_E, aN/D_N on
+// the padded global grid, with the input validation fused in (c1 > 0, c2 > 0, r >= 0, finite;
+// P:208-212).  c1, c2, r are compact ((N-1)^2, x fastest).  D_E and D_N (the diagonal
+// at the East / North neighbour) are recomputed from the neighbour's samples with the same
+// arithmetic; beyond the last interior node they are absent (the coupling is 0).
+__device__ __forceinline__ void coef_at(int i, int j, int n, double eps, double hx, double Hx, double hy,
+                                        double Hy, double c1, double c2, double r, const double *aW,
+                                        const double *aS, double &e, double &no, double &D)
+{
+    const double h = i <= n ? hx : Hx, h1 = (i + 1) <= n ? hx : Hx, hb = 0.5 * (h + h1);
+    const double k = j <= n ? hy : Hy, k1 = (j + 1) <= n ? hy : Hy, kb = 0.5 * (k + k1);
+    e = eps / (hb * h1) + c1 / h1;
+    no = eps / (kb * k1) + c2 / k1;
+    D = ((aW[i] + e) + (aS[j] + no)) + r;
+}
+
 __global__ void k_coef_2d(int N, long P, double eps, double hx, double Hx, double hy, double Hy,
                           const double *c1, const double *c2, const double *r, const double *aW,
                           const double *aS, double *aE, double *aN, double *rr, double *ca,
-                          double *cn, double *cd)
+                          double *cn, double *cd, double *ya, double *yn, int *bad)
 {
     const int n = N / 2, m = N - 1;
     const long tot = (long)m * m;
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
         const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
-        const double h = i <= n ? hx : Hx, h1 = (i + 1) <= n ? hx : Hx, hb = 0.5 * (h + h1);
-        const double k = j <= n ? hy : Hy, k1 = (j + 1) <= n ? hy : Hy, kb = 0.5 * (k + k1);
-        const double e = eps / (hb * h1) + c1[p] / h1;
-        const double no = eps / (kb * k1) + c2[p] / k1;
-        const double rv = r[p];
-        const double D = ((aW[i] + e) + (aS[j] + no)) + rv;
+        const double a = c1[p], b = c2[p], rv = r[p];
+        if (!(a > 0.0) || !(b > 0.0) || !(rv >= 0.0) || !isfinite(a) || !isfinite(b) || !isfinite(rv)) atomicOr(bad, 1);
+        double e, no, D;
+        coef_at(i, j, n, eps, hx, Hx, hy, Hy, a, b, rv, aW, aS, e, no, D);
         const long g = (long)j * P + i;
         aE[g] = e; aN[g] = no; rr[g] = rv;
         ca[g] = e / D; cn[g] = no / D; cd[g] = 1.0 / D;
-        (void)h; (void)k;
+        double cdE = 0.0, cdN = 0.0, t0, t1, DD;
+        if (i < m) { coef_at(i + 1, j, n, eps, hx, Hx, hy, Hy, c1[p + 1], c2[p + 1], r[p + 1], aW, aS, t0, t1, DD); cdE = 1.0 / DD; }
+        if (j < m) { coef_at(i, j + 1, n, eps, hx, Hx, hy, Hy, c1[p + m], c2[p + m], r[p + m], aW, aS, t0, t1, DD); cdN = 1.0 / DD; }
+        ya[g] = e * cdE; yn[g] = no * cdN;
     }
 }
 
