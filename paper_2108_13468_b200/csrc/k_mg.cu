@@ -303,22 +303,9 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
             const int lim = c * WCW + WCW - WLAG * 31 - WEB;
             if (lim > 0) { while (*((volatile int *)&cons[w + 1]) < lim) __nanosleep(32); }
         }
-        SPP_TP(tb);
-        if (!EXPF_NOMBAR) mbar_wait((unsigned)__cvta_generic_to_shared(&bars[w][c % WNS]), (unsigned)((c / WNS) & 1));
-        __syncwarp();
-        SPP_TP(tc);
-        double *sq = ring + (size_t)(c % WNS) * WSLOT;
-        // Two columns per step (the lane skew is two columns, so lane t-1 finished this pair one
-        // step earlier, and the pair shares one 16-byte swizzle unit: one 128-bit load per array).
-        // Every shared-memory load of the chunk is issued before the first store: a store ahead
-        // of a possibly aliasing load would serialise the load behind it.
-        double2 Q[8], A1[8], A2[8], E[8];
-#pragma unroll
-        for (int st = 0; st < 8; ++st) {                        // columns 2st, 2st+1 of the chunk
-            Q[st] = *reinterpret_cast<const double2 *>(sq + xo[st]);     // (2st+1, 2st) as (lo, hi)
-            A1[st] = *reinterpret_cast<const double2 *>(sq + WBOX + xo[st]);
-            A2[st] = *reinterpret_cast<const double2 *>(sq + 2 * WBOX + xo[st]);
-        }
+        // the North inflow of the chunk, loaded before the operand wait: lane 0 needs E[0] at the
+        // first step, and a load queued behind the 24 operand loads delays the whole step chain
+        double2 E[8];
         if (w > 0 && !EXPF_NOE) {
 #pragma unroll
             for (int st = 0; st < 8; ++st) E[st] = *reinterpret_cast<const double2 *>(&edge[w - 1][(c * WCW + 2 * st) & (WEB - 1)]);
@@ -328,6 +315,22 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
         } else {
 #pragma unroll
             for (int st = 0; st < 8; ++st) E[st] = make_double2(0.0, 0.0);
+        }
+        SPP_TP(tb);
+        if (!EXPF_NOMBAR) mbar_wait((unsigned)__cvta_generic_to_shared(&bars[w][c % WNS]), (unsigned)((c / WNS) & 1));
+        __syncwarp();
+        SPP_TP(tc);
+        double *sq = ring + (size_t)(c % WNS) * WSLOT;
+        // Two columns per step (the lane skew is two columns, so lane t-1 finished this pair one
+        // step earlier, and the pair shares one 16-byte swizzle unit: one 128-bit load per array).
+        // Every shared-memory load of the chunk is issued before the first store: a store ahead
+        // of a possibly aliasing load would serialise the load behind it.
+        double2 Q[8], A1[8], A2[8];
+#pragma unroll
+        for (int st = 0; st < 8; ++st) {                        // columns 2st, 2st+1 of the chunk
+            Q[st] = *reinterpret_cast<const double2 *>(sq + xo[st]);     // (2st+1, 2st) as (lo, hi)
+            A1[st] = *reinterpret_cast<const double2 *>(sq + WBOX + xo[st]);
+            A2[st] = *reinterpret_cast<const double2 *>(sq + 2 * WBOX + xo[st]);
         }
         if (w > 0 && lane == 0) *((volatile int *)&cons[w]) = need;
         auto steps = [&](auto fast_tag) {
