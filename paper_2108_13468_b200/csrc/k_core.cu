@@ -106,16 +106,6 @@ __global__ void k_level0_1d(int N, double hx, double Hx, double hy, double Hy, c
     }
 }
 
-// validation: c1 > 0, c2 > 0, r >= 0, all finite
-__global__ void k_validate(long tot, const double *c1, const double *c2, const double *r, int *bad)
-{
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const double a = c1[p], b = c2 ? c2[p] : 1.0, c = r[p];
-        if (!(a > 0.0) || !(b > 0.0) || !(c >= 0.0) || !isfinite(a) || !isfinite(b) || !isfinite(c))
-            atomicOr(bad, 1);
-    }
-}
-
 // ===================================================================================== layout
 __global__ void k_pack(int m, long P, const double *src, double *dst)   // compact -> padded
 {

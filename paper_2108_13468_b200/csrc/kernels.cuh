@@ -15,7 +15,6 @@ __global__ void k_coef_level(int N, int nl, int step, long Pl, double eps, doubl
                              double *aE, double *aN, double *rr, double *ca, double *cn, double *cd);
 __global__ void k_level0_1d(int N, double hx, double Hx, double hy, double Hy, const double *aW,
                             const double *aS, double *lW, double *lS, double *hb, double *kb);
-__global__ void k_validate(long tot, const double *c1, const double *c2, const double *r, int *bad);
 __global__ void k_pack(int m, long P, const double *src, double *dst);
 __global__ void k_unpack(int m, long P, const double *src, double *dst);
 __global__ void k_spmv(int m, long P, const double *z, const double *aE, const double *aN,
