@@ -48,7 +48,7 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg4")
-    ap.add_argument("--n", type=int, default=None, help="override N (diagnostics only)")
+    ap.add_argument("--n", "--size", dest="n", type=int, default=None, help="override N (diagnostics only)")
     ap.add_argument("--eps", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -145,6 +145,17 @@ def run_reference(args, rank, world):
 
 
 # ---------------------------------------------------------------------------- our arm
+def max_over_ranks(ms, world, device):
+    """The step time of the job: the maximum over ranks (one value per rank, all_reduce MAX on the
+    process group; gloo on CPU tensors in the tests, NCCL on the GPU in the bench)."""
+    if world <= 1:
+        return ms
+    import torch
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 def cpu_baseline(cfg):
     """The oracle timed on this host on a bounded sample: one full solve of the same workload
     (~10 s of single-threaded CPU work at 4096^2)."""
@@ -222,11 +233,8 @@ def run_ours(args, rank, world):
     torch.cuda.synchronize()
     clocks = clk.stop()
     launches = S.kernel_launches() - l0
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, dev)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
         torch.distributed.barrier()
     # roofline pass: the same steps again with CUDA events bracketing every launch of the dominant
     # kernel class (on the library's stream), for its average launch duration
@@ -255,11 +263,7 @@ def run_ours(args, rank, world):
             step(hp[0], hp[1], hp[2], hp[3], hu)
         e1.record(stream)
         torch.cuda.synchronize()
-        ems = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / ne
-        if world > 1:
-            t = torch.tensor([ems], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = max_over_ranks(max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / ne, world, dev)
         e2e = {"value": cfg.unknowns * world / (ems * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": 4 * m * m * 8, "d2h_bytes_per_step": m * m * 8, "ms_per_step": ems}
 
