@@ -359,3 +359,23 @@ def test_scan_line_factorisation_matches_sequential(name, N, eps):
     assert r_scan.stats["iters"] == r_seq.stats["iters"] == ores["iters"]
     assert rel(u_scan, u_seq) <= 1e-12
     assert rel(u_scan, ores["u"]) <= 1e-9
+
+
+@pytest.mark.parametrize("N", [512, 1024, 2048])
+def test_paper_tables_6_7_large_N_on_gpu(N):
+    """Paper mode at the larger sizes of Tables 6/7, GPU only, pinned to the
+    printed numbers: FGMRES counts exactly (Table 7) and the max-norm error to 4 digits
+    (Table 6), every apply taking the paper's 5 corner cycles."""
+    from conftest import load_table, rounds_to
+    t6, t7 = load_table("table6_exp_errors.txt"), load_table("table7_exp_iters.txt")
+    col = {128: 0, 256: 1, 512: 2, 1024: 3, 2048: 4}[N]
+    for eps in sorted(t7):
+        cfg, x, y, (c1, c2, r, f), S, P = make("exp2d", N, eps, stop=spp.SPP_STOP_ABS_L2, sigma=2.5,
+                                                bx=1.99, by=2.99)
+        P.close()
+        res = S.solve(dev(f))
+        u = host(res.u)
+        assert res.stats["iters"] == int(t7[eps][col]), (N, eps, res.stats["iters"])
+        assert res.stats["mg_cycles_min"] == 5 and res.stats["mg_cycles_max"] == 5
+        err = np.max(np.abs(u.reshape(N - 1, N - 1) - si.exact_solution(cfg, x, y)))
+        assert rounds_to(err, t6[eps][col]), (N, eps, err)
