@@ -324,7 +324,8 @@ __global__ void k_update_x(long n2, int k, const double *const *Z, const double 
 // written to the level-0 value grid; partial ||S_0 b_C||^2 (S_0 = diag(hbar_i kbar_j)).
 __global__ void __launch_bounds__(kRedThreads) k_corner_rhs(int N, long P, long P0, const double *v,
     const double *z, const double *aE, const double *aN, const double *rr, const double *aW,
-    const double *aS, const double *hb, const double *kb, int weighted, double *bc, double *part, double *bc2)
+    const double *aS, const double *hb, const double *kb, int weighted, double *bc, double *part, double *bc2,
+    const double *cd, double *q0)
 {
     __shared__ double sm[32];
     const int n = N / 2;
@@ -340,6 +341,7 @@ __global__ void __launch_bounds__(kRedThreads) k_corner_rhs(int N, long P, long 
         if (i == n) b += aE[g] * z[g + 1];
         bc[(long)j * P0 + i] = b;
         if (bc2) bc2[(long)j * P0 + i] = b;           // corner graph: the first cycle's residual
+        if (q0) q0[(long)j * P0 + i] = b * cd[g];      // z-form: the first cycle's pre-smoothing rhs
         const double t = (hb[i] * kb[j]) * b;
         acc += t * t;
     }

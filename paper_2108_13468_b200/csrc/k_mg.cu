@@ -52,9 +52,9 @@ constexpr int WCW = 16;          // columns per chunk (box width, 128 bytes)
 constexpr int WNS = 3;           // staging ring slots
 constexpr int WNA = 4;           // boxes per slot: q (overwritten in place by y), a1, a2, 1/D
 constexpr int WBOX = 32 * WCW;   // doubles per box (4 KB)
-constexpr int WSLOT = WNA * WBOX;             // doubles per staging slot (16 KB)
-constexpr int WWARP = WNS * WSLOT;            // doubles per warp (48 KB, a 1 KB multiple)
-constexpr int WMAXW = 4;         // sweeping warps per CTA (max); +1 TMA producer warp
+// doubles per staging slot: 4 boxes in y-form (16 KB), 3 in z-form (12 KB; no 1/D box)
+__host__ __device__ constexpr int wslot(bool yform) { return (yform ? WNA : WNA - 1) * WBOX; }
+constexpr int WMAXW = 5;         // sweeping warps per CTA (max; 5 only in z-form); +W write-back +1 TMA
 constexpr int WEB = 128;         // edge ring (columns)
 constexpr int WPF = 8;           // L2 prefetch distance (chunks)
 constexpr int WLAG = 2;
@@ -123,6 +123,8 @@ __device__ __forceinline__ void st_relaxed2(double *p, double v0, double v1)
 template <bool YFORM, bool CHAIN>
 __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const __grid_constant__ WaveMaps m)
 {
+    constexpr int WSLOT = wslot(YFORM);                 // doubles per staging slot
+    constexpr int WWARP = WNS * WSLOT;                  // doubles per warp (1 KB multiple)
     extern __shared__ double smem_raw[];
     __shared__ double edge[WMAXW][WEB];
     __shared__ int prod[WMAXW], cons[WMAXW];
@@ -404,7 +406,7 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
 #endif
 }
 
-static size_t wave_smem(int warps) { return sizeof(double) * (size_t)warps * WWARP + 1024; }
+static size_t wave_smem(int warps, bool yform) { return sizeof(double) * (size_t)warps * WNS * wslot(yform) + 1024; }
 
 #ifdef SPP_WAVE_PROF
 // debugging build only: per-warp cycle breakdown of the first launch of each kind
@@ -446,11 +448,11 @@ cudaError_t wave_init()
         SPP_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&g_encode, cudaEnableDefault, &q));
         if (!g_encode || q != cudaDriverEntryPointSuccess) return cudaErrorNotSupported;
     }
-    const int sm = (int)wave_smem(WMAXW);
-    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    const int smy = (int)wave_smem(4, true), smz = (int)wave_smem(WMAXW, false);
+    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smy));
+    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smz));
+    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smy));
+    SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smz));
     return cudaSuccess;
 }
 
@@ -508,7 +510,7 @@ void launch_wave(Ctx *c, WaveArgs a, long rows_v, long rows_c, int warps, bool y
     WaveMaps m;
     if (!wave_maps(c, a, rows_v, rows_c, &m)) { c->sticky = cudaErrorInvalidValue; return; }
     const dim3 grid((a.nl + a.cols_out - 1) / a.cols_out, (a.nl + a.rows_out - 1) / a.rows_out);
-    const size_t sm = wave_smem(warps);
+    const size_t sm = wave_smem(warps, yform);
     ProfScope ps(c, cls, bytes);
 #ifdef SPP_WAVE_PROF
     static long long *prof = nullptr;
@@ -537,7 +539,7 @@ void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform,
     a.chain_buf = c->chain;
     a.chain_ld = c->chain_ld;
     cudaMemsetAsync(c->chain, 0xff, sizeof(double) * (size_t)ncta * c->chain_ld, c->st);   // kChainSentinel
-    const size_t sm = wave_smem(W);
+    const size_t sm = wave_smem(W, yform);
     void *args[] = {(void *)&a, (void *)&m};
     ProfScope ps(c, cls, bytes);
 #ifdef SPP_WAVE_PROF
@@ -570,7 +572,8 @@ __device__ __forceinline__ double interp_c(const double *ec, long Pc, int i, int
 
 __global__ void __launch_bounds__(256) k_gs_prep(int nl, long pv, const double *__restrict__ e,
     const double *__restrict__ ec, long pcv, const double *__restrict__ b,
-    const double *__restrict__ aW, const double *__restrict__ aS, double *g)
+    const double *__restrict__ aW, const double *__restrict__ aS, double *g,
+    const double *__restrict__ cd, long pc)
 {
     const long tot = (long)nl * nl;
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
@@ -581,37 +584,69 @@ __global__ void __launch_bounds__(256) k_gs_prep(int nl, long pv, const double *
             ew += (i > 1) ? interp_c(ec, pcv, i - 1, j) : 0.0;
             es += (j > 1) ? interp_c(ec, pcv, i, j - 1) : 0.0;
         }
-        g[v] = (b[v] + aW[i] * ew) + aS[j] * es;
+        const double gv = (b[v] + aW[i] * ew) + aS[j] * es;
+        g[v] = cd ? gv * cd[(long)j * pc + i] : gv;   // z-form sweeps take g / D
+    }
+}
+
+// q = b / D (z-form sweep from zero for a right-hand side nobody pre-scaled: test hooks)
+__global__ void k_scale_cd(int nl, long pv, long pc, const double *__restrict__ b, const double *__restrict__ cd, double *q)
+{
+    const long tot = (long)nl * nl;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
+        q[(long)j * pv + i] = b[(long)j * pv + i] * cd[(long)j * pc + i];
     }
 }
 
 static inline int gblocks(long work) { long b = (work + 255) / 256; return (int)std::max(1L, std::min(b, 148L * 16)); }
 
-// One downstream GS sweep on level l (y-form): mode 0 from zero (q = b); mode 1 from e_old
-// (+ P ec when ec != null): q = prep(e_old [+ P ec]).
-void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, double *enew, const double *ec)
+// level l's g = b / D (z-form pre-smoothing rhs when no producer wrote it)
+void launch_scale_cd(Ctx *c, int l, const double *b)
+{
+    Level &L = c->lev[l];
+    k_scale_cd<<<gblocks((long)L.n * L.n), 256, 0, c->st>>>(L.n, L.pitch, L.cpitch, b, L.cd, L.g);
+    c->launches++;
+}
+
+// One downstream GS sweep on level l: mode 0 from zero (q = b); mode 1 from e_old (+ P ec when
+// ec != null): q = prep(e_old [+ P ec]).  z-form (c->mg_zform): z = q/D + (aE/D) z_E + (aN/D) z_N,
+// so q arrives divided by D -- q0 (b/D written by the kernel that produced b) for mode 0, the
+// prep kernel's output for mode 1; y-form: y = q + ya y_E + yn y_N, z = y/D at write-back.
+void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, double *enew, const double *ec,
+               const double *q0)
 {
     Level &L = c->lev[l];
     const double nn = (double)L.n * L.n;
+    const bool zf = c->mg_zform;
     WaveArgs a{};
     a.nl = L.n; a.pv = L.pitch; a.pc = L.cpitch;
-    a.ca = L.ya; a.cn = L.yn; a.cd = L.cd; a.z = enew;
-    if (mode == 0) a.q = b;
-    else {
+    if (zf) { a.ca = l == 0 ? c->ca : L.ya; a.cn = l == 0 ? c->cn : L.yn; }   // levels >= 1 keep aE/D, aN/D in ya, yn
+    else { a.ca = L.ya; a.cn = L.yn; }
+    a.cd = L.cd; a.z = enew;
+    if (mode == 0) {
+        if (!zf) a.q = b;
+        else if (q0) a.q = q0;
+        else {
+            k_scale_cd<<<gblocks((long)L.n * L.n), 256, 0, c->st>>>(L.n, L.pitch, L.cpitch, b, L.cd, L.g);
+            c->launches++;
+            a.q = L.g;
+        }
+    } else {
         {
-            ProfScope ps(c, 5, nn * 24.0);
+            ProfScope ps(c, 5, nn * (zf ? 32.0 : 24.0));
             k_gs_prep<<<gblocks((long)L.n * L.n), 256, 0, c->st>>>(L.n, L.pitch, eold, ec,
-                ec ? c->lev[l + 1].pitch : 0, b, L.aW, L.aS, L.g);
+                ec ? c->lev[l + 1].pitch : 0, b, L.aW, L.aS, L.g, zf ? L.cd : nullptr, L.cpitch);
             c->launches++;
             dbg_sync(c, "k_gs_prep");
         }
         a.q = L.g;
     }
-    const double bytes = nn * 40.0;   // q, ya, yn, cd read; z written
+    const double bytes = nn * (zf ? 32.0 : 40.0);   // q, couplings (+ 1/D in y-form) read; z written
     const long rows_v = L.n + 2, rows_c = l == 0 ? c->N + 1 : L.n + 2;   // level 0 shares the global coefficients
-    if (L.tile_warps == 0) { launch_wave_chain(c, a, rows_v, rows_c, true, 3, bytes); return; }
+    if (L.tile_warps == 0) { launch_wave_chain(c, a, rows_v, rows_c, !zf, 3, bytes); return; }
     a.rows_out = L.tile_rows; a.cols_out = L.tile_cols; a.halo_y = L.halo_y; a.halo_x = L.halo_x;
-    launch_wave(c, a, rows_v, rows_c, L.tile_warps, true, 3, bytes);
+    launch_wave(c, a, rows_v, rows_c, L.tile_warps, !zf, 3, bytes);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -813,7 +848,8 @@ __global__ void __launch_bounds__(256) k_resid_restrict(int nf, long pv, long pc
     const double *__restrict__ R, const double *__restrict__ aE, const double *__restrict__ aN,
     const double *__restrict__ rr, const double *__restrict__ aW, const double *__restrict__ aS,
     const double *__restrict__ hbf, const double *__restrict__ kbf, int nc, long pvc,
-    const double *__restrict__ hbc, const double *__restrict__ kbc, double *bc)
+    const double *__restrict__ hbc, const double *__restrict__ kbc, double *bc,
+    const double *__restrict__ cdc, long pcc, double *qc)
 {
     constexpr int RFW = 2 * RT + 1;
     __shared__ double s[RFW * RFW];
@@ -845,7 +881,9 @@ __global__ void __launch_bounds__(256) k_resid_restrict(int nf, long pv, long pc
             const double rs = (0.5 * srow[-1] + srow[0]) + 0.5 * srow[1];
             acc += (bb == 0 ? 1.0 : 0.5) * rs;
         }
-        bc[(long)J * pvc + I] = acc / (hbc[I] * kbc[J]);
+        const double bv = acc / (hbc[I] * kbc[J]);
+        bc[(long)J * pvc + I] = bv;
+        if (qc) qc[(long)J * pvc + I] = bv * cdc[(long)J * pcc + I];   // z-form pre-smoothing rhs
     }
 }
 
@@ -858,7 +896,8 @@ void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e)
     const int RTn = C.n >= 128 ? 16 : 8;
     const dim3 grid((C.n + RTn - 1) / RTn, (C.n + RTn - 1) / RTn);
 #define SPP_RR(T) k_resid_restrict<T><<<grid, T >= 32 ? 256 : (T >= 16 ? 256 : 128), 0, c->st>>>(F.n, F.pitch, \
-        F.cpitch, e, R, F.aE, F.aN, F.rr, F.aW, F.aS, F.hb, F.kb, C.n, C.pitch, C.hb, C.kb, C.b)
+        F.cpitch, e, R, F.aE, F.aN, F.rr, F.aW, F.aS, F.hb, F.kb, C.n, C.pitch, C.hb, C.kb, C.b, C.cd, C.cpitch, \
+        c->mg_zform ? C.g : nullptr)
     if (RTn == 32) SPP_RR(32);
     else if (RTn == 16) SPP_RR(16);
     else SPP_RR(8);
@@ -876,7 +915,7 @@ __global__ void __launch_bounds__(kRedThreads) k_cycle_update(int nl, long pv, l
     const double *__restrict__ e, double *znew, const double *__restrict__ b, const double *__restrict__ aE,
     const double *__restrict__ aN, const double *__restrict__ rr, const double *__restrict__ aW,
     const double *__restrict__ aS, const double *__restrict__ hb, const double *__restrict__ kb, double *rho,
-    double *part, const MGState *ms)
+    double *part, const MGState *ms, const double *__restrict__ cd, double *q0)
 {
     __shared__ double sm[32];
     if (ms) { z = ms->zcur; znew = ms->znext; }        // corner graph: buffers from the device state
@@ -891,6 +930,7 @@ __global__ void __launch_bounds__(kRedThreads) k_cycle_update(int nl, long pv, l
         const double r = b[g] - Az;
         znew[g] = zc;
         rho[g] = r;
+        if (q0) q0[g] = r * cd[q];                      // z-form: the next cycle's pre-smoothing rhs
         const double t = (hb[i] * kb[j]) * r;
         acc += t * t;
     }
@@ -912,9 +952,10 @@ void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew,
 {
     Level &L = c->lev[0];
     const double nn = (double)L.n * L.n;
-    ProfScope ps(c, 6, nn * (z ? 64.0 : 56.0));
+    ProfScope ps(c, 6, nn * ((z ? 64.0 : 56.0) + (c->mg_zform ? 16.0 : 0.0)));
     k_cycle_update<<<kRedBlocks, kRedThreads, 0, c->st>>>(L.n, L.pitch, L.cpitch, z, e, znew, b, L.aE, L.aN, L.rr,
-                                                          L.aW, L.aS, L.hb, L.kb, rho, part, ms);
+                                                          L.aW, L.aS, L.hb, L.kb, rho, part, ms, L.cd,
+                                                          c->mg_zform ? L.g : nullptr);
     c->launches++;
 }
 
@@ -968,7 +1009,7 @@ void launch_ycoef(Ctx *c, int nl, long pc, const double *aE, const double *aN, c
 cudaError_t setup_mg_tiles(Ctx *c)
 {
     const Tune &T = c->tune;
-    const int Wt = std::max(1, std::min(T.gs_warps, WMAXW));
+    const int Wt = std::max(1, std::min(T.gs_warps, c->mg_zform ? WMAXW : 4));   // 5 warps only fit in z-form
     for (int l = 0; l < c->L; ++l) {
         k_level_rho<<<kRedBlocks, kRedThreads, 0, c->st>>>(c->lev[l].n, c->lev[l].cpitch, c->lev[l].aE,
                                                            c->lev[l].aN, c->lev[l].cd, c->part + (size_t)l * kRedBlocks);

@@ -72,7 +72,7 @@ struct WaveArgs {
 
 // tunables (defaults in spp_create; overridable through SPP_TUNE="key=val,..." for experiments)
 struct Tune {
-    int gs_warps = 4;          // warps (32-row strips) per GS tile
+    int gs_warps = 5;          // max warps (32-row strips) per GS tile (4 in y-form)
     int gs_tile_cols = 0;      // output columns per GS tile (0: one wave of CTAs per level)
     int gs_max_halo = 128;     // no certified halo below this -> exact chained sweep
     int sweep_warps = 2;       // warps per CTA of the exact chained sweep (M_II; 2 measured best)
@@ -158,6 +158,7 @@ struct Ctx {
     bool capturing = false;
     int use_graph = 1;
     int no_lines_tma = 0;                  // SPP_NO_LINES_TMA=1: LSU-loaded line kernel
+    int mg_zform = 1;                      // corner GS sweeps in z-form (SPP_MG_YFORM=1: y-form)
 };
 
 // kernels / launchers (defined in the .cu files)
@@ -166,7 +167,8 @@ cudaError_t setup_levels(Ctx *c, const double *c1, const double *c2, const doubl
 cudaError_t setup_lines(Ctx *c);
 void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double> &ky);
 // corner multigrid (k_mg.cu)
-void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, double *enew, const double *ec);
+void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, double *enew, const double *ec,
+               const double *q0 = nullptr);
 void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform, int cls, double bytes);
 void launch_ycoef(Ctx *c, int nl, long pc, const double *aE, const double *aN, const double *cd, double *ya, double *yn);
 cudaError_t wave_init();
@@ -176,6 +178,7 @@ void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e);
 void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew, const double *b, double *rho,
                          double *part, const MGState *ms = nullptr);
 cudaError_t setup_mg_tiles(Ctx *c);
+void launch_scale_cd(Ctx *c, int l, const double *b);
 bool launch_coarse_vcycle(Ctx *c, int lc, const double *R);
 
 // profiling helpers
