@@ -108,24 +108,26 @@ static double *part_slot(Ctx *c, int k) { return c->part + (size_t)k * kRedBlock
 // V(1,1) cycle for A_l e = R, zero initial guess ("standard V(1,1) cycling", one
 // downstream GS sweep before and after the coarse-grid correction; coarsest grid: "four sweeps",
 // P:1208-1209 / P:1281-1283).  Returns the buffer holding e (lev[l].e or lev[l].q).
-// Rq: R / D when the caller's producer wrote it (z-form sweeps; nullptr: formed here if needed).
-static double *vcycle(Ctx *c, int l, const double *R, const double *Rq)
+// rs: R holds R / D (the z-form V-cycle stores every level's right-hand side divided by D; the
+// caller's R may be plain, e.g. the test hooks).
+static double *vcycle(Ctx *c, int l, const double *R, bool rs)
 {
     Level &L = c->lev[l];
+    const bool zf = c->mg_zform;
     double *ea = L.e, *eb = L.q;
-    if (launch_coarse_vcycle(c, l, R)) return eb;   // levels l..L-1 fused (smem-resident)
+    if (launch_coarse_vcycle(c, l, R, zf && rs)) return eb;   // levels l..L-1 fused (smem-resident)
     if (l == c->L - 1) {
-        launch_gs(c, l, 0, R, nullptr, ea, nullptr, Rq);
-        launch_gs(c, l, 1, R, ea, eb, nullptr);
-        launch_gs(c, l, 1, R, eb, ea, nullptr);
-        launch_gs(c, l, 1, R, ea, eb, nullptr);
+        launch_gs(c, l, 0, R, nullptr, ea, nullptr, rs);
+        launch_gs(c, l, 1, R, ea, eb, nullptr, rs);
+        launch_gs(c, l, 1, R, eb, ea, nullptr, rs);
+        launch_gs(c, l, 1, R, ea, eb, nullptr, rs);
         return eb;
     }
     Level &C = c->lev[l + 1];
-    launch_gs(c, l, 0, R, nullptr, ea, nullptr, Rq);         // pre-smoothing from zero
-    launch_resid_restrict(c, l, R, ea);                       // C.b = S^-1 P^T S (R - A_l ea) (+ C.g = C.b / D)
-    const double *ec = vcycle(c, l + 1, C.b, c->mg_zform ? C.g : nullptr);
-    launch_gs(c, l, 1, R, ea, eb, ec);                        // post-smoothing from ea + P ec
+    launch_gs(c, l, 0, R, nullptr, ea, nullptr, rs);          // pre-smoothing from zero
+    launch_resid_restrict(c, l, R, ea, zf && rs, zf);         // C.b = S^-1 P^T S (R - A_l ea) (/ D_c in z-form)
+    const double *ec = vcycle(c, l + 1, C.b, zf);
+    launch_gs(c, l, 1, R, ea, eb, ec, rs);                    // post-smoothing from ea + P ec
     return eb;
 }
 
@@ -141,7 +143,7 @@ static int corner_solve(Ctx *c, const double *bc, double b0sq, int *cap_hit, cud
     *err = cudaSuccess;
     const double b0 = std::sqrt(b0sq);
     double res = b0;
-    const double *R = bc;
+    const double *R = L0.rho;                          // b_C (/ D in z-form), written with b_C
     const double *z = nullptr;
     double *zb[2] = {c->Zc, c->Zc2};
     int cycles = 0;
@@ -152,7 +154,7 @@ static int corner_solve(Ctx *c, const double *bc, double b0sq, int *cap_hit, cud
             if (res <= c->opt.mg_reduction * b0) break;
             if (cycles >= c->opt.mg_max_cycles) { *cap_hit = 1; break; }
         }
-        const double *e = vcycle(c, 0, R, c->mg_zform ? L0.g : nullptr);   // L0.g = R / D (corner rhs / cycle update)
+        const double *e = vcycle(c, 0, R, c->mg_zform);
         double *zn = zb[cycles & 1];
         launch_cycle_update(c, z, e, zn, bc, L0.rho, part_slot(c, 0));   // z += e; rho = b - A z
         z = zn;
@@ -266,7 +268,7 @@ static cudaError_t corner_graph_build(Ctx *c)
             e = cudaStreamBeginCaptureToGraph(c->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
             if (e == cudaSuccess) {
                 const int64_t b0 = c->launches;
-                const double *ev = vcycle(c, 0, L0.rho, c->mg_zform ? L0.g : nullptr);
+                const double *ev = vcycle(c, 0, L0.rho, c->mg_zform);
                 launch_cycle_update(c, nullptr, ev, nullptr, c->Bc, L0.rho, part_slot(c, 0), c->mgs);
                 k_mg_check<<<1, 1, 0, c->st>>>(part_slot(c, 0), c->mgs, red, maxc, fixed, h);
                 c->launches++;
@@ -329,7 +331,7 @@ static int apply_precond(Ctx *c, const double *v, double *z, int *cap_hit, cudaE
         ProfScope ps(c, 9, 40.0 * (double)n * n);
         k_corner_rhs<<<kRedBlocks, kRedThreads, 0, c->st>>>(N, c->P, L0.pitch, v, z, c->aE, c->aN, c->rr, c->aW,
                                                             c->aS, L0.hb, L0.kb, c->weighted, c->Bc, part_slot(c, 1),
-                                                            gm ? L0.rho : nullptr, c->cd, c->mg_zform ? L0.g : nullptr);
+                                                            L0.rho, c->cd, c->mg_zform);
         c->launches++;
     }
     if (gm) {                                           // cycles known after the caller's next sync
@@ -956,7 +958,7 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
         pk(in + mm, B);
         Level &L0 = c->lev[0];
         k_corner_rhs<<<kRedBlocks, kRedThreads, 0, c->st>>>(c->N, c->P, L0.pitch, A, B, c->aE, c->aN, c->rr, c->aW,
-                                                            c->aS, L0.hb, L0.kb, 0, c->Bc, part_slot(c, 0), nullptr, c->cd, nullptr);
+                                                            c->aS, L0.hb, L0.kb, 0, c->Bc, part_slot(c, 0), nullptr, c->cd, 0);
         k_unpack_level<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, c->Bc, out);
     } else if (s == SPP_STAGE_CORNER_SOLVE) {
         Level &L0 = c->lev[0];
@@ -968,7 +970,9 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
                                                           L0.rr, L0.aW, L0.aS, L0.hb, L0.kb, L0.rho, part_slot(c, 1));
         double b0sq = 0;
         CK(c, fetch_sum(c, part_slot(c, 1), &b0sq));
-        if (c->mg_zform) launch_scale_cd(c, 0, c->Bc);   // L0.g = b_C / D for the first cycle
+        // the first cycle's V-cycle input: b_C (/ D in z-form)
+        if (c->mg_zform) launch_scale_cd(c, 0, c->Bc, L0.rho);
+        else CK(c, cudaMemcpyAsync(L0.rho, c->Bc, sizeof(double) * L0.elems, cudaMemcpyDeviceToDevice, c->st));
         int cap = 0; cudaError_t err = cudaSuccess;
         const double *zc = nullptr;
         int k = corner_solve(c, c->Bc, b0sq, &cap, &err, &zc);
@@ -994,7 +998,7 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
             double *tmp = c->T1;   // level-l rhs must not alias the level buffers used by vcycle
             CK(c, cudaMemsetAsync(tmp, 0, sizeof(double) * Lv.elems, c->st));
             k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in, tmp);
-            const double *res = vcycle(c, l, tmp, nullptr);
+            const double *res = vcycle(c, l, tmp, false);
             k_unpack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, res, out);
         } else if (s == SPP_STAGE_RESTRICT) {
             // the fused residual-restriction kernel with e = 0 restricts R = in

@@ -325,7 +325,7 @@ __global__ void k_update_x(long n2, int k, const double *const *Z, const double 
 __global__ void __launch_bounds__(kRedThreads) k_corner_rhs(int N, long P, long P0, const double *v,
     const double *z, const double *aE, const double *aN, const double *rr, const double *aW,
     const double *aS, const double *hb, const double *kb, int weighted, double *bc, double *part, double *bc2,
-    const double *cd, double *q0)
+    const double *cd, int scale2)
 {
     __shared__ double sm[32];
     const int n = N / 2;
@@ -340,8 +340,7 @@ __global__ void __launch_bounds__(kRedThreads) k_corner_rhs(int N, long P, long 
         if (j == n) b += aN[g] * z[g + P];
         if (i == n) b += aE[g] * z[g + 1];
         bc[(long)j * P0 + i] = b;
-        if (bc2) bc2[(long)j * P0 + i] = b;           // corner graph: the first cycle's residual
-        if (q0) q0[(long)j * P0 + i] = b * cd[g];      // z-form: the first cycle's pre-smoothing rhs
+        if (bc2) bc2[(long)j * P0 + i] = scale2 ? b * cd[g] : b;   // the first cycle's V-cycle input (b/D in z-form)
         const double t = (hb[i] * kb[j]) * b;
         acc += t * t;
     }

@@ -573,7 +573,7 @@ __device__ __forceinline__ double interp_c(const double *ec, long Pc, int i, int
 __global__ void __launch_bounds__(256) k_gs_prep(int nl, long pv, const double *__restrict__ e,
     const double *__restrict__ ec, long pcv, const double *__restrict__ b,
     const double *__restrict__ aW, const double *__restrict__ aS, double *g,
-    const double *__restrict__ cd, long pc)
+    const double *__restrict__ cd, long pc, int bscaled)
 {
     const long tot = (long)nl * nl;
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
@@ -584,8 +584,9 @@ __global__ void __launch_bounds__(256) k_gs_prep(int nl, long pv, const double *
             ew += (i > 1) ? interp_c(ec, pcv, i - 1, j) : 0.0;
             es += (j > 1) ? interp_c(ec, pcv, i, j - 1) : 0.0;
         }
-        const double gv = (b[v] + aW[i] * ew) + aS[j] * es;
-        g[v] = cd ? gv * cd[(long)j * pc + i] : gv;   // z-form sweeps take g / D
+        if (!cd) { g[v] = (b[v] + aW[i] * ew) + aS[j] * es; continue; }
+        const double dinv = cd[(long)j * pc + i];      // z-form sweeps take g / D
+        g[v] = bscaled ? b[v] + (aW[i] * ew + aS[j] * es) * dinv : ((b[v] + aW[i] * ew) + aS[j] * es) * dinv;
     }
 }
 
@@ -602,19 +603,20 @@ __global__ void k_scale_cd(int nl, long pv, long pc, const double *__restrict__ 
 static inline int gblocks(long work) { long b = (work + 255) / 256; return (int)std::max(1L, std::min(b, 148L * 16)); }
 
 // level l's g = b / D (z-form pre-smoothing rhs when no producer wrote it)
-void launch_scale_cd(Ctx *c, int l, const double *b)
+void launch_scale_cd(Ctx *c, int l, const double *b, double *q)
 {
     Level &L = c->lev[l];
-    k_scale_cd<<<gblocks((long)L.n * L.n), 256, 0, c->st>>>(L.n, L.pitch, L.cpitch, b, L.cd, L.g);
+    k_scale_cd<<<gblocks((long)L.n * L.n), 256, 0, c->st>>>(L.n, L.pitch, L.cpitch, b, L.cd, q);
     c->launches++;
 }
 
 // One downstream GS sweep on level l: mode 0 from zero (q = b); mode 1 from e_old (+ P ec when
-// ec != null): q = prep(e_old [+ P ec]).  z-form (c->mg_zform): z = q/D + (aE/D) z_E + (aN/D) z_N,
-// so q arrives divided by D -- q0 (b/D written by the kernel that produced b) for mode 0, the
-// prep kernel's output for mode 1; y-form: y = q + ya y_E + yn y_N, z = y/D at write-back.
+// ec != null): q = prep(e_old [+ P ec]).  z-form (c->mg_zform): z = q + (aE/D) z_E + (aN/D) z_N
+// with q = rhs/D; inside the V-cycle the level right-hand sides are stored divided by D
+// (bscaled), so mode 0 streams b itself; a caller's plain rhs is scaled here.  y-form:
+// y = q + ya y_E + yn y_N, z = y/D at write-back.
 void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, double *enew, const double *ec,
-               const double *q0)
+               bool bscaled)
 {
     Level &L = c->lev[l];
     const double nn = (double)L.n * L.n;
@@ -625,18 +627,13 @@ void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, dou
     else { a.ca = L.ya; a.cn = L.yn; }
     a.cd = L.cd; a.z = enew;
     if (mode == 0) {
-        if (!zf) a.q = b;
-        else if (q0) a.q = q0;
-        else {
-            k_scale_cd<<<gblocks((long)L.n * L.n), 256, 0, c->st>>>(L.n, L.pitch, L.cpitch, b, L.cd, L.g);
-            c->launches++;
-            a.q = L.g;
-        }
+        if (!zf || bscaled) a.q = b;
+        else { launch_scale_cd(c, l, b, L.g); a.q = L.g; }
     } else {
         {
             ProfScope ps(c, 5, nn * (zf ? 32.0 : 24.0));
             k_gs_prep<<<gblocks((long)L.n * L.n), 256, 0, c->st>>>(L.n, L.pitch, eold, ec,
-                ec ? c->lev[l + 1].pitch : 0, b, L.aW, L.aS, L.g, zf ? L.cd : nullptr, L.cpitch);
+                ec ? c->lev[l + 1].pitch : 0, b, L.aW, L.aS, L.g, zf ? L.cd : nullptr, L.cpitch, bscaled ? 1 : 0);
             c->launches++;
             dbg_sync(c, "k_gs_prep");
         }
@@ -668,6 +665,7 @@ struct CoarseArgs {
     int nlev;                       // levels lc .. lc+nlev-1 (the last is the coarsest)
     CoarseLev lv[8];
     const double *R; long rpitch;   // rhs of level lc (value layout)
+    int rs;                         // R stored as R / D (z-form V-cycle)
     double *out; long opitch;       // result e of level lc (value layout)
 };
 
@@ -728,9 +726,15 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
     __syncthreads();
     {   // level lc rhs
         const int n = a.lv[0].n;
+        const CoarseLev &F = a.lv[0];
         for (int k = threadIdx.x; k < n * n; k += blockDim.x) {
             const int j = k / n + 1, i = k % n + 1;
-            B[0][j * st[0] + i] = a.R[(long)j * a.rpitch + i];
+            double rv = a.R[(long)j * a.rpitch + i];
+            if (a.rs) {                                 // R / D -> R
+                const int q = j * F.cpitch + i;
+                rv *= ((__ldg(F.aW + i) + __ldg(F.aE + q)) + (__ldg(F.aS + j) + __ldg(F.aN + q))) + __ldg(F.rr + q);
+            }
+            B[0][j * st[0] + i] = rv;
         }
         __syncthreads();
     }
@@ -807,7 +811,7 @@ static size_t coarse_smem(const Ctx *c, int lc)
 
 // V-cycle of levels lc..L-1 in one launch; result in lev[lc].q.  Returns false when the levels
 // do not fit (the caller then recurses level by level).
-bool launch_coarse_vcycle(Ctx *c, int lc, const double *R)
+bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs)
 {
     if (c->L - lc > 8 || c->lev[lc].n > c->tune.coarse_max) return false;
     const size_t sm = coarse_smem(c, lc);
@@ -824,7 +828,7 @@ bool launch_coarse_vcycle(Ctx *c, int lc, const double *R)
         const Level &L = c->lev[l];
         a.lv[l - lc] = CoarseLev{L.n, (int)L.cpitch, L.aE, L.aN, L.rr, L.cd, L.aW, L.aS, L.hb, L.kb};
     }
-    a.R = R; a.rpitch = c->lev[lc].pitch;
+    a.R = R; a.rpitch = c->lev[lc].pitch; a.rs = rs ? 1 : 0;
     a.out = c->lev[lc].q; a.opitch = c->lev[lc].pitch;
     double nn = 0;
     for (int l = lc; l < c->L; ++l) nn += (double)c->lev[l].n * c->lev[l].n;
@@ -849,7 +853,7 @@ __global__ void __launch_bounds__(256) k_resid_restrict(int nf, long pv, long pc
     const double *__restrict__ rr, const double *__restrict__ aW, const double *__restrict__ aS,
     const double *__restrict__ hbf, const double *__restrict__ kbf, int nc, long pvc,
     const double *__restrict__ hbc, const double *__restrict__ kbc, double *bc,
-    const double *__restrict__ cdc, long pcc, double *qc)
+    const double *__restrict__ cdc, long pcc, int rs_in, int scale_out)
 {
     constexpr int RFW = 2 * RT + 1;
     __shared__ double s[RFW * RFW];
@@ -863,9 +867,11 @@ __global__ void __launch_bounds__(256) k_resid_restrict(int nf, long pv, long pc
         if (i <= nf && j <= nf) {
             const long g = (long)j * pv + i, q = (long)j * pc + i;
             const double ec = e[g];
-            const double Ae = aW[i] * (ec - e[g - 1]) + aE[q] * (ec - e[g + 1]) + aS[j] * (ec - e[g - pv]) +
-                              aN[q] * (ec - e[g + pv]) + rr[q] * ec;
-            v = (hbf[i] * kbf[j]) * (R[g] - Ae);
+            const double vW = aW[i], vE = aE[q], vS = aS[j], vN = aN[q], vr = rr[q];
+            const double Ae = vW * (ec - e[g - 1]) + vE * (ec - e[g + 1]) + vS * (ec - e[g - pv]) +
+                              vN * (ec - e[g + pv]) + vr * ec;
+            const double Rv = rs_in ? R[g] * (((vW + vE) + (vS + vN)) + vr) : R[g];   // R stored as R/D (z-form)
+            v = (hbf[i] * kbf[j]) * (Rv - Ae);
         }
         s[p] = v;
     }
@@ -882,12 +888,11 @@ __global__ void __launch_bounds__(256) k_resid_restrict(int nf, long pv, long pc
             acc += (bb == 0 ? 1.0 : 0.5) * rs;
         }
         const double bv = acc / (hbc[I] * kbc[J]);
-        bc[(long)J * pvc + I] = bv;
-        if (qc) qc[(long)J * pvc + I] = bv * cdc[(long)J * pcc + I];   // z-form pre-smoothing rhs
+        bc[(long)J * pvc + I] = scale_out ? bv * cdc[(long)J * pcc + I] : bv;   // z-form: stored as b_c / D_c
     }
 }
 
-void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e)
+void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e, bool rs_in, bool scale_out)
 {
     Level &F = c->lev[l], &C = c->lev[l + 1];
     ProfScope ps(c, 4, (double)F.n * F.n * 40.0 + 8.0 * C.n * (double)C.n);
@@ -897,7 +902,7 @@ void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e)
     const dim3 grid((C.n + RTn - 1) / RTn, (C.n + RTn - 1) / RTn);
 #define SPP_RR(T) k_resid_restrict<T><<<grid, T >= 32 ? 256 : (T >= 16 ? 256 : 128), 0, c->st>>>(F.n, F.pitch, \
         F.cpitch, e, R, F.aE, F.aN, F.rr, F.aW, F.aS, F.hb, F.kb, C.n, C.pitch, C.hb, C.kb, C.b, C.cd, C.cpitch, \
-        c->mg_zform ? C.g : nullptr)
+        rs_in ? 1 : 0, scale_out ? 1 : 0)
     if (RTn == 32) SPP_RR(32);
     else if (RTn == 16) SPP_RR(16);
     else SPP_RR(8);
@@ -915,7 +920,7 @@ __global__ void __launch_bounds__(kRedThreads) k_cycle_update(int nl, long pv, l
     const double *__restrict__ e, double *znew, const double *__restrict__ b, const double *__restrict__ aE,
     const double *__restrict__ aN, const double *__restrict__ rr, const double *__restrict__ aW,
     const double *__restrict__ aS, const double *__restrict__ hb, const double *__restrict__ kb, double *rho,
-    double *part, const MGState *ms, const double *__restrict__ cd, double *q0)
+    double *part, const MGState *ms, const double *__restrict__ cd, int scale_rho)
 {
     __shared__ double sm[32];
     if (ms) { z = ms->zcur; znew = ms->znext; }        // corner graph: buffers from the device state
@@ -929,8 +934,7 @@ __global__ void __launch_bounds__(kRedThreads) k_cycle_update(int nl, long pv, l
         const double Az = aW[i] * (zc - zw) + aE[q] * (zc - ze) + aS[j] * (zc - zs) + aN[q] * (zc - zn) + rr[q] * zc;
         const double r = b[g] - Az;
         znew[g] = zc;
-        rho[g] = r;
-        if (q0) q0[g] = r * cd[q];                      // z-form: the next cycle's pre-smoothing rhs
+        rho[g] = scale_rho ? r * cd[q] : r;             // the next V-cycle's input (rho/D in z-form)
         const double t = (hb[i] * kb[j]) * r;
         acc += t * t;
     }
@@ -952,10 +956,10 @@ void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew,
 {
     Level &L = c->lev[0];
     const double nn = (double)L.n * L.n;
-    ProfScope ps(c, 6, nn * ((z ? 64.0 : 56.0) + (c->mg_zform ? 16.0 : 0.0)));
+    ProfScope ps(c, 6, nn * ((z ? 64.0 : 56.0) + (c->mg_zform ? 8.0 : 0.0)));
     k_cycle_update<<<kRedBlocks, kRedThreads, 0, c->st>>>(L.n, L.pitch, L.cpitch, z, e, znew, b, L.aE, L.aN, L.rr,
                                                           L.aW, L.aS, L.hb, L.kb, rho, part, ms, L.cd,
-                                                          c->mg_zform ? L.g : nullptr);
+                                                          c->mg_zform ? 1 : 0);
     c->launches++;
 }
 

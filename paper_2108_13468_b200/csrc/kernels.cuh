@@ -34,7 +34,7 @@ __global__ void k_update_x(long n2, int k, const double *const *Z, const double 
 __global__ void k_corner_rhs(int N, long P, long P0, const double *v, const double *z,
                              const double *aE, const double *aN, const double *rr, const double *aW,
                              const double *aS, const double *hb, const double *kb, int weighted,
-                             double *bc, double *part, double *bc2, const double *cd, double *q0);
+                             double *bc, double *part, double *bc2, const double *cd, int scale2);
 __global__ void k_mg_resid(int nl, long Pv, long Pc, double *z, const double *e, const double *b,
                            const double *aE, const double *aN, const double *rr, const double *aW,
                            const double *aS, const double *hb, const double *kb, double *rho,

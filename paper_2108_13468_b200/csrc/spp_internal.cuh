@@ -168,18 +168,18 @@ cudaError_t setup_lines(Ctx *c);
 void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double> &ky);
 // corner multigrid (k_mg.cu)
 void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, double *enew, const double *ec,
-               const double *q0 = nullptr);
+               bool bscaled = false);
 void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform, int cls, double bytes);
 void launch_ycoef(Ctx *c, int nl, long pc, const double *aE, const double *aN, const double *cd, double *ya, double *yn);
 cudaError_t wave_init();
 const CUtensorMap *tmap2d(Ctx *c, const void *base, unsigned long long d0, unsigned long long d1,
                           unsigned long long stride_bytes, unsigned b0, unsigned b1, bool swz128);
-void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e);
+void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e, bool rs_in = false, bool scale_out = false);
 void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew, const double *b, double *rho,
                          double *part, const MGState *ms = nullptr);
 cudaError_t setup_mg_tiles(Ctx *c);
-void launch_scale_cd(Ctx *c, int l, const double *b);
-bool launch_coarse_vcycle(Ctx *c, int lc, const double *R);
+void launch_scale_cd(Ctx *c, int l, const double *b, double *q);
+bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs = false);
 
 // profiling helpers
 struct ProfScope {
