@@ -426,6 +426,7 @@ static void parse_tune(Ctx *c)
             else if (k == "gs_max_halo") c->tune.gs_max_halo = v;
             else if (k == "sweep_warps") c->tune.sweep_warps = v;
             else if (k == "coarse_max") c->tune.coarse_max = v;
+            else if (k == "gs_lag") c->tune.gs_lag = v;
         }
         pos = end + 1;
     }

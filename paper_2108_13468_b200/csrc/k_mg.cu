@@ -1037,7 +1037,8 @@ cudaError_t setup_mg_tiles(Ctx *c)
         // warp sweeps (tile columns + halo + 62) / 16 chunks.  Pick the warps per tile (3 or 4;
         // the halo rows are part of the tile) and the column tiling with the smallest such time
         // among the plans that run as one wave of one CTA per SM.
-        auto cost = [](int W, int cols) { return (cols + WLAG * 31 + WCW - 1) / WCW + 5 * (W - 1); };
+        const int lag = T.gs_lag;
+        auto cost = [lag](int W, int cols) { return (cols + WLAG * 31 + WCW - 1) / WCW + lag * (W - 1); };
         if (halo < 0 || halo + 16 > 32 * Wt) {
             if (n <= 32 * Wt) {                                // one CTA, exact
                 L.tile_warps = (n + 31) / 32;

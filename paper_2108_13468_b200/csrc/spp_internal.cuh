@@ -76,6 +76,7 @@ struct Tune {
     int gs_tile_cols = 0;      // output columns per GS tile (0: one wave of CTAs per level)
     int gs_max_halo = 128;     // no certified halo below this -> exact chained sweep
     int sweep_warps = 2;       // warps per CTA of the exact chained sweep (M_II; 2 measured best)
+    int gs_lag = 5;            // tiling model: chunk-times each extra warp adds
     int coarse_max = 16;       // levels with n <= this run as one fused single-CTA V-cycle (16 measured best)
 };
 
