@@ -643,7 +643,7 @@ spp_status spp_create(const spp_problem *p, const spp_options *o, void *stream, 
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev);
-    if (wave_init() != cudaSuccess) { delete c; FAIL((Ctx *)nullptr, SPP_E_CUDA, "kernel attribute setup failed"); }
+    if (wave_init() != cudaSuccess || lines_init() != cudaSuccess) { delete c; FAIL((Ctx *)nullptr, SPP_E_CUDA, "kernel attribute setup failed"); }
     spp_status s;
     double tx = 0, ty = 0;
     if ((s = check_mesh(p->x, N, &tx, c)) != SPP_OK) { g_err = c->err; delete c; return s; }

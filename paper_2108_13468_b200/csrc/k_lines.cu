@@ -582,6 +582,14 @@ cudaError_t setup_lines(Ctx *c)
     return cudaStreamSynchronize(c->st);
 }
 
+// per-device kernel attributes (spp_create, on the context's device)
+cudaError_t lines_init()
+{
+    SPP_CUDA_TRY(cudaFuncSetAttribute(k_lines_tma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 2048));
+    SPP_CUDA_TRY(cudaFuncSetAttribute(k_lines_tma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 2048));
+    return cudaSuccess;
+}
+
 static size_t lines_tma_smem(int len, int nst)
 {
     return ((size_t)nst * 6 * len + len + len / 32 + 32) * sizeof(double) + 1024;   // stages + z staging
@@ -612,13 +620,6 @@ static bool launch_lines_tma(Ctx *c, const double *v, double *z)
     const int nst = lines_tma_smem(len, 2) <= 227 * 1024 - 2048 ? 2 : 1;
     if (lines_tma_smem(len, nst) > 227 * 1024 - 2048) return false;
     const size_t sm = lines_tma_smem(len, nst);
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_lines_tma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 2048) != cudaSuccess ||
-            cudaFuncSetAttribute(k_lines_tma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 2048) != cudaSuccess)
-            return false;
-        attr = true;
-    }
     LineMaps m;
     const int nl = c->n - 1;
     const unsigned long long rows = (unsigned long long)nl * len / 16;

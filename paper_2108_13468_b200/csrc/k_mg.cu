@@ -441,6 +441,8 @@ static void dbg_sync(Ctx *c, const char *what)
 // ---------------------------------------------------------------------------------- tensor maps
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
+struct CoarseArgs;
+__global__ void k_coarse_vcycle(CoarseArgs a);
 cudaError_t wave_init()
 {
     if (!g_encode) {
@@ -453,6 +455,7 @@ cudaError_t wave_init()
     SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smz));
     SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smy));
     SPP_CUDA_TRY(cudaFuncSetAttribute(k_wave<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smz));
+    SPP_CUDA_TRY(cudaFuncSetAttribute(k_coarse_vcycle, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     return cudaSuccess;
 }
 
@@ -816,12 +819,6 @@ bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs)
     if (c->L - lc > 8 || c->lev[lc].n > c->tune.coarse_max) return false;
     const size_t sm = coarse_smem(c, lc);
     if (sm > 200 * 1024) return false;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_coarse_vcycle, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess)
-            return false;
-        attr = true;
-    }
     CoarseArgs a{};
     a.nlev = c->L - lc;
     for (int l = lc; l < c->L; ++l) {

@@ -173,6 +173,7 @@ void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, dou
 void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform, int cls, double bytes);
 void launch_ycoef(Ctx *c, int nl, long pc, const double *aE, const double *aN, const double *cd, double *ya, double *yn);
 cudaError_t wave_init();
+cudaError_t lines_init();
 const CUtensorMap *tmap2d(Ctx *c, const void *base, unsigned long long d0, unsigned long long d1,
                           unsigned long long stride_bytes, unsigned b0, unsigned b1, bool swz128);
 void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e, bool rs_in = false, bool scale_out = false);
