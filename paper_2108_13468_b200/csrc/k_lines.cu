@@ -511,13 +511,17 @@ void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double
         const std::vector<double> &k = chain == 0 ? kx : ky;
         std::vector<double> lg(nl + 1, 0.0);                 // prefix sums of log kappa
         for (int l = 0; l < nl; ++l) lg[l + 1] = lg[l] + std::log(std::max(k[l], 1e-300));
-        auto warm = [&](int first) {                          // warm-up start for a chunk
-            int st = first;
-            while (st > 0 && lg[first] - lg[st] > target) --st;
-            return st;
-        };
+        // warm-up start of a chunk beginning at line f: the largest st <= f with
+        // lg[f] - lg[st] <= target (prod kappa small enough), or 0.  lg decreases, so st(f) is
+        // nondecreasing in f: one two-pointer pass (the plan runs inside every setup).
+        std::vector<int> wst(nl + 1, 0);
+        for (int f = 0, st = 0; f <= nl; ++f) {
+            while (st < f && lg[f] - lg[st + 1] <= target) ++st;  // advance while st+1 still suffices
+            wst[f] = (lg[f] - lg[st] <= target) ? st : 0;
+        }
+        auto warm = [&](int first) { return wst[first]; };
         int bestG = nl; long bestCost = nl;
-        for (int G = 1; G <= nl; G = (G < 8 ? G + 1 : G + G / 4)) {
+        for (int G = (nl + budget - 1) / budget; G <= nl; ++G) {     // smallest chunks that fit the budget first
             const int P = (nl + G - 1) / G;
             if (P > budget) continue;
             long worst = 0;
