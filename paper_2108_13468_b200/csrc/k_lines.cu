@@ -216,8 +216,7 @@ __global__ void __launch_bounds__(256) k_line_factor_scan(int N, long P, const d
     __syncthreads();
     if (wid == 0) {                                     // exclusive prefix over warps
         M2 x = lane < nw ? wtot[lane] : M2{1.0, 0.0, 0.0, 1.0};
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
+        for (int d = 1; d < nw; d <<= 1) {
             const M2 up = m2shfl_up(x, d);
             if (lane >= d) x = m2mul(x, up);
         }

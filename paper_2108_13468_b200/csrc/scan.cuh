@@ -26,8 +26,7 @@ __device__ __forceinline__ void fwd_scan(double (&al)[K], double (&b)[K], double
     __syncthreads();
     if (w == 0) {
         double WA = lane < nw ? sA[lane] : 1.0, WB = lane < nw ? sB[lane] : 0.0;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
+        for (int d = 1; d < nw; d <<= 1) {             // nw warps: log2(nw) levels
             const double Au = __shfl_up_sync(0xffffffffu, WA, d), Bu = __shfl_up_sync(0xffffffffu, WB, d);
             if (lane >= d) { WB = WA * Bu + WB; WA = WA * Au; }
         }
@@ -63,8 +62,7 @@ __device__ __forceinline__ void bwd_scan(double (&be)[K], double (&y)[K], double
     if (w == 0) {
         const int r = nw - 1 - lane;       // reversed warp order
         double WA = lane < nw ? sA[r] : 1.0, WB = lane < nw ? sB[r] : 0.0;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
+        for (int d = 1; d < nw; d <<= 1) {             // nw warps: log2(nw) levels
             const double Au = __shfl_up_sync(0xffffffffu, WA, d), Bu = __shfl_up_sync(0xffffffffu, WB, d);
             if (lane >= d) { WB = WA * Bu + WB; WA = WA * Au; }
         }
