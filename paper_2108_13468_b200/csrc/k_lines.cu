@@ -470,8 +470,8 @@ __global__ void __launch_bounds__(256) k_lines_tma(LineChain cx, LineChain cy, c
             b[k] = in ? bb : 0.0;
             if (!in) { al[k] = 0.0; be[k] = 0.0; }
         }
-        fwd_scan<K>(al, b, y, sA, sB);
-        bwd_scan<K>(be, y, zz, sA, sB);
+        fwd_scan<K, false>(al, b, y, sA, sB);   // the backward scan follows; the z staging barrier ends the line
+        bwd_scan<K, false>(be, y, zz, sA, sB);
         LP(te);
         // the line's results leave as coalesced segments through shared memory: X lines are row
         // segments of z, Y lines (columns of z) go line-major to the scratch (k_ysc_transpose)

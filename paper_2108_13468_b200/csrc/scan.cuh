@@ -8,7 +8,9 @@
 
 namespace spp {
 
-template <int K>
+// TAIL = false drops the trailing barrier when the caller's next shared-memory use is another scan
+// or is itself behind a barrier (the scratch slots are disjoint between phases; see k_lines_tma).
+template <int K, bool TAIL = true>
 __device__ __forceinline__ void fwd_scan(double (&al)[K], double (&b)[K], double (&y)[K],
                                          double *sA, double *sB)
 {
@@ -41,10 +43,10 @@ __device__ __forceinline__ void fwd_scan(double (&al)[K], double (&b)[K], double
     double yin = (lane == 0) ? yw : Ae * yw + Be;
 #pragma unroll
     for (int k = 0; k < K; ++k) { yin = al[k] * yin + b[k]; y[k] = yin; }
-    __syncthreads();
+    if (TAIL) __syncthreads();
 }
 
-template <int K>
+template <int K, bool TAIL = true>
 __device__ __forceinline__ void bwd_scan(double (&be)[K], double (&y)[K], double (&z)[K],
                                          double *sA, double *sB)
 {
@@ -75,7 +77,7 @@ __device__ __forceinline__ void bwd_scan(double (&be)[K], double (&y)[K], double
     double zin = (lane == 31) ? zw : Ae * zw + Be;
 #pragma unroll
     for (int k = K - 1; k >= 0; --k) { zin = be[k] * zin + y[k]; z[k] = zin; }
-    __syncthreads();
+    if (TAIL) __syncthreads();
 }
 
 }  // namespace spp
