@@ -329,7 +329,7 @@ static int apply_precond(Ctx *c, const double *v, double *z, int *cap_hit, cudaE
     const bool gm = graph_mode(c);
     {
         ProfScope ps(c, 9, 40.0 * (double)n * n);
-        k_corner_rhs<<<kRedBlocks, kRedThreads, 0, c->st>>>(N, c->P, L0.pitch, v, z, c->aE, c->aN, c->rr, c->aW,
+        k_corner_rhs<<<red_grid((long)n * n), kRedThreads, 0, c->st>>>(N, c->P, L0.pitch, v, z, c->aE, c->aN, c->rr, c->aW,
                                                             c->aS, L0.hb, L0.kb, c->weighted, c->Bc, part_slot(c, 1),
                                                             L0.rho, c->cd, c->mg_zform);
         c->launches++;
@@ -741,7 +741,7 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
     // v0 = W f / beta
     {
         ProfScope ps(c, 7, 48.0 * mm);
-        k_rhs<<<kRedBlocks, kRedThreads, 0, c->st>>>(m, c->P, c->F, c->aE, c->aN, c->rr, c->aW, c->aS, weighted,
+        k_rhs<<<red_grid((long)m * m), kRedThreads, 0, c->st>>>(m, c->P, c->F, c->aE, c->aN, c->rr, c->aW, c->aS, weighted,
                                                      c->V[0], part_slot(c, 0));
         c->launches++;
     }
@@ -773,22 +773,22 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
             // w = W A z_k, with <w, v_0>
             {
                 ProfScope ps(c, 0, 48.0 * mm);
-                k_spmv<<<kRedBlocks, kRedThreads, 0, c->st>>>(m, c->P, c->Z[k], c->aE, c->aN, c->rr, c->aW, c->aS,
+                k_spmv<<<red_grid((long)m * m), kRedThreads, 0, c->st>>>(m, c->P, c->Z[k], c->aE, c->aN, c->rr, c->aW, c->aS,
                                                               weighted, c->w, c->V[0], part_slot(c, 0));
                 c->launches++;
             }
             // modified Gram-Schmidt: h_{j,k} for j = 0..k, then ||w||
             for (int j = 1; j <= k; ++j) {
                 ProfScope ps(c, 7, 32.0 * G);
-                k_mgs<<<kRedBlocks, kRedThreads, 0, c->st>>>(G, c->w, c->V[j - 1], part_slot(c, j - 1),
+                k_mgs<<<red_grid(G), kRedThreads, 0, c->st>>>(G, c->w, c->V[j - 1], part_slot(c, j - 1),
                                                              c->dscal + (j - 1), c->V[j], part_slot(c, j));
                 c->launches++;
             }
             {
                 ProfScope ps(c, 7, 24.0 * G + 16.0 * G);
-                k_mgs<<<kRedBlocks, kRedThreads, 0, c->st>>>(G, c->w, c->V[k], part_slot(c, k), c->dscal + k,
+                k_mgs<<<red_grid(G), kRedThreads, 0, c->st>>>(G, c->w, c->V[k], part_slot(c, k), c->dscal + k,
                                                              c->w, part_slot(c, k + 1));
-                k_normalize<<<kRedBlocks, kRedThreads, 0, c->st>>>(G, c->w, part_slot(c, k + 1), c->dscal + k + 1,
+                k_normalize<<<red_grid(G), kRedThreads, 0, c->st>>>(G, c->w, part_slot(c, k + 1), c->dscal + k + 1,
                                                                    c->V[k + 1]);
                 c->launches += 2;
             }

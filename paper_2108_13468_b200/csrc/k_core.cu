@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(kRedThreads) k_spmv(int m, long P, const doubl
     if (part) {
         const double s = block_sum(acc, sm);
         if (threadIdx.x == 0) part[blockIdx.x] = s;
+        zero_tail(part);
     }
 }
 
@@ -227,6 +228,7 @@ __global__ void __launch_bounds__(kRedThreads) k_resid_stats(int m, long P, cons
     t = block_sum(s1, sm); if (threadIdx.x == 0) part4[kRedBlocks + blockIdx.x] = t;
     t = block_sum(s2, sm); if (threadIdx.x == 0) part4[2 * kRedBlocks + blockIdx.x] = t;
     t = block_sum(s3, sm); if (threadIdx.x == 0) part4[3 * kRedBlocks + blockIdx.x] = t;
+    for (int a4 = 0; a4 < 4; ++a4) zero_tail(part4 + (size_t)a4 * kRedBlocks);
 }
 
 // ===================================================================================== Krylov vectors
@@ -248,6 +250,7 @@ __global__ void __launch_bounds__(kRedThreads) k_rhs(int m, long P, const double
     }
     const double s = block_sum(acc, sm);
     if (threadIdx.x == 0) part[blockIdx.x] = s;
+    zero_tail(part);
 }
 
 // x *= alpha (alpha from host)
@@ -285,6 +288,7 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs(long n2, double *w, const d
     }
     const double s = block_sum(acc, sm);
     if (threadIdx.x == 0) part_out[blockIdx.x] = s;
+    zero_tail(part_out);
 }
 
 // h = sqrt(sum(part_in)) -> hslot;  v = w / h (0 if h == 0)
@@ -346,6 +350,7 @@ __global__ void __launch_bounds__(kRedThreads) k_corner_rhs(int N, long P, long 
     }
     const double s = block_sum(acc, sm);
     if (threadIdx.x == 0) part[blockIdx.x] = s;
+    zero_tail(part);
 }
 
 // z += e; rho = b - A z (level grid, difference form); partial ||S rho||^2.  If e == nullptr
@@ -378,6 +383,7 @@ __global__ void __launch_bounds__(kRedThreads) k_mg_resid(int nl, long Pv, long 
     if (part) {
         const double s = block_sum(acc, sm);
         if (threadIdx.x == 0) part[blockIdx.x] = s;
+        zero_tail(part);
     }
 }
 

@@ -946,6 +946,7 @@ __global__ void __launch_bounds__(kRedThreads) k_cycle_update(int nl, long pv, l
         for (int k = 0; k < nwp; ++k) s += sm[k];
         part[blockIdx.x] = s;
     }
+    zero_tail(part);
 }
 
 void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew, const double *b, double *rho,
@@ -954,7 +955,7 @@ void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew,
     Level &L = c->lev[0];
     const double nn = (double)L.n * L.n;
     ProfScope ps(c, 6, nn * ((z ? 64.0 : 56.0) + (c->mg_zform ? 8.0 : 0.0)));
-    k_cycle_update<<<kRedBlocks, kRedThreads, 0, c->st>>>(L.n, L.pitch, L.cpitch, z, e, znew, b, L.aE, L.aN, L.rr,
+    k_cycle_update<<<red_grid((long)L.n * L.n), kRedThreads, 0, c->st>>>(L.n, L.pitch, L.cpitch, z, e, znew, b, L.aE, L.aN, L.rr,
                                                           L.aW, L.aS, L.hb, L.kb, rho, part, ms, L.cd,
                                                           c->mg_zform ? 1 : 0);
     c->launches++;
@@ -986,6 +987,7 @@ __global__ void k_level_rho(int nl, long pc, const double *aE, const double *aN,
         for (int k = 0; k < nwp; ++k) s = fmax(s, sm[k]);
         part[blockIdx.x] = s;
     }
+    zero_tail(part);
 }
 
 // ya = aE / D_E = aE(i,j) cd(i+1,j), yn = aN / D_N = aN(i,j) cd(i,j+1) on [1, nl]^2 (the ghost

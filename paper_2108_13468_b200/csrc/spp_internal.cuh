@@ -23,6 +23,19 @@ namespace spp {
 constexpr int kMaxLevels = 24;
 constexpr int kWarp = 32;
 constexpr int kRedBlocks = 592;      // 4 x 148 SMs: fixed grid for deterministic reductions
+// reduction grid for `work` elements: kRedBlocks for large grids; fewer for small ones (the
+// producers zero the unused partial slots, so every consumer still sums kRedBlocks partials)
+inline int red_grid(long work)
+{
+    const long b = (work + 511) / 512;                 // ~2 elements per thread
+    return (int)(b < 1 ? 1 : (b > kRedBlocks ? kRedBlocks : b));
+}
+// the unused tail of a partials array (blocks >= gridDim.x of a shortened reduction grid)
+__device__ __forceinline__ void zero_tail(double *part)
+{
+    if (blockIdx.x == 0)
+        for (int b = gridDim.x + threadIdx.x; b < kRedBlocks; b += blockDim.x) part[b] = 0.0;
+}
 constexpr int kRedThreads = 256;
 constexpr long kTmaSlack = 1L << 16;     // doubles appended to grid allocations (TMA over-read)
 
