@@ -47,7 +47,9 @@ def _args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--config", default="cfg4", help="cfg1..cfg5, or cfg5-sweep (the five eps values as "
+                    "independent problems over the ranks)")
+    ap.add_argument("--max-iters", type=int, default=100, help="cfg5-sweep: common FGMRES cap (SURVEY A19)")
     ap.add_argument("--n", "--size", dest="n", type=int, default=None, help="override N (diagnostics only)")
     ap.add_argument("--eps", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -171,6 +173,87 @@ def cpu_baseline(cfg):
     P.close()
     return {"value": cfg.unknowns / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"one full {cfg.name} solve (setup + FGMRES, {res['iters']} iterations), {dt:.2f} s"}
+
+
+CFG5_EPS = [1e-2, 1e-4, 1e-6, 1e-8, 1e-10]   # B:11
+
+
+def sweep_share(n_items, rank, world):
+    """Independent problems of a sweep, round-robin over ranks (no data-path collective)."""
+    return [i for i in range(n_items) if i % world == rank]
+
+
+def run_sweep(args, rank, world):
+    """cfg5's epsilon sweep (B:11) as one step: the five independent 8192^2 solves, sharded over
+    the ranks round-robin; the step time is the max over ranks.  Common iteration cap for the
+    non-converging large-eps cells."""
+    import torch
+    import paper_2108_13468_b200 as spp
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    mine = sweep_share(len(CFG5_EPS), rank, world)
+    jobs = []
+    for i in mine:
+        cfg = si.config("cfg5", N=args.n, eps=CFG5_EPS[i])
+        N = cfg.N
+        x = spp.spp_shishkin_mesh(N, cfg.eps, cfg.sigma, cfg.beta_x)
+        y = spp.spp_shishkin_mesh(N, cfg.eps, cfg.sigma, cfg.beta_y)
+        c1, c2, r, f = si.sample_2d(cfg, x, y)
+        d = [torch.from_numpy(np.ascontiguousarray(a).ravel()).to(dev) for a in (c1, c2, r, f)]
+        o = spp.spp_default_options(2)
+        o.tol = cfg.tol
+        o.max_iters = args.max_iters
+        jobs.append((cfg, x, y, d, torch.empty_like(d[3]), o))
+
+    def step():
+        # one problem at a time: create (eps fixes the mesh), set up, solve, free -- a capped
+        # non-converging cell keeps 2 x max_iters Krylov vectors of 537 MB alive
+        its = {}
+        for cfg, x, y, d, u, o in jobs:
+            S = spp.Solver(2, cfg.N, cfg.eps, x, y, d[0], d[1], d[2], options=o)
+            res = S.solve(d[3], u)
+            its[f"{cfg.eps:g}"] = res.stats["iters"]
+            S.close()
+        return its
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(dev.index)
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        its = step()
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, dev)
+    iters = {}
+    if world > 1:
+        allits = [None] * world
+        torch.distributed.all_gather_object(allits, its)
+        for d_ in allits:
+            iters.update(d_)
+    else:
+        iters = its
+    if rank != 0:
+        return None
+    N = si.config("cfg5", N=args.n).N
+    total = len(CFG5_EPS) * (N - 1) ** 2
+    return {"metric": METRIC, "value": total / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg5 epsilon sweep: {len(CFG5_EPS)} independent {N}x{N} solves "
+                                   f"(eps {CFG5_EPS}), round-robin over ranks", "N": N,
+                       "unknowns": total, "max_iters": args.max_iters,
+                       "iters_per_eps": {k: iters[k] for k in sorted(iters, key=float, reverse=True)},
+                       "parallelism": f"independent problems over {world} GPU(s)",
+                       "l2": "inputs larger than L2"},
+            "clocks": clocks}
 
 
 def run_ours(args, rank, world):
@@ -313,7 +396,10 @@ def main():
         if backend == "nccl":
             torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         dist.init_process_group(backend)
-    line = run_reference(args, rank, world) if args.impl == "reference" else run_ours(args, rank, world)
+    if args.config == "cfg5-sweep" and args.impl != "reference":
+        line = run_sweep(args, rank, world)
+    else:
+        line = run_reference(args, rank, world) if args.impl == "reference" else run_ours(args, rank, world)
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

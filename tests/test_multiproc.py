@@ -53,3 +53,14 @@ def test_reference_arm_under_torchrun_two_ranks():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_sweep_share_partitions_the_problems():
+    """cfg5's epsilon sweep over N ranks: every problem solved exactly once, round-robin."""
+    sys.path.insert(0, ROOT)
+    import bench
+    for world in range(1, 9):
+        shares = [bench.sweep_share(len(bench.CFG5_EPS), r, world) for r in range(world)]
+        flat = sorted(i for sh in shares for i in sh)
+        assert flat == list(range(len(bench.CFG5_EPS)))
+        assert max(len(sh) for sh in shares) == -(-len(bench.CFG5_EPS) // world)
