@@ -845,7 +845,7 @@ bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs)
 // written to HBM.
 // ------------------------------------------------------------------------------------------
 template <int RT>
-__global__ void __launch_bounds__(256) k_resid_restrict(int nf, long pv, long pc, const double *__restrict__ e,
+__global__ void __launch_bounds__(256, 7) k_resid_restrict(int nf, long pv, long pc, const double *__restrict__ e,
     const double *__restrict__ R, const double *__restrict__ aE, const double *__restrict__ aN,
     const double *__restrict__ rr, const double *__restrict__ aW, const double *__restrict__ aS,
     const double *__restrict__ hbf, const double *__restrict__ kbf, int nc, long pvc,
