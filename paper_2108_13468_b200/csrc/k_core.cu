@@ -40,7 +40,7 @@ __device__ __forceinline__ void coef_at(int i, int j, int n, double eps, double 
     D = ((aW[i] + e) + (aS[j] + no)) + r;
 }
 
-__global__ void k_coef_2d(int N, long P, double eps, double hx, double Hx, double hy, double Hy,
+__global__ void __launch_bounds__(256, 6) k_coef_2d(int N, long P, double eps, double hx, double Hx, double hy, double Hy,
                           const double *c1, const double *c2, const double *r, const double *aW,
                           const double *aS, double *aE, double *aN, double *rr, double *ca,
                           double *cn, double *cd, double *ya, double *yn, int *bad)
