@@ -50,6 +50,7 @@ def _args():
     ap.add_argument("--config", default="cfg4", help="cfg1..cfg5, or cfg5-sweep (the five eps values as "
                     "independent problems over the ranks)")
     ap.add_argument("--max-iters", type=int, default=100, help="cfg5-sweep: common FGMRES cap (SURVEY A19)")
+    ap.add_argument("--batch", type=int, default=16384, help="cfg1-batch: problems per GPU")
     ap.add_argument("--n", "--size", dest="n", type=int, default=None, help="override N (diagnostics only)")
     ap.add_argument("--eps", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -116,6 +117,23 @@ def run_reference(args, rank, world):
     if rank != 0:
         return None
     import oracle
+    if args.config == "cfg1-batch":
+        eps = batch1d_inputs(args.batch, 0)
+        for _ in range(args.warmup):
+            batch1d_oracle_sample(eps, 0, seconds=1.0)
+        t0, done = time.perf_counter(), 0
+        for _ in range(args.steps):
+            d, _, _ = batch1d_oracle_sample(eps, 0, seconds=10.0)
+            done += d
+        dt = time.perf_counter() - t0
+        val = done * (BATCH_N - 1) / dt
+        return {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+                "config": {"workload": f"cfg1-batch (bounded sample of the {args.batch}-problem batch)"},
+                "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                 "sample": f"{done} problems of the batch in {args.steps} steps of ~10 s"},
+                "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     cfg = si.config(args.config, N=args.n, eps=args.eps)
     N = cfg.N
     x = oracle.mesh(N, cfg.eps, cfg.sigma, cfg.beta_x)
@@ -143,6 +161,134 @@ def run_reference(args, rank, world):
                              "sample": f"one full {cfg.name} solve (setup + FGMRES, {res['iters']} iterations) "
                                        f"per step, single-threaded C oracle"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    return line
+
+
+# ---------------------------------------------------------------------------- batched 1D
+BATCH_N, BATCH_EPS, BATCH_SEED, BATCH_MAXIT = 256, (1e-8, 1e-2), 7, 64
+
+
+def batch1d_inputs(nprob, first=0):
+    """cfg1-batch: nprob cfg1-sized 1D problems (N = 256), eps log-uniform
+    in [1e-8, 1e-2], seeded coefficients / rhs (spp_inputs.sample_batch1d); problems
+    first .. first+nprob-1 of the global sequence (each rank its own slice)."""
+    _, eps_all = si.batch1d_params(first + nprob, BATCH_SEED, (BATCH_N,), BATCH_EPS)
+    eps = eps_all[first:]
+    return eps
+
+
+def _batch_arrays(eps, first, mesh):
+    xs, cs, rs, fs = [], [], [], []
+    for k, e in enumerate(eps):
+        x = mesh(BATCH_N, float(e), 2.0, 1.0)
+        c, r, f = si.sample_batch1d(first + k, x, BATCH_SEED)
+        xs.append(x); cs.append(c); rs.append(r); fs.append(f)
+    return [np.concatenate(a) for a in (xs, cs, rs, fs)]
+
+
+def batch1d_oracle_sample(eps, first, seconds=15.0):
+    """The oracle's 1D GMRES over a bounded sample of the batch (as many problems as fit in
+    ~`seconds` of single-threaded CPU time)."""
+    import oracle
+    t0, done, its = time.perf_counter(), 0, []
+    for k, e in enumerate(eps):
+        x = oracle.mesh(BATCH_N, float(e), 2.0, 1.0)
+        c, r, f = si.sample_batch1d(first + k, x, BATCH_SEED)
+        res = oracle.solve1d(BATCH_N, float(e), x, c, r, f, tol=1e-10, maxit=BATCH_MAXIT)
+        its.append(res["iters"])
+        done += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    return done, dt, its
+
+
+def run_batch1d(args, rank, world):
+    import torch
+    import paper_2108_13468_b200 as spp
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    P, first = args.batch, rank * args.batch
+    eps = batch1d_inputs(P, first)
+    xcat, ccat, rcat, fcat = _batch_arrays(eps, first, spp.spp_shishkin_mesh)
+    Ns = np.full(P, BATCH_N, np.int32)
+    d_c, d_r, d_f = [torch.from_numpy(a).to(dev) for a in (ccat, rcat, fcat)]
+    u = torch.empty_like(d_f)
+    o = spp.spp_default_options(1)
+    o.max_iters = BATCH_MAXIT
+    stream = torch.cuda.current_stream(dev)
+    unknowns = P * (BATCH_N - 1)
+
+    B = spp.Batch1D(Ns, eps, xcat, d_c, d_r, options=o, stream=stream)   # workspace + first setup
+
+    def step(c_, r_, f_, u_):
+        n0 = B.launches()
+        B.setup(c_, r_)                  # setup counted in time-to-solution (P:1393-1398)
+        res = B.solve(f_, u_)
+        return res, B.launches() - n0
+
+    for _ in range(args.warmup):
+        res, _ = step(d_c, d_r, d_f, u)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(dev.index)
+    clk.start()
+    launches = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        res, n = step(d_c, d_r, d_f, u)
+        launches += n
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, dev)
+    solve_ms = res.stats["solve_s"] * 1e3
+    e2e = None
+    if not args.no_e2e:
+        hp = [torch.from_numpy(a).pin_memory() for a in (ccat, rcat, fcat)]
+        hu = torch.empty(unknowns, dtype=torch.float64).pin_memory()
+        step(hp[0], hp[1], hp[2], hu)
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        for _ in range(max(1, min(args.steps, 3))):
+            step(hp[0], hp[1], hp[2], hu)
+        ems = max_over_ranks((time.perf_counter() - t0) * 1e3 / max(1, min(args.steps, 3)), world, dev)
+        e2e = {"value": unknowns * world / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 3 * unknowns * 8,
+               "d2h_bytes_per_step": unknowns * 8, "ms_per_step": ems}
+    if rank != 0:
+        return None
+    peak, peak_kind = _peaks()
+    # dominant kernel k_solve1d_batch: algorithmic bytes = inputs c, r, f read + u written
+    # (32 B/node); the Krylov basis stays in L1/L2 per CTA (DESIGN.md "Batched 1D")
+    alg = 32.0 * unknowns
+    line = {
+        "metric": METRIC, "value": unknowns * world / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg1-batch: {P} independent 1D problems per GPU (N={BATCH_N}, eps log-uniform "
+                               f"{BATCH_EPS}, seeded c, r, f), right FGMRES, Jacobi-weighted rtol 1e-10, fp64",
+                   "problems_per_s": P * world / (ms * 1e-3), "unknowns": unknowns,
+                   "iters": {"min": int(res.iters.min()), "median": float(np.median(res.iters)),
+                             "max": int(res.iters.max())}, "converged": int(res.converged.sum()),
+                   "setup_s": res.stats["setup_s"], "solve_s": res.stats["solve_s"],
+                   "l2": "per-step setup + solve; per-CTA Krylov basis re-read from L1/L2",
+                   "parallelism": "independent problems per GPU" if world > 1 else "single GPU"},
+        "roofline": {"kernel": "k_solve1d_batch", "bound": "hbm", "achieved": alg / (solve_ms * 1e-3) / 1e9,
+                     "peak": peak, "unit": "GB/s", "frac": alg / (solve_ms * 1e-3) / 1e9 / peak, "traffic": None,
+                     "peak_kind": peak_kind, "avg_launch_ms": solve_ms, "algorithmic_bytes_per_launch": alg},
+        "gpu_launches": int(launches // max(args.steps, 1)),
+        "clocks": clocks,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline:
+        done, dt, its = batch1d_oracle_sample(eps, first)
+        line["cpu_baseline"] = {"value": done * (BATCH_N - 1) / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": f"the first {done} problems of the batch, {dt:.1f} s"}
     return line
 
 
@@ -398,6 +544,8 @@ def main():
         dist.init_process_group(backend)
     if args.config == "cfg5-sweep" and args.impl != "reference":
         line = run_sweep(args, rank, world)
+    elif args.config == "cfg1-batch" and args.impl != "reference":
+        line = run_batch1d(args, rank, world)
     else:
         line = run_reference(args, rank, world) if args.impl == "reference" else run_ours(args, rank, world)
     if rank == 0 and line is not None:

@@ -183,6 +183,38 @@ SPP_API const char *spp_profile_name(int32_t k);
 
 SPP_API void spp_destroy(spp_ctx *c);
 
+/* ---- Batched 1D solves (the 1D method of P:375-386 / P:828-833) ----
+ * nprob independent problems -eps_p u'' - c_p u' + r_p u = f_p on their own Shishkin meshes,
+ * each solved exactly as a single spp_create(dim=1)/spp_solve would (same kernels' setup and
+ * Krylov body, one CTA per problem; results are bitwise those of the single solve), with one
+ * set of options for the whole batch.
+ *   n, eps     host, nprob entries: N_p (even, 4 <= N_p <= 8192) and eps_p in (0,1].
+ *   x          host, concatenated meshes: problem p's N_p+1 coordinates start at
+ *              sum_{q<p} (N_q+1); each is validated as in spp_create (SPP_E_MESH).
+ *   c, r       concatenated interior samples with residency `mem`: problem p's N_p-1 values
+ *              start at sum_{q<p} (N_q-1) (the same layout for f and u below).  Copied at
+ *              create; SPP_E_COEF names the first problem with c <= 0 or r < 0.
+ *   o          options shared by every problem (NULL = spp_default_options(1)); max_iters <= 512.
+ * spp_batch1d_solve: f, u_out concatenated as c; iters_out, converged_out, res_out (host, may be
+ * NULL; nprob entries) receive each problem's iterations, convergence flag and final monitored
+ * residual.  st (may be NULL): iters = max over problems, applies = sum, converged = all,
+ * setup_s / solve_s device times.  Returns SPP_OK if every problem converged, else
+ * SPP_NOT_CONVERGED (results still valid).  Errors at create leave *out NULL and are reported
+ * by spp_last_error(NULL); errors at solve by spp_batch1d_last_error(b).
+ * spp_batch1d_setup: re-run the setup for new c, r (same layout and residency rules as at
+ * create) on the same problems and meshes, reusing the device workspace. */
+typedef struct spp_batch1d spp_batch1d;
+SPP_API spp_status spp_batch1d_create(int32_t nprob, const int32_t *n, const double *eps, const double *x,
+                              const double *c, const double *r, spp_mem mem, const spp_options *o,
+                              void *cuda_stream, spp_batch1d **out);
+SPP_API spp_status spp_batch1d_setup(spp_batch1d *b, const double *c, const double *r, spp_mem mem);
+SPP_API spp_status spp_batch1d_solve(spp_batch1d *b, const double *f, double *u_out, spp_mem mem,
+                             int32_t *iters_out, int32_t *converged_out, double *res_out, spp_stats *st);
+SPP_API int32_t spp_batch1d_nprob(const spp_batch1d *b);
+SPP_API int64_t spp_batch1d_launches(const spp_batch1d *b);
+SPP_API const char *spp_batch1d_last_error(const spp_batch1d *b);
+SPP_API void spp_batch1d_destroy(spp_batch1d *b);
+
 /* Last error message for this context (or the thread-local one when c == NULL). */
 SPP_API const char *spp_last_error(const spp_ctx *c);
 

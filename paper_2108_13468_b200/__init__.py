@@ -57,7 +57,9 @@ class spp_stats(ctypes.Structure):
 ABI_FUNCTIONS = ["spp_default_options", "spp_shishkin_mesh", "spp_create", "spp_setup",
                  "spp_solve", "spp_apply_stage", "spp_kernel_launches", "spp_mg_levels", "spp_mg_level_n",
                  "spp_profile_enable", "spp_profile_reset", "spp_profile_get", "spp_profile_name",
-                 "spp_destroy", "spp_last_error", "spp_version"]
+                 "spp_destroy", "spp_last_error", "spp_version",
+                 "spp_batch1d_create", "spp_batch1d_setup", "spp_batch1d_solve", "spp_batch1d_nprob", "spp_batch1d_launches",
+                 "spp_batch1d_last_error", "spp_batch1d_destroy"]
 
 if not LIB_PATH.exists():
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
@@ -87,6 +89,18 @@ _lib.spp_last_error.argtypes = [_vp]
 _lib.spp_last_error.restype = ctypes.c_char_p
 _lib.spp_version.argtypes = []
 _lib.spp_version.restype = ctypes.c_char_p
+_ip = ctypes.POINTER(ctypes.c_int32)
+_lib.spp_batch1d_create.argtypes = [ctypes.c_int32, _ip, _dp, _dp, _vp, _vp, ctypes.c_int,
+                                    ctypes.POINTER(spp_options), _vp, ctypes.POINTER(_vp)]
+_lib.spp_batch1d_setup.argtypes = [_vp, _vp, _vp, ctypes.c_int]
+_lib.spp_batch1d_solve.argtypes = [_vp, _vp, _vp, ctypes.c_int, _ip, _ip, _dp, ctypes.POINTER(spp_stats)]
+_lib.spp_batch1d_nprob.argtypes = [_vp]
+_lib.spp_batch1d_launches.argtypes = [_vp]
+_lib.spp_batch1d_launches.restype = ctypes.c_int64
+_lib.spp_batch1d_last_error.argtypes = [_vp]
+_lib.spp_batch1d_last_error.restype = ctypes.c_char_p
+_lib.spp_batch1d_destroy.argtypes = [_vp]
+_lib.spp_batch1d_destroy.restype = None
 
 
 class SppError(RuntimeError):
@@ -238,3 +252,76 @@ class Solver:
             _lib.spp_profile_get(self.h, k, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(b))
             out[_lib.spp_profile_name(k).decode()] = dict(launches=n.value, ms=ms.value, bytes=b.value)
         return out
+
+
+@dataclass
+class BatchResult:
+    u: object
+    iters: np.ndarray
+    converged: np.ndarray
+    res: np.ndarray
+    status: int
+    stats: dict
+
+
+class Batch1D:
+    """One spp_batch1d: nprob independent 1D problems (spp.h "Batched 1D solves").  n, eps and
+    the concatenated meshes x are host arrays; c, r (and f, u at solve) are concatenated
+    interior samples, numpy (host) or torch CUDA float64 (device)."""
+
+    def __init__(self, n, eps, x, c, r, options: spp_options | None = None, stream=None):
+        self.n = np.ascontiguousarray(n, dtype=np.int32)
+        self.eps = np.ascontiguousarray(eps, dtype=np.float64)
+        self._x = np.ascontiguousarray(x, dtype=np.float64)
+        self.total = int(np.sum(self.n - 1))
+        self.opt = options if options is not None else spp_default_options(1)
+        pc, mem, kc = _ptr(c)
+        pr, _, kr = _ptr(r)
+        h = _vp()
+        self._stream = _stream_handle(stream)
+        _check(_lib.spp_batch1d_create(len(self.n), self.n.ctypes.data_as(_ip), self.eps.ctypes.data_as(_dp),
+                                       self._x.ctypes.data_as(_dp), pc, pr, mem, ctypes.byref(self.opt),
+                                       self._stream, ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.spp_batch1d_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def launches(self):
+        return _lib.spp_batch1d_launches(self.h)
+
+    def setup(self, c, r):
+        pc, mem, kc = _ptr(c)
+        pr, _, kr = _ptr(r)
+        rc = _lib.spp_batch1d_setup(self.h, pc, pr, mem)
+        if rc < 0:
+            raise SppError(rc, (_lib.spp_batch1d_last_error(self.h) or b"").decode())
+
+    def solve(self, f, u=None) -> BatchResult:
+        pf, mem, kf = _ptr(f)
+        if u is None:
+            if mem == SPP_HOST:
+                u = np.zeros(self.total)
+            else:
+                import torch
+                u = torch.zeros_like(f)
+        pu, memu, ku = _ptr(u)
+        if memu != mem:
+            raise ValueError("f and u must have the same residency")
+        P = len(self.n)
+        it, cv, res = np.zeros(P, np.int32), np.zeros(P, np.int32), np.zeros(P)
+        st = spp_stats()
+        rc = _lib.spp_batch1d_solve(self.h, pf, pu, mem, it.ctypes.data_as(_ip), cv.ctypes.data_as(_ip),
+                                    res.ctypes.data_as(_dp), ctypes.byref(st))
+        if rc < 0:
+            raise SppError(rc, (_lib.spp_batch1d_last_error(self.h) or b"").decode())
+        return BatchResult(u=ku if mem == SPP_HOST else u, iters=it, converged=cv.astype(bool), res=res,
+                           status=rc, stats=st.asdict())

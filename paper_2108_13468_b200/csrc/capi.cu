@@ -1033,4 +1033,148 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
     return SPP_OK;
 }
 
+// ------------------------------------------------------------------ batched 1D (NEXT-3)
+#define BFAIL(bp, code, ...)                                                  \
+    do {                                                                      \
+        char _b[512];                                                         \
+        snprintf(_b, sizeof(_b), __VA_ARGS__);                                \
+        if (bp) (bp)->err = _b;                                               \
+        g_err = _b;                                                           \
+        return code;                                                          \
+    } while (0)
+#define BCK(bp, expr)                                                         \
+    do {                                                                      \
+        cudaError_t _e = (expr);                                              \
+        if (_e != cudaSuccess)                                                \
+            BFAIL(bp, SPP_E_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+    } while (0)
+
+static void batch1d_free(Batch1 *b)
+{
+    if (!b) return;
+    if (b->st) cudaStreamSynchronize(b->st); else cudaDeviceSynchronize();
+    cudaFree(b->scratch); cudaFree(b->dpar); cudaFree(b->doff); cudaFree(b->dint); cudaFree(b->stage);
+    delete b;
+}
+
+spp_status spp_batch1d_setup(spp_batch1d *bx, const double *c, const double *r, spp_mem mem)
+{
+    Batch1 *b = (Batch1 *)bx;
+    if (!b) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_batch1d_setup: NULL batch");
+    if (!c || !r) BFAIL(b, SPP_E_ARG, "spp_batch1d_setup: NULL coefficient array");
+    const int nprob = b->nprob;
+    const size_t bytes = sizeof(double) * (size_t)b->total;
+    const double *dc = c, *dr = r;
+    if (mem == SPP_HOST) {
+        if (!b->stage) BCK(b, cudaMalloc(&b->stage, 2 * bytes));
+        BCK(b, cudaMemcpyAsync(b->stage, c, bytes, cudaMemcpyHostToDevice, b->st));
+        BCK(b, cudaMemcpyAsync(b->stage + b->total, r, bytes, cudaMemcpyHostToDevice, b->st));
+        dc = b->stage; dr = b->stage + b->total;
+    }
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0, b->st);
+    cudaError_t ce = batch1d_setup(b, dc, dr);
+    cudaEventRecord(e1, b->st);
+    std::vector<int> bad(nprob);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(bad.data(), b->dint + 4 * nprob, sizeof(int) * nprob, cudaMemcpyDeviceToHost, b->st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(b->st);
+    cudaEventElapsedTime(&b->setup_ms, e0, e1);
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    if (ce != cudaSuccess) BFAIL(b, SPP_E_CUDA, "1D batch setup: %s", cudaGetErrorString(ce));
+    for (int p = 0; p < nprob; ++p)
+        if (bad[p]) BFAIL(b, SPP_E_COEF, "problem %d: coefficients violate c > 0, r >= 0 (P:208-212)", p);
+    return SPP_OK;
+}
+
+spp_status spp_batch1d_create(int32_t nprob, const int32_t *n, const double *eps, const double *x,
+                              const double *c, const double *r, spp_mem mem, const spp_options *o,
+                              void *stream, spp_batch1d **out)
+{
+    if (!out || !n || !eps || !x || !c || !r || nprob < 1) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_batch1d_create: bad argument");
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        FAIL((Ctx *)nullptr, SPP_E_CUDA, "spp_batch1d_create: no CUDA device (this library has no CPU path)");
+    Batch1 *b = new (std::nothrow) Batch1();
+    if (!b) FAIL((Ctx *)nullptr, SPP_E_NOMEM, "host allocation failed");
+    b->st = (cudaStream_t)stream;
+    if (o) b->opt = *o; else spp_default_options(1, &b->opt);
+    if (b->opt.max_iters < 1) b->opt.max_iters = 1;
+    b->nprob = nprob; b->maxit = b->opt.max_iters;
+    if (b->maxit > 512) { delete b; FAIL((Ctx *)nullptr, SPP_E_ARG, "1D batch: max_iters <= 512 (single-CTA solver)"); }
+    b->n.assign(n, n + nprob);
+    b->eps.assign(eps, eps + nprob);
+    b->h.resize(nprob); b->H.resize(nprob);
+    long long xoff = 0;
+    for (int p = 0; p < nprob; ++p) {
+        const int N = n[p];
+        if (N < 4 || (N % 2) || N - 1 > 8191) { delete b; FAIL((Ctx *)nullptr, SPP_E_ARG, "problem %d: N must be even, 4 <= N <= 8192 (got %d)", p, N); }
+        if (!(eps[p] > 0.0) || eps[p] > 1.0) { delete b; FAIL((Ctx *)nullptr, SPP_E_ARG, "problem %d: eps must be in (0,1]", p); }
+        double tau = 0.0;
+        const spp_status s = check_mesh(x + xoff, N, &tau, nullptr);
+        if (s != SPP_OK) { const std::string m = g_err; delete b; FAIL((Ctx *)nullptr, s, "problem %d: %s", p, m.c_str()); }
+        b->h[p] = tau / (N / 2); b->H[p] = (1.0 - tau) / (N / 2);
+        xoff += N + 1;
+    }
+    if (batch1d_alloc(b) != cudaSuccess) { batch1d_free(b); FAIL((Ctx *)nullptr, SPP_E_NOMEM, "1D batch: device allocation failed"); }
+    const spp_status s = spp_batch1d_setup((spp_batch1d *)b, c, r, mem);
+    if (s != SPP_OK) { batch1d_free(b); return s; }
+    *out = (spp_batch1d *)b;
+    return SPP_OK;
+}
+
+spp_status spp_batch1d_solve(spp_batch1d *bx, const double *f, double *u, spp_mem mem, int32_t *iters,
+                             int32_t *converged, double *res, spp_stats *st)
+{
+    Batch1 *b = (Batch1 *)bx;
+    if (!b) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_batch1d_solve: NULL batch");
+    if (!f || !u) BFAIL(b, SPP_E_ARG, "spp_batch1d_solve: NULL f or u");
+    const int P = b->nprob;
+    const size_t bytes = sizeof(double) * (size_t)b->total;
+    if (mem == SPP_HOST && !b->stage) BCK(b, cudaMalloc(&b->stage, 2 * bytes));
+    const int64_t l0 = b->launches;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0, b->st);
+    const double *df = f;
+    double *du = u;
+    if (mem == SPP_HOST) {
+        BCK(b, cudaMemcpyAsync(b->stage, f, bytes, cudaMemcpyHostToDevice, b->st));
+        df = b->stage; du = b->stage + b->total;
+    }
+    BCK(b, batch1d_solve(b, df, du));
+    if (mem == SPP_HOST) BCK(b, cudaMemcpyAsync(u, du, bytes, cudaMemcpyDeviceToHost, b->st));
+    cudaEventRecord(e1, b->st);
+    std::vector<int> io(2 * (size_t)P);
+    std::vector<double> rr(2 * (size_t)P);
+    BCK(b, cudaMemcpyAsync(io.data(), b->dint + 2 * P, sizeof(int) * 2 * P, cudaMemcpyDeviceToHost, b->st));
+    BCK(b, cudaMemcpyAsync(rr.data(), b->dpar + 3 * P, sizeof(double) * 2 * P, cudaMemcpyDeviceToHost, b->st));
+    BCK(b, cudaStreamSynchronize(b->st));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    int all = 1, itmax = 0, itsum = 0;
+    for (int p = 0; p < P; ++p) {
+        if (iters) iters[p] = io[p];
+        if (converged) converged[p] = io[P + p];
+        if (res) res[p] = rr[P + p];
+        all &= io[P + p] ? 1 : 0;
+        itmax = std::max(itmax, io[p]); itsum += io[p];
+    }
+    if (st) {
+        memset(st, 0, sizeof(*st));
+        st->iters = itmax; st->converged = all; st->applies = itsum;
+        st->kernel_launches = (int32_t)(b->launches - l0);
+        st->setup_s = b->setup_ms * 1e-3; st->solve_s = ms * 1e-3;
+        st->res0 = -1.0; st->res_final = -1.0; st->true_res_l2_rel = -1.0; st->true_res_jacobi_rel = -1.0;
+    }
+    return all ? SPP_OK : SPP_NOT_CONVERGED;
+}
+
+int32_t spp_batch1d_nprob(const spp_batch1d *b) { return b ? ((const Batch1 *)b)->nprob : 0; }
+int64_t spp_batch1d_launches(const spp_batch1d *b) { return b ? ((const Batch1 *)b)->launches : 0; }
+const char *spp_batch1d_last_error(const spp_batch1d *b) { return b ? ((const Batch1 *)b)->err.c_str() : g_err.c_str(); }
+void spp_batch1d_destroy(spp_batch1d *b) { batch1d_free((Batch1 *)b); }
+
 }  // extern "C"

@@ -8,7 +8,10 @@
 // Givens update by thread 0.  Two drivers:
 //   right/flexible FGMRES with the recurrence stop (SPP_STOP_REL_JACOBI / REL_L2 / ABS_L2),
 //   left GMRES with the true inf-norm residual stop (SPP_STOP_ABS_MAX; reading R10).
+#include <algorithm>
 #include <cmath>
+#include <tuple>
+#include <vector>
 #include <cstring>
 
 #include "kernels.cuh"
@@ -26,12 +29,11 @@ struct OneD {
     double *dout;
 };
 
-// setup: coefficients + Thomas factors of M (one thread; N <= 8192)
-__global__ void k_setup1d(int N, double eps, double h, double H, const double *c, const double *r,
-                          double *aW, double *aE, double *rr, double *D, double *g, double *al,
-                          double *be, int *bad)
+// setup: coefficients + Thomas factors of M for one problem (one thread; N <= 8192).
+// Returns 1 if the coefficients violate c > 0, r >= 0.
+__device__ int setup1d_one(int N, double eps, double h, double H, const double *c, const double *r,
+                           double *aW, double *aE, double *rr, double *D, double *g, double *al, double *be)
 {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const int n = N / 2, m = N - 1, NL = n;
     double gprev = 0.0, supprev = 0.0;
     int b = 0;
@@ -51,7 +53,15 @@ __global__ void k_setup1d(int N, double eps, double h, double H, const double *c
         g[k] = gk; al[k] = sub * gk; be[k] = sup * gk;
         gprev = gk; supprev = sup;
     }
-    *bad = b;
+    return b;
+}
+
+__global__ void k_setup1d(int N, double eps, double h, double H, const double *c, const double *r,
+                          double *aW, double *aE, double *rr, double *D, double *g, double *al,
+                          double *be, int *bad)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    *bad = setup1d_one(N, eps, h, H, c, r, aW, aE, rr, D, g, al, be);
 }
 
 template <int K>
@@ -144,10 +154,15 @@ __device__ __forceinline__ void axpy1(const OneD &a, double alpha, const double 
 }
 
 template <int K>
-__global__ void __launch_bounds__(512) k_solve1d(OneD a)
+__device__ __forceinline__ void solve1d_body(const OneD &a)
 {
     __shared__ double sA[32], sB[64], red[32];
-    __shared__ double cs[520], sn[520], gg[521], yy[520];
+    // Givens cosines/sines, rotated rhs, LSQ solution and the current Hessenberg column, sized
+    // by max_iters (dynamic shared memory, smem1d_bytes) so that small problems pack many CTAs
+    // per SM; columns are copied to a.H once rotated (for the final back-substitution)
+    extern __shared__ double dyn1[];
+    const int L = a.maxit + 2;
+    double *cs = dyn1, *sn = cs + L, *gg = sn + L, *yy = gg + L, *hc = yy + L;
     __shared__ int s_stop;
     const int m = a.m, maxit = a.maxit, ld = maxit + 1;
     const int k0 = threadIdx.x * K;
@@ -170,7 +185,7 @@ __global__ void __launch_bounds__(512) k_solve1d(OneD a)
                 double *vk = a.V + (size_t)k * m, *zk = a.Z + (size_t)k * m;
                 prec1<K>(a, vk, zk, a.weighted, sA, sB);
                 mv1<K>(a, zk, a.w, a.weighted);
-                double *h = a.H + (size_t)k * ld;
+                double *h = hc;
                 for (int j = 0; j <= k; ++j) {
                     const double hj = dot1<K>(a, a.w, a.V + (size_t)j * m, red);
                     if (threadIdx.x == 0) h[j] = hj;
@@ -191,6 +206,7 @@ __global__ void __launch_bounds__(512) k_solve1d(OneD a)
                     h[k] = den; h[k + 1] = 0.0;
                     gg[k + 1] = -sn[k] * gg[k];
                     gg[k] = cs[k] * gg[k];
+                    for (int i = 0; i <= k + 1; ++i) a.H[(size_t)k * ld + i] = h[i];
                     const double res = fabs(gg[k + 1]);
                     a.hist[k + 1] = res;
                     int stop = !(hn > 0.0);
@@ -231,7 +247,7 @@ __global__ void __launch_bounds__(512) k_solve1d(OneD a)
             for (int k = 0; k < maxit; ++k) {
                 mv1<K>(a, a.V + (size_t)k * m, a.t, false);
                 prec1<K>(a, a.t, a.w, false, sA, sB);
-                double *h = a.H + (size_t)k * ld;
+                double *h = hc;
                 for (int j = 0; j <= k; ++j) {
                     const double hj = dot1<K>(a, a.w, a.V + (size_t)j * m, red);
                     if (threadIdx.x == 0) h[j] = hj;
@@ -252,6 +268,7 @@ __global__ void __launch_bounds__(512) k_solve1d(OneD a)
                     h[k] = den; h[k + 1] = 0.0;
                     gg[k + 1] = -sn[k] * gg[k];
                     gg[k] = cs[k] * gg[k];
+                    for (int i = 0; i <= k + 1; ++i) a.H[(size_t)k * ld + i] = h[i];
                     const int kk = k + 1;
                     for (int i = kk - 1; i >= 0; --i) {
                         double t = gg[i];
@@ -282,17 +299,25 @@ __global__ void __launch_bounds__(512) k_solve1d(OneD a)
     }
 }
 
+template <int K>
+__global__ void __launch_bounds__(512) k_solve1d(OneD a) { solve1d_body<K>(a); }
+
+static size_t smem1d_bytes(int maxit) { return sizeof(double) * 5 * (size_t)(maxit + 2); }
+
 // ------------------------------------------------------------------------------ host
 struct Buf1 {
     double *aW, *aE, *rr, *D, *g, *al, *be, *V, *Z, *x, *w, *t, *H, *hist, *f, *dout;
     int *iout;
 };
 
-static Buf1 layout1(Ctx *c)
+__host__ __device__ static size_t need1(int m, int it)
+{
+    return (size_t)m * 12 + (size_t)(2 * it + 1) * m + (size_t)(it + 1) * (it + 1) + it + 16;
+}
+
+__host__ __device__ static Buf1 layout_at(double *p, int m, int it)
 {
     Buf1 b{};
-    const int m = c->m, it = c->opt.max_iters;
-    double *p = c->d1;
     b.aW = p; p += m; b.aE = p; p += m; b.rr = p; p += m; b.D = p; p += m;
     b.g = p; p += m; b.al = p; p += m; b.be = p; p += m;
     b.V = p; p += (size_t)(it + 1) * m; b.Z = p; p += (size_t)it * m;
@@ -305,6 +330,8 @@ static Buf1 layout1(Ctx *c)
     return b;
 }
 
+static Buf1 layout1(Ctx *c) { return layout_at(c->d1, c->m, c->opt.max_iters); }
+
 spp_status setup_1d(Ctx *c, const double *cc, const double *r, spp_mem mem)
 {
     const int m = c->m, it = c->opt.max_iters;
@@ -313,7 +340,7 @@ spp_status setup_1d(Ctx *c, const double *cc, const double *r, spp_mem mem)
         return SPP_E_ARG;
     }
     if (!c->d1) {
-        const size_t need = (size_t)m * 12 + (size_t)(2 * it + 1) * m + (size_t)(it + 1) * (it + 1) + it + 16;
+        const size_t need = need1(m, it);
         if (cudaMalloc(&c->d1, sizeof(double) * need) != cudaSuccess) { c->err = "1D: cudaMalloc failed"; return SPP_E_NOMEM; }
         cudaMemsetAsync(c->d1, 0, sizeof(double) * need, c->st);
     }
@@ -364,11 +391,12 @@ spp_status solve_1d_abi(Ctx *c, const double *f, double *u, spp_mem mem, double 
     if (T < 32) T = 32;
     if (T > 512) T = 512;
     const int K = (m + T - 1) / T;
-    if (K <= 1) k_solve1d<1><<<1, T, 0, c->st>>>(a);
-    else if (K <= 2) k_solve1d<2><<<1, T, 0, c->st>>>(a);
-    else if (K <= 4) k_solve1d<4><<<1, T, 0, c->st>>>(a);
-    else if (K <= 8) k_solve1d<8><<<1, T, 0, c->st>>>(a);
-    else k_solve1d<16><<<1, T, 0, c->st>>>(a);
+    const size_t sm = smem1d_bytes(it);
+    if (K <= 1) k_solve1d<1><<<1, T, sm, c->st>>>(a);
+    else if (K <= 2) k_solve1d<2><<<1, T, sm, c->st>>>(a);
+    else if (K <= 4) k_solve1d<4><<<1, T, sm, c->st>>>(a);
+    else if (K <= 8) k_solve1d<8><<<1, T, sm, c->st>>>(a);
+    else k_solve1d<16><<<1, T, sm, c->st>>>(a);
     c->launches++;
     if (u) cudaMemcpyAsync(u, b.x, sizeof(double) * m, mem == SPP_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, c->st);
     cudaEventRecord(e1, c->st);
@@ -396,6 +424,155 @@ spp_status solve_1d_abi(Ctx *c, const double *f, double *u, spp_mem mem, double 
         st->true_res_l2_rel = -1.0; st->true_res_jacobi_rel = -1.0;
     }
     return io[1] ? SPP_OK : SPP_NOT_CONVERGED;
+}
+
+// ------------------------------------------------------------------------------ batched 1D
+// NEXT-3: many independent 1D problems (any mix of N <= 8192 and eps) in one
+// launch per launch shape, one CTA per problem -- the same setup and Krylov body as the single
+// solve, so every problem's result is bitwise the single-problem result.
+struct Batch1Args {
+    const int *n, *idx;
+    const double *eps, *h, *H;
+    const long long *xo, *so;
+    const double *c, *r, *f;
+    double *u, *scratch, *res0, *res;
+    int *iters, *conv, *bad;
+    OneD proto;          // option fields shared by the batch
+    int nprob, maxit;
+};
+
+__global__ void k_setup1d_batch(Batch1Args b)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;   // one thread per problem
+    if (p >= b.nprob) return;
+    const int N = b.n[p], m = N - 1;
+    Buf1 l = layout_at(b.scratch + b.so[p], m, b.maxit);
+    b.bad[p] = setup1d_one(N, b.eps[p], b.h[p], b.H[p], b.c + b.xo[p], b.r + b.xo[p], l.aW, l.aE, l.rr, l.D,
+                           l.g, l.al, l.be);
+}
+
+template <int K>
+__global__ void __launch_bounds__(512) k_solve1d_batch(Batch1Args b)
+{
+    const int p = b.idx[blockIdx.x];
+    const int m = b.n[p] - 1;
+    Buf1 l = layout_at(b.scratch + b.so[p], m, b.maxit);
+    OneD a = b.proto;
+    a.m = m;
+    a.aW = l.aW; a.aE = l.aE; a.rr = l.rr; a.D = l.D; a.g = l.g; a.al = l.al; a.be = l.be;
+    a.f = b.f + b.xo[p];
+    a.V = l.V; a.Z = l.Z; a.x = l.x; a.w = l.w; a.t = l.t; a.H = l.H; a.hist = l.hist;
+    a.iout = l.iout; a.dout = l.dout;
+    solve1d_body<K>(a);
+    __syncthreads();
+    double *u = b.u + b.xo[p];
+    for (int k = threadIdx.x; k < m; k += blockDim.x) u[k] = a.x[k];
+    if (threadIdx.x == 0) {
+        b.iters[p] = a.iout[0]; b.conv[p] = a.iout[1];
+        b.res0[p] = a.dout[0]; b.res[p] = a.dout[1];
+    }
+}
+
+// launch shape of a problem with m unknowns: T threads, K rows per thread (as the single solve)
+static void shape1(int m, int *T_, int *K_)
+{
+    int T = (m + 7) / 8;
+    T = ((T + 31) / 32) * 32;
+    if (T < 32) T = 32;
+    if (T > 512) T = 512;
+    int K = (m + T - 1) / T;
+    K = K <= 1 ? 1 : K <= 2 ? 2 : K <= 4 ? 4 : K <= 8 ? 8 : 16;
+    *T_ = T; *K_ = K;
+}
+
+static Batch1Args bargs(Batch1 *b)
+{
+    Batch1Args a{};
+    const int P = b->nprob;
+    a.eps = b->dpar; a.h = b->dpar + P; a.H = b->dpar + 2 * P; a.res0 = b->dpar + 3 * P; a.res = b->dpar + 4 * P;
+    a.xo = b->doff; a.so = b->doff + P;
+    a.n = b->dint; a.idx = b->dint + P; a.iters = b->dint + 2 * P; a.conv = b->dint + 3 * P; a.bad = b->dint + 4 * P;
+    a.scratch = b->scratch;
+    a.nprob = P; a.maxit = b->maxit;
+    OneD &o = a.proto;
+    o.maxit = b->maxit; o.fixed = b->opt.fixed_iters; o.tol = b->opt.tol; o.side = b->opt.side;
+    o.leftmax = b->opt.side == SPP_LEFT ? 1 : 0;
+    o.weighted = b->opt.stop == SPP_STOP_REL_JACOBI;
+    o.stop_abs = b->opt.stop == SPP_STOP_ABS_L2;
+    return a;
+}
+
+cudaError_t batch1d_alloc(Batch1 *b)
+{
+    const int P = b->nprob;
+    b->xo.resize(P); b->so.resize(P);
+    long long xo = 0, so = 0;
+    std::vector<std::tuple<int, int, int>> key(P);
+    for (int p = 0; p < P; ++p) {
+        const int m = b->n[p] - 1;
+        b->xo[p] = xo; b->so[p] = so;
+        xo += m; so += (long long)need1(m, b->maxit);
+        int T, K;
+        shape1(m, &T, &K);
+        key[p] = std::make_tuple(K, T, p);
+    }
+    b->total = xo; b->scratch_len = so;
+    std::sort(key.begin(), key.end());
+    b->order.resize(P);
+    for (int p = 0; p < P; ++p) {
+        const int K = std::get<0>(key[p]), T = std::get<1>(key[p]);
+        b->order[p] = std::get<2>(key[p]);
+        if (p == 0 || K != b->gK.back() || T != b->gT.back()) {
+            b->gstart.push_back(p); b->gcount.push_back(0); b->gK.push_back(K); b->gT.push_back(T);
+        }
+        b->gcount.back()++;
+    }
+    SPP_CUDA_TRY(cudaMalloc(&b->scratch, sizeof(double) * so));
+    SPP_CUDA_TRY(cudaMemsetAsync(b->scratch, 0, sizeof(double) * so, b->st));
+    SPP_CUDA_TRY(cudaMalloc(&b->dpar, sizeof(double) * 5 * P));
+    SPP_CUDA_TRY(cudaMalloc(&b->doff, sizeof(long long) * 2 * P));
+    SPP_CUDA_TRY(cudaMalloc(&b->dint, sizeof(int) * 5 * P));
+    std::vector<double> par(3 * (size_t)P);
+    for (int p = 0; p < P; ++p) { par[p] = b->eps[p]; par[P + p] = b->h[p]; par[2 * P + p] = b->H[p]; }
+    std::vector<long long> off(2 * (size_t)P);
+    for (int p = 0; p < P; ++p) { off[p] = b->xo[p]; off[P + p] = b->so[p]; }
+    std::vector<int> in(2 * (size_t)P);
+    for (int p = 0; p < P; ++p) { in[p] = b->n[p]; in[P + p] = b->order[p]; }
+    SPP_CUDA_TRY(cudaMemcpyAsync(b->dpar, par.data(), sizeof(double) * 3 * P, cudaMemcpyHostToDevice, b->st));
+    SPP_CUDA_TRY(cudaMemcpyAsync(b->doff, off.data(), sizeof(long long) * 2 * P, cudaMemcpyHostToDevice, b->st));
+    SPP_CUDA_TRY(cudaMemcpyAsync(b->dint, in.data(), sizeof(int) * 2 * P, cudaMemcpyHostToDevice, b->st));
+    return cudaStreamSynchronize(b->st);   // host vectors above go out of scope
+}
+
+cudaError_t batch1d_setup(Batch1 *b, const double *c, const double *r)
+{
+    Batch1Args a = bargs(b);
+    a.c = c; a.r = r;
+    k_setup1d_batch<<<(b->nprob + 127) / 128, 128, 0, b->st>>>(a);
+    b->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t batch1d_solve(Batch1 *b, const double *f, double *u)
+{
+    Batch1Args a = bargs(b);
+    a.f = f; a.u = u;
+    const size_t sm = smem1d_bytes(b->maxit);
+    for (size_t g = 0; g < b->gstart.size(); ++g) {
+        Batch1Args ag = a;
+        ag.idx = a.idx + b->gstart[g];
+        const dim3 grid(b->gcount[g]);
+        const int T = b->gT[g];
+        switch (b->gK[g]) {
+        case 1: k_solve1d_batch<1><<<grid, T, sm, b->st>>>(ag); break;
+        case 2: k_solve1d_batch<2><<<grid, T, sm, b->st>>>(ag); break;
+        case 4: k_solve1d_batch<4><<<grid, T, sm, b->st>>>(ag); break;
+        case 8: k_solve1d_batch<8><<<grid, T, sm, b->st>>>(ag); break;
+        default: k_solve1d_batch<16><<<grid, T, sm, b->st>>>(ag); break;
+        }
+        b->launches++;
+    }
+    return cudaGetLastError();
 }
 
 }  // namespace spp

@@ -51,4 +51,28 @@ spp_status setup_1d(Ctx *c, const double *cc, const double *r, spp_mem mem);
 spp_status solve_1d_abi(Ctx *c, const double *f, double *u, spp_mem mem, double *hist, int hcap,
                         spp_stats *st);
 
+// Batched 1D solves: nprob independent problems, one CTA each.
+struct Batch1 {
+    cudaStream_t st = nullptr;
+    spp_options opt{};
+    int nprob = 0, maxit = 0;
+    std::vector<int> n;                  // N per problem
+    std::vector<double> eps, h, H;       // mesh widths per problem (h = tau/(N/2), H = (1-tau)/(N/2))
+    std::vector<long long> xo, so;       // offsets of the interior samples / scratch block
+    long long total = 0, scratch_len = 0;
+    std::vector<int> order;              // problems sorted by launch shape
+    std::vector<int> gstart, gcount, gK, gT;
+    double *scratch = nullptr;           // per-problem workspace blocks
+    double *dpar = nullptr;              // eps, h, H, res0, res (5 * nprob)
+    long long *doff = nullptr;           // xo, so (2 * nprob)
+    int *dint = nullptr;                 // n, order, iters, conv, bad (5 * nprob)
+    double *stage = nullptr;             // host-residency staging: f, u (2 * total)
+    int64_t launches = 0;
+    float setup_ms = 0.f;
+    std::string err;
+};
+cudaError_t batch1d_alloc(Batch1 *b);
+cudaError_t batch1d_setup(Batch1 *b, const double *c, const double *r);   // device c, r
+cudaError_t batch1d_solve(Batch1 *b, const double *f, double *u);         // device f, u
+
 }  // namespace spp

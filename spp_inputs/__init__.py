@@ -14,6 +14,7 @@ Configurations (BASELINE.json ``configs``, B:7-11):
   cfg4  2D  c=(1.5+0.5 sin pi x, 1.5+0.5 cos pi y), r=2, f=1+0.1 U(-1,1) seed 0,
             eps=1e-8, N=4096, rtol 1e-8
   cfg5  2D  c=(1,2), r=1, f=1+0.1 U(-1,1) seed 1,  N=8192, eps in {1e-2..1e-10}, rtol 1e-8
+  cfg1-batch  many independent 1D problems: see batch1d_params/sample_batch1d
 Paper workloads (pins):
   ex1d  eq:1D example:   c = 2 + sin 5x, r = 1, f = 4 e^{-x}, C_lower = 0.99
   exp2d eq:exponential_MMS: c = (2,3), r = 1, f = L u*
@@ -121,6 +122,27 @@ def sample_1d(cfg: Config, x):
     if cfg.kind == "ex1d":          # eq:1D example
         return 2.0 + np.sin(5.0 * xi), np.ones_like(xi), 4.0 * np.exp(-xi)
     raise KeyError(cfg.kind)
+
+
+def batch1d_params(nprob: int, seed: int = 7, Ns=(256,), eps_range=(1e-8, 1e-2)):
+    """(N_p, eps_p) of a batch of 1D problems: N cycles through Ns, eps log-uniform in
+    eps_range (counter-based draws, stream 2*p)."""
+    p = np.arange(nprob, dtype=np.uint64)
+    u = splitmix_uniform(seed, 2 * p)
+    lo, hi = np.log10(eps_range[0]), np.log10(eps_range[1])
+    eps = 10.0 ** (lo + (hi - lo) * u)
+    N = np.array([Ns[k % len(Ns)] for k in range(nprob)], dtype=np.int32)
+    return N, eps
+
+
+def sample_batch1d(p: int, x, seed: int = 7):
+    """(c, r, f) of batch problem p at interior nodes: c = 2 + sin(5x + 2 pi U_p) (>= 1, so
+    C_lower = 1), r = 1 + U'_p, f = 1 + x + 0.1 U(-1,1) per node (seed stream p)."""
+    xi = np.asarray(x, dtype=np.float64)[1:-1]
+    u2 = splitmix_uniform(seed, np.array([2 * p + 1], dtype=np.uint64))[0]
+    u3 = splitmix_uniform(seed + 1, np.array([p], dtype=np.uint64))[0]
+    noise = 2.0 * splitmix_uniform(seed + 1000 + p, np.arange(xi.size, dtype=np.uint64)) - 1.0
+    return 2.0 + np.sin(5.0 * xi + 2.0 * np.pi * u2), (1.0 + u3) * np.ones_like(xi), 1.0 + xi + 0.1 * noise
 
 
 def sample_2d(cfg: Config, x, y):

@@ -64,3 +64,14 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(spp.SppError) as ei:
         spp.Solver(2, 16, 1e-3, x, x, np.ones(225), np.ones(225), np.ones(225))
     assert ei.value.code == -6
+
+
+def test_batch1d_no_cpu_fallback_and_argument_checks():
+    import torch
+    import paper_2108_13468_b200 as spp
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    x = spp.spp_shishkin_mesh(16, 1e-3)
+    with pytest.raises(spp.SppError) as ei:
+        spp.Batch1D([16], [1e-3], x, np.ones(15), np.ones(15))
+    assert ei.value.code == -6
