@@ -70,6 +70,7 @@ __device__ __forceinline__ double cta_sum(double v, double *red)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if (nw == 1) return 0.0 + v;                  // one-warp CTA: the same value, no barriers
     __syncthreads();
     if (lane == 0) red[wid] = v;
     __syncthreads();
@@ -153,6 +154,57 @@ __device__ __forceinline__ void axpy1(const OneD &a, double alpha, const double 
     __syncthreads();
 }
 
+// register-slice forms (thread owns rows k0 .. k0+K-1)
+template <int K>
+__device__ __forceinline__ double dotr(int m, const double (&x)[K], const double (&y)[K], double *red)
+{
+    const int k0 = threadIdx.x * K;
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < K; ++u) if (k0 + u < m) s += x[u] * y[u];
+    return cta_sum<K>(s, red);
+}
+
+// z = M^{-1} (s q) with q, z register slices
+template <int K>
+__device__ __forceinline__ void prec1r(const OneD &a, const double (&q)[K], double (&zz)[K], bool scaled,
+                                       double *sA, double *sB)
+{
+    const int k0 = threadIdx.x * K;
+    double al[K], be[K], b[K], y[K];
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+        const int k = k0 + u;
+        if (k < a.m) {
+            b[u] = a.g[k] * (scaled ? a.D[k] * q[u] : q[u]);
+            al[u] = a.al[k]; be[u] = a.be[k];
+        } else { b[u] = 0.0; al[u] = 0.0; be[u] = 0.0; }
+    }
+    fwd_scan<K>(al, b, y, sA, sB);
+    bwd_scan<K>(be, y, zz, sA, sB);
+}
+
+// w = (W) A z with z's register slice zr; the two neighbour rows outside the slice come from
+// zmem (written and synchronised by the caller)
+template <int K>
+__device__ __forceinline__ void mv1r(const OneD &a, const double (&zr)[K], const double *zmem, double (&w)[K],
+                                     bool weighted)
+{
+    const int k0 = threadIdx.x * K;
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+        const int k = k0 + u;
+        if (k < a.m) {
+            const double c = zr[u];
+            const double xw = u > 0 ? zr[u - 1] : (k > 0 ? zmem[k - 1] : 0.0);
+            const double xe = u < K - 1 ? (k < a.m - 1 ? zr[u + 1] : 0.0) : (k < a.m - 1 ? zmem[k + 1] : 0.0);
+            double v = a.aW[k] * (c - xw) + a.aE[k] * (c - xe) + a.rr[k] * c;
+            if (weighted) v /= a.D[k];
+            w[u] = v;
+        } else w[u] = 0.0;
+    }
+}
+
 template <int K>
 __device__ __forceinline__ void solve1d_body(const OneD &a)
 {
@@ -164,6 +216,7 @@ __device__ __forceinline__ void solve1d_body(const OneD &a)
     const int L = a.maxit + 2;
     double *cs = dyn1, *sn = cs + L, *gg = sn + L, *yy = gg + L, *hc = yy + L;
     __shared__ int s_stop;
+    __shared__ double s_res;
     const int m = a.m, maxit = a.maxit, ld = maxit + 1;
     const int k0 = threadIdx.x * K;
     for (int u = 0; u < K; ++u) { const int k = k0 + u; if (k < m) a.x[k] = 0.0; }
@@ -172,28 +225,57 @@ __device__ __forceinline__ void solve1d_body(const OneD &a)
     double res0 = 0.0, resf = 0.0;
     if (!a.leftmax) {
         // ---------------- right / flexible FGMRES ----------------
-        for (int u = 0; u < K; ++u) { const int k = k0 + u; if (k < m) a.V[k] = a.weighted ? a.f[k] / a.D[k] : a.f[k]; }
-        __syncthreads();
-        const double beta = sqrt(dot1<K>(a, a.V, a.V, red));
+        // Each thread keeps its K-row slices of v_k, z_k and w in registers (the MGS loop reads
+        // each basis vector once for both its dot product and its update); V and Z go to
+        // memory for the later iterations and the final combination.  Same operations in the
+        // same order as the memory-resident form.
+        double vr[K], zr[K], wr[K];
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            const int k = k0 + u;
+            vr[u] = k < m ? (a.weighted ? a.f[k] / a.D[k] : a.f[k]) : 0.0;
+        }
+        const double beta = sqrt(dotr<K>(m, vr, vr, red));
         res0 = beta; resf = beta;
         if (threadIdx.x == 0) { a.hist[0] = beta; gg[0] = beta; }
         const double target = a.stop_abs ? a.tol : a.tol * beta;
         if (beta > 0.0) {
-            for (int u = 0; u < K; ++u) { const int k = k0 + u; if (k < m) a.V[k] /= beta; }
-            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < K; ++u) { const int k = k0 + u; if (k < m) { vr[u] /= beta; a.V[k] = vr[u]; } }
             for (int k = 0; k < maxit; ++k) {
-                double *vk = a.V + (size_t)k * m, *zk = a.Z + (size_t)k * m;
-                prec1<K>(a, vk, zk, a.weighted, sA, sB);
-                mv1<K>(a, zk, a.w, a.weighted);
+                double *zk = a.Z + (size_t)k * m;
+                prec1r<K>(a, vr, zr, a.weighted, sA, sB);
+#pragma unroll
+                for (int u = 0; u < K; ++u) { const int q = k0 + u; if (q < m) zk[q] = zr[u]; }
+                __syncthreads();
+                mv1r<K>(a, zr, zk, wr, a.weighted);
                 double *h = hc;
+                double vv[K], vnx[K];
+#pragma unroll
+                for (int u = 0; u < K; ++u) { const int q = k0 + u; vv[u] = q < m ? a.V[q] : 0.0; }
                 for (int j = 0; j <= k; ++j) {
-                    const double hj = dot1<K>(a, a.w, a.V + (size_t)j * m, red);
+                    if (j < k) {             // prefetch v_{j+1} under the reduction of step j
+                        const double *vj1 = a.V + (size_t)(j + 1) * m;
+#pragma unroll
+                        for (int u = 0; u < K; ++u) { const int q = k0 + u; vnx[u] = q < m ? vj1[q] : 0.0; }
+                    }
+                    const double hj = dotr<K>(m, wr, vv, red);
                     if (threadIdx.x == 0) h[j] = hj;
-                    axpy1<K>(a, -hj, a.V + (size_t)j * m, a.w);
+#pragma unroll
+                    for (int u = 0; u < K; ++u) {
+                        const int q = k0 + u;
+                        if (q < m) wr[u] += -hj * vv[u];
+                        vv[u] = vnx[u];
+                    }
                 }
-                const double hn = sqrt(dot1<K>(a, a.w, a.w, red));
+                const double hn = sqrt(dotr<K>(m, wr, wr, red));
                 double *vn = a.V + (size_t)(k + 1) * m;
-                for (int u = 0; u < K; ++u) { const int kk = k0 + u; if (kk < m) vn[kk] = hn > 0.0 ? a.w[kk] / hn : 0.0; }
+#pragma unroll
+                for (int u = 0; u < K; ++u) {
+                    const int q = k0 + u;
+                    vr[u] = hn > 0.0 ? wr[u] / hn : 0.0;
+                    if (q < m) vn[q] = vr[u];
+                }
                 if (threadIdx.x == 0) {
                     h[k + 1] = hn;
                     for (int i = 0; i < k; ++i) {
@@ -209,6 +291,7 @@ __device__ __forceinline__ void solve1d_body(const OneD &a)
                     for (int i = 0; i <= k + 1; ++i) a.H[(size_t)k * ld + i] = h[i];
                     const double res = fabs(gg[k + 1]);
                     a.hist[k + 1] = res;
+                    s_res = res;
                     int stop = !(hn > 0.0);
                     if (a.fixed > 0) stop |= (k + 1 >= a.fixed);
                     else stop |= (res <= target);
@@ -216,7 +299,7 @@ __device__ __forceinline__ void solve1d_body(const OneD &a)
                 }
                 __syncthreads();
                 iters = k + 1;
-                resf = a.hist[k + 1];
+                resf = s_res;
                 if (s_stop) break;
             }
             conv = resf <= target;
@@ -228,7 +311,17 @@ __device__ __forceinline__ void solve1d_body(const OneD &a)
                 }
             }
             __syncthreads();
-            for (int j = 0; j < iters; ++j) axpy1<K>(a, yy[j], a.Z + (size_t)j * m, a.x);
+            double xr[K];
+#pragma unroll
+            for (int u = 0; u < K; ++u) xr[u] = 0.0;
+            for (int j = 0; j < iters; ++j) {
+                const double *zj = a.Z + (size_t)j * m, yj = yy[j];
+#pragma unroll
+                for (int u = 0; u < K; ++u) { const int q = k0 + u; if (q < m) xr[u] += yj * zj[q]; }
+            }
+#pragma unroll
+            for (int u = 0; u < K; ++u) { const int q = k0 + u; if (q < m) a.x[q] = xr[u]; }
+            __syncthreads();
         } else conv = 1;
     } else {
         // ---------------- left GMRES, true inf-norm residual stop ----------------
