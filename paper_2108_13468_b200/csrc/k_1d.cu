@@ -171,17 +171,19 @@ __device__ __forceinline__ void prec1r(const OneD &a, const double (&q)[K], doub
                                        double *sA, double *sB)
 {
     const int k0 = threadIdx.x * K;
-    double al[K], be[K], b[K], y[K];
+    double c[K], b[K], y[K];
 #pragma unroll
     for (int u = 0; u < K; ++u) {
         const int k = k0 + u;
         if (k < a.m) {
             b[u] = a.g[k] * (scaled ? a.D[k] * q[u] : q[u]);
-            al[u] = a.al[k]; be[u] = a.be[k];
-        } else { b[u] = 0.0; al[u] = 0.0; be[u] = 0.0; }
+            c[u] = a.al[k];
+        } else { b[u] = 0.0; c[u] = 0.0; }
     }
-    fwd_scan<K>(al, b, y, sA, sB);
-    bwd_scan<K>(be, y, zz, sA, sB);
+    fwd_scan<K>(c, b, y, sA, sB);
+#pragma unroll
+    for (int u = 0; u < K; ++u) { const int k = k0 + u; c[u] = k < a.m ? a.be[k] : 0.0; }   // be after the forward pass (register pressure)
+    bwd_scan<K>(c, y, zz, sA, sB);
 }
 
 // w = (W) A z with z's register slice zr; the two neighbour rows outside the slice come from
@@ -534,18 +536,56 @@ struct Batch1Args {
     int nprob, maxit;
 };
 
-__global__ void k_setup1d_batch(Batch1Args b)
+// one warp per problem: the per-row coefficients 32 rows at a time (coalesced), the Thomas
+// recurrence of those 32 rows by lane 0 from shared memory (the same operations as
+// setup1d_one, row by row)
+__global__ void __launch_bounds__(128) k_setup1d_batch(Batch1Args b)
 {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;   // one thread per problem
-    if (p >= b.nprob) return;
-    const int N = b.n[p], m = N - 1;
+    __shared__ double sd[4][3][32];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int p = blockIdx.x * 4 + wq;
+    if (p >= b.nprob) return;                            // whole warp
+    const int N = b.n[p], m = N - 1, n = N / 2, NL = n;
+    const double eps = b.eps[p], h = b.h[p], H = b.H[p];
+    const double *c = b.c + b.xo[p], *r = b.r + b.xo[p];
     Buf1 l = layout_at(b.scratch + b.so[p], m, b.maxit);
-    b.bad[p] = setup1d_one(N, b.eps[p], b.h[p], b.H[p], b.c + b.xo[p], b.r + b.xo[p], l.aW, l.aE, l.rr, l.D,
-                           l.g, l.al, l.be);
+    double gprev = 0.0, supprev = 0.0;
+    int bad = 0;
+    for (int base = 0; base < m; base += 32) {
+        const int k = base + lane;
+        if (k < m) {
+            const int i = k + 1;
+            const double hi = i <= n ? h : H, hi1 = (i + 1) <= n ? h : H, hb = 0.5 * (hi + hi1);
+            const double cv = c[k], rv = r[k];
+            if (!(cv > 0.0) || !(rv >= 0.0) || !isfinite(cv) || !isfinite(rv)) bad = 1;
+            const double w = eps / (hb * hi), e = eps / (hb * hi1) + cv / hi1;
+            const double d = (w + e) + rv;
+            l.aW[k] = w; l.aE[k] = e; l.rr[k] = rv; l.D[k] = d;
+            sd[wq][0][lane] = d;
+            sd[wq][1][lane] = (i >= NL + 2 || k == 0) ? 0.0 : w;     // sub (eq:block_M)
+            sd[wq][2][lane] = (k == m - 1) ? 0.0 : e;                // sup
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const int cnt = min(32, m - base);
+            for (int t = 0; t < cnt; ++t) {
+                const double d = sd[wq][0][t], sub = sd[wq][1][t], sup = sd[wq][2][t];
+                const double den = (base + t == 0) ? d : d - sub * (supprev * gprev);
+                const double gk = 1.0 / den;
+                sd[wq][0][t] = gk; sd[wq][1][t] = sub * gk; sd[wq][2][t] = sup * gk;
+                gprev = gk; supprev = sup;
+            }
+        }
+        __syncwarp();
+        if (k < m) { l.g[k] = sd[wq][0][lane]; l.al[k] = sd[wq][1][lane]; l.be[k] = sd[wq][2][lane]; }
+        __syncwarp();
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) b.bad[p] = bad;
 }
 
 template <int K>
-__global__ void __launch_bounds__(512) k_solve1d_batch(Batch1Args b)
+__device__ __forceinline__ void solve1d_batch_body(const Batch1Args &b)
 {
     const int p = b.idx[blockIdx.x];
     const int m = b.n[p] - 1;
@@ -565,6 +605,9 @@ __global__ void __launch_bounds__(512) k_solve1d_batch(Batch1Args b)
         b.res0[p] = a.dout[0]; b.res[p] = a.dout[1];
     }
 }
+
+template <int K>
+__global__ void __launch_bounds__(512) k_solve1d_batch(Batch1Args b) { solve1d_batch_body<K>(b); }
 
 // launch shape of a problem with m unknowns: T threads, K rows per thread (as the single solve)
 static void shape1(int m, int *T_, int *K_)
@@ -641,7 +684,7 @@ cudaError_t batch1d_setup(Batch1 *b, const double *c, const double *r)
 {
     Batch1Args a = bargs(b);
     a.c = c; a.r = r;
-    k_setup1d_batch<<<(b->nprob + 127) / 128, 128, 0, b->st>>>(a);
+    k_setup1d_batch<<<(b->nprob + 3) / 4, 128, 0, b->st>>>(a);
     b->launches++;
     return cudaGetLastError();
 }
