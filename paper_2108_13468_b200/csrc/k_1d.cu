@@ -643,21 +643,24 @@ cudaError_t batch1d_alloc(Batch1 *b)
     const int P = b->nprob;
     b->xo.resize(P); b->so.resize(P);
     long long xo = 0, so = 0;
-    std::vector<std::tuple<int, int, int>> key(P);
+    std::vector<std::tuple<int, int, double, int>> key(P);
     for (int p = 0; p < P; ++p) {
         const int m = b->n[p] - 1;
         b->xo[p] = xo; b->so[p] = so;
         xo += m; so += (long long)need1(m, b->maxit);
         int T, K;
         shape1(m, &T, &K);
-        key[p] = std::make_tuple(K, T, p);
+        // within a launch shape, the problems most likely to need many iterations first (largest
+        // eps*N: outside the regime eps*N << 1 the counts grow), so that the long
+        // solves do not start at the end of the launch
+        key[p] = std::make_tuple(K, T, -b->eps[p] * b->n[p], p);
     }
     b->total = xo; b->scratch_len = so;
     std::sort(key.begin(), key.end());
     b->order.resize(P);
     for (int p = 0; p < P; ++p) {
         const int K = std::get<0>(key[p]), T = std::get<1>(key[p]);
-        b->order[p] = std::get<2>(key[p]);
+        b->order[p] = std::get<3>(key[p]);
         if (p == 0 || K != b->gK.back() || T != b->gT.back()) {
             b->gstart.push_back(p); b->gcount.push_back(0); b->gK.push_back(K); b->gT.push_back(T);
         }
