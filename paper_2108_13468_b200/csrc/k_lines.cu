@@ -480,12 +480,12 @@ __global__ void __launch_bounds__(256) k_lines_tma(LineChain cx, LineChain cy, c
         for (int k = 0; k < K; ++k) {
             zp[k] = zz[k];
             const int kk = k0 + k;
-            zs[kk + (kk >> 5)] = zz[k];                 // one pad per 32: conflict-light
+            zs[kk ^ ((kk >> 4) & 15)] = zz[k];          // XOR swizzle within 16: two-way on the stores, none on the reads
         }
         __syncthreads();
         if (l >= ck.first) {
             double *out = chain == 0 ? z + g0 : ysc + (long)l * len;
-            for (int kk = threadIdx.x; kk < len; kk += blockDim.x) out[kk] = zs[kk + (kk >> 5)];
+            for (int kk = threadIdx.x; kk < len; kk += blockDim.x) out[kk] = zs[kk ^ ((kk >> 4) & 15)];
         }
 #ifdef SPP_LINES_PROF
         LP(tf);
@@ -585,17 +585,20 @@ cudaError_t setup_lines(Ctx *c)
     return cudaStreamSynchronize(c->st);
 }
 
+// dynamic shared memory of k_lines_tma: 227 KB per block minus its static part (rounded up)
+constexpr int kLinesSmemMax = 227 * 1024 - 2048;
+
 // per-device kernel attributes (spp_create, on the context's device)
 cudaError_t lines_init()
 {
-    SPP_CUDA_TRY(cudaFuncSetAttribute(k_lines_tma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 2048));
-    SPP_CUDA_TRY(cudaFuncSetAttribute(k_lines_tma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 2048));
+    SPP_CUDA_TRY(cudaFuncSetAttribute(k_lines_tma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLinesSmemMax));
+    SPP_CUDA_TRY(cudaFuncSetAttribute(k_lines_tma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLinesSmemMax));
     return cudaSuccess;
 }
 
 static size_t lines_tma_smem(int len, int nst)
 {
-    return ((size_t)nst * 6 * len + len + len / 32 + 32) * sizeof(double) + 1024;   // stages + z staging
+    return ((size_t)nst * 6 * len + len) * sizeof(double) + 1024;   // stages + z staging (+ alignment)
 }
 
 // z (Y region) <- scratch: line l (column i = N-1-l), element k (row j = k+1); 32x32 tiles
@@ -620,8 +623,8 @@ static bool launch_lines_tma(Ctx *c, const double *v, double *z)
     const int len = c->n, T = c->lines_threads, K = (len + T - 1) / T;
     // 1 KB aligned boxes (the 128B swizzle phase) need len % 128 == 0
     if (len % 128 != 0 || len > 4096 || (K != 8 && K != 16) || T * K != len || c->no_lines_tma) return false;
-    const int nst = lines_tma_smem(len, 2) <= 227 * 1024 - 2048 ? 2 : 1;
-    if (lines_tma_smem(len, nst) > 227 * 1024 - 2048) return false;
+    const int nst = lines_tma_smem(len, 2) <= (size_t)kLinesSmemMax ? 2 : 1;   // len 4096: one stage (196 KB)
+    if (lines_tma_smem(len, nst) > (size_t)kLinesSmemMax) return false;
     const size_t sm = lines_tma_smem(len, nst);
     LineMaps m;
     const int nl = c->n - 1;
