@@ -444,13 +444,20 @@ __global__ void __launch_bounds__(256) k_lines_tma(LineChain cx, LineChain cy, c
             al[k] = a2.x; al[k + 1] = a2.y; be[k] = a3.x; be[k + 1] = a3.y;
         }
         const long g0 = ch.v0 + (long)l * ch.vline;
+        double *zs = sm + (size_t)nst * stage;          // z staging (free until the scans end)
         if (chain == 0) {
 #pragma unroll
             for (int k = 0; k < K; ++k) vv[k] = st[4 * len + swz16(k0 + k + 1)];
         } else {
+            // the strip holds (column pair) x rows: reading a thread's K consecutive rows
+            // directly would put every lane on one bank; repack the line's column through the
+            // z staging buffer (coalesced, XOR-swizzled within 16) first
             const int ic = (int)(g0 % P) & 1;
+            __syncthreads();                            // the previous line's stores from zs are done
+            for (int kk = threadIdx.x; kk < len; kk += blockDim.x) zs[kk ^ ((kk >> 4) & 15)] = st[4 * len + 2 * kk + ic];
+            __syncthreads();
 #pragma unroll
-            for (int k = 0; k < K; ++k) vv[k] = st[4 * len + 2 * (k0 + k) + ic];
+            for (int k = 0; k < K; ++k) vv[k] = zs[(k0 + k) ^ (((k0 + k) >> 4) & 15)];
         }
         const double tI = tnext;
         LP(tc);
@@ -475,7 +482,6 @@ __global__ void __launch_bounds__(256) k_lines_tma(LineChain cx, LineChain cy, c
         LP(te);
         // the line's results leave as coalesced segments through shared memory: X lines are row
         // segments of z, Y lines (columns of z) go line-major to the scratch (k_ysc_transpose)
-        double *zs = sm + (size_t)nst * stage;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             zp[k] = zz[k];
@@ -493,7 +499,7 @@ __global__ void __launch_bounds__(256) k_lines_tma(LineChain cx, LineChain cy, c
 #endif
     }
 #ifdef SPP_LINES_PROF
-    if ((threadIdx.x == 0 || threadIdx.x == 255) && (blockIdx.x == 0 || blockIdx.x == 70))
+    if ((threadIdx.x == 0 || threadIdx.x == 255) && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
         printf("[lines-prof] cta %d thr %d lines %d per line: wait %lld read %lld relsync %lld scans %lld store %lld\n",
                blockIdx.x, threadIdx.x, nlines, q0 / nlines, q1 / nlines, q2 / nlines, q3 / nlines, q4 / nlines);
 #endif
