@@ -64,3 +64,21 @@ def test_sweep_share_partitions_the_problems():
         flat = sorted(i for sh in shares for i in sh)
         assert flat == list(range(len(bench.CFG5_EPS)))
         assert max(len(sh) for sh in shares) == -(-len(bench.CFG5_EPS) // world)
+
+
+def test_batch1d_reference_arm_and_rank_slices():
+    """cfg1-batch: the reference arm (the oracle over a bounded sample) prints one line; each
+    rank's slice of the global problem sequence is disjoint and reproducible."""
+    sys.path.insert(0, ROOT)
+    import bench
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    p = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "cfg1-batch", "--batch", "32",
+                        "--steps", "1", "--warmup", "0"], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    d = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
+    e_all = bench.batch1d_inputs(64, 0)
+    e0, e1 = bench.batch1d_inputs(32, 0), bench.batch1d_inputs(32, 32)
+    assert (e_all[:32] == e0).all() and (e_all[32:] == e1).all()
+    assert (1e-8 <= e_all).all() and (e_all <= 1e-2).all()
