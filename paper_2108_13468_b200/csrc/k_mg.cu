@@ -56,7 +56,15 @@ constexpr int WBOX = 32 * WCW;   // doubles per box (4 KB)
 __host__ __device__ constexpr int wslot(bool yform) { return (yform ? WNA : WNA - 1) * WBOX; }
 constexpr int WMAXW = 5;         // sweeping warps per CTA (max; 5 only in z-form); +W write-back +1 TMA
 constexpr int WEB = 128;         // edge ring (columns)
-constexpr int WPF = 8;           // L2 prefetch distance (chunks)
+// L2 prefetch distance (chunks; 0 = none).  Measured: none is best -- at cfg5's 4096^2 level 0
+// the prefetched boxes of 129 tiles (8 chunks ahead: ~60 MB in flight) were evicted before use
+// (cfg5 41.0 -> 39.1 ms per solve without them, cfg4 20.66 -> 20.43 ms).  L2 eviction-priority
+// hints on the boxes (keep the certified halos, drop the rest) cut cfg4's level-0 DRAM traffic
+// from 188 to 138 MB per sweep but were slower (20.50 / 39.4 ms) and are not used.
+#ifndef SPP_WPF
+#define SPP_WPF 0
+#endif
+constexpr int WPF = SPP_WPF;
 constexpr int WLAG = 2;
 // timing experiments only (wrong results): compile with -DEXP_...
 #ifdef EXP_NOSPIN
@@ -183,7 +191,7 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
             tma_load(dst + WBOX * 8, &m.a1, x, R0, bar);
             tma_load(dst + 2 * WBOX * 8, &m.a2, x, R0, bar);
             if (YFORM) tma_load(dst + 3 * WBOX * 8, &m.cd, x, R0, bar);
-            if (c + WPF < nch) {
+            if (WPF > 0 && c + WPF < nch) {
                 const int xp = Xb - (c + WPF) * WCW;
                 tma_prefetch(&m.q, xp, R0); tma_prefetch(&m.a1, xp, R0); tma_prefetch(&m.a2, xp, R0);
                 if (YFORM) tma_prefetch(&m.cd, xp, R0);
