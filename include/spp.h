@@ -54,7 +54,10 @@ typedef enum {
     SPP_E_CUDA = -6,        /* CUDA runtime error, or no usable device                         */
     SPP_E_NCCL = -7,
     SPP_E_NOMEM = -8,       /* device or host allocation failed                                */
-    SPP_E_STATE = -9        /* call not valid in this context state                            */
+    SPP_E_STATE = -9,       /* call not valid in this context state                            */
+    SPP_E_NONFINITE = -10   /* NaN/Inf in the Krylov recurrence (beta or a Hessenberg entry):
+                               non-finite input data or a preconditioner blow-up (SURVEY 5
+                               "NaN/Inf guard on h_{k+1,k}"); outputs undefined               */
 } spp_status;
 
 typedef enum { SPP_HOST = 0, SPP_DEVICE = 1 } spp_mem;
@@ -91,7 +94,7 @@ typedef struct {
     spp_stop stop;
     double tol;
     int32_t max_iters;       /* Arnoldi steps (default 200)                           */
-    int32_t restart;         /* 0 = no restart (paper); other values reserved         */
+    int32_t restart;         /* must be 0: no restart (paper); other values SPP_E_ARG  */
     double mg_reduction;     /* corner MG relative reduction of ||S_0 rho||_2 (1e-3) */
     int32_t mg_max_cycles;   /* cycle cap (20)                                        */
     int32_t mg_fixed_cycles; /* 0 = adaptive (paper); > 0 = exactly this many (parity mode)  */
@@ -115,7 +118,11 @@ typedef struct {
 typedef struct spp_ctx spp_ctx;
 
 /* Defaults: right/flexible, SPP_STOP_REL_JACOBI, tol 1e-8, 200 iterations, MG 1e-3 / 20 /
- * adaptive / coarsest 4. */
+ * adaptive / coarsest 4.
+ * Option validation (spp_create, spp_create_dist, spp_batch1d_create return SPP_E_ARG):
+ * restart != 0; 2D with side = SPP_LEFT or stop = SPP_STOP_ABS_MAX; 1D with exactly one of
+ * side = SPP_LEFT / stop = SPP_STOP_ABS_MAX (the left GMRES of P:828-833 always stops on the
+ * true max-norm residual, and that stop exists only there); tol <= 0 or not finite. */
 SPP_API void spp_default_options(int32_t dim, spp_options *o);
 
 /* Shishkin mesh on the host (eq:tau 1D P:278-284 / eq:tau exponential P:914-928):

@@ -42,6 +42,7 @@
 #define ORC_E_ARG (-1)
 #define ORC_E_PIVOT (-4)
 #define ORC_E_NOMEM (-8)
+#define ORC_E_NONFINITE (-10)   /* NaN/Inf beta or Hessenberg entry (SURVEY 5 NaN/Inf guard) */
 
 /* ===================================================================================== */
 /*  Mesh                                                                                 */
@@ -245,6 +246,7 @@ int orc_fgmres(const orc_sys *s, const double *f, double *x, int weighted, int s
     for (size_t i = 0; i < n; i++) V[0][i] = weighted ? f[i] / s->D[i] : f[i];
     double beta = sqrt(dot(n, V[0], V[0]));
     st->res0 = beta;
+    if (!isfinite(beta)) { st->status = ORC_E_NONFINITE; goto done; }
     if (hist_cap > 0) hist[0] = beta;
     memset(x, 0, sizeof(double) * n);
     if (beta == 0.0) { st->converged = 1; st->res_final = 0.0; goto done; }
@@ -271,14 +273,17 @@ int orc_fgmres(const orc_sys *s, const double *f, double *x, int weighted, int s
         h[k + 1] = sqrt(dot(n, w, w));
         V[k + 1] = malloc(sizeof(double) * n);
         if (!V[k + 1]) { st->status = ORC_E_NOMEM; goto done; }
-        int brk = !(h[k + 1] > 0.0);
+        /* SURVEY 5 "NaN/Inf guard on h_{k+1,k}": a non-finite entry is a failure, and only an
+         * exact zero h_{k+1,k} is a (happy) breakdown */
+        for (int j = 0; j <= k + 1; j++) if (!isfinite(h[j])) { st->status = ORC_E_NONFINITE; goto done; }
+        int brk = h[k + 1] == 0.0;
         for (size_t i = 0; i < n; i++) V[k + 1][i] = brk ? 0.0 : w[i] / h[k + 1];
         apply_givens(h, cs, sn, g, k);
         double res = fabs(g[k + 1]);
         if (k + 1 < hist_cap) hist[k + 1] = res;
         st->iters = k + 1;
         st->res_final = res;
-        if (brk) { st->breakdown = 1; st->converged = 1; k++; break; }
+        if (brk) { st->breakdown = 1; st->converged = (res <= target); k++; break; }
         if (fixed_iters > 0) { if (k + 1 >= fixed_iters) { st->converged = (res <= target); k++; break; } }
         else if (res <= target) { st->converged = 1; k++; break; }
     }

@@ -144,6 +144,32 @@ def _ptr(a):
     return a.data_ptr(), (SPP_DEVICE if a.is_cuda else SPP_HOST), a
 
 
+def _where(a):
+    """Residency key of an array: 'host' or the CUDA device it lives on."""
+    if isinstance(a, np.ndarray) or not getattr(a, "is_cuda", False):
+        return "host"
+    return str(a.device)
+
+
+def _check_arrays(named, count):
+    """Every array must have exactly `count` float64 elements and all must share one residency
+    (host, or one CUDA device): the library trusts these sizes and the mem flag (spp.h)."""
+    where = None
+    for name, a in named:
+        if a is None:
+            continue
+        n = a.size if isinstance(a, np.ndarray) else a.numel()
+        if n != count:
+            raise ValueError(f"{name}: {n} elements, expected {count}")
+        if str(getattr(a, "dtype", "")) not in ("float64", "torch.float64"):
+            raise TypeError(f"{name}: dtype {a.dtype}, expected float64")
+        w = _where(a)
+        if where is None:
+            where = w
+        elif w != where:
+            raise ValueError(f"{name} lives on {w}, the other arrays on {where}: one residency per call")
+
+
 def _stream_handle(stream):
     if stream is None:
         try:
@@ -173,6 +199,9 @@ class Solver:
         self.opt = options if options is not None else spp_default_options(dim)
         self._x = np.ascontiguousarray(x, dtype=np.float64)
         self._y = None if y is None else np.ascontiguousarray(y, dtype=np.float64)
+        if self._x.size != n + 1 or (dim == 2 and (self._y is None or self._y.size != n + 1)):
+            raise ValueError(f"mesh coordinates: need {n + 1} values per axis")
+        _check_arrays([("c1", c1), ("c2", c2), ("r", r)], (n - 1) ** dim)
         p1, mem, k1 = _ptr(c1)
         p2, _, k2 = _ptr(c2)
         p3, _, k3 = _ptr(r)
@@ -201,6 +230,7 @@ class Solver:
         return self.n - 1
 
     def setup(self, c1, c2, r):
+        _check_arrays([("c1", c1), ("c2", c2), ("r", r)], self.m ** self.dim)
         p1, mem, k1 = _ptr(c1)
         p2, _, k2 = _ptr(c2)
         p3, _, k3 = _ptr(r)
@@ -214,6 +244,7 @@ class Solver:
             else:
                 import torch
                 u = torch.zeros_like(f)
+        _check_arrays([("f", f), ("u", u)], self.m ** self.dim)
         pu, memu, ku = _ptr(u)
         if memu != mem:
             raise ValueError("f and u must have the same residency")
@@ -275,6 +306,9 @@ class Batch1D:
         self._x = np.ascontiguousarray(x, dtype=np.float64)
         self.total = int(np.sum(self.n - 1))
         self.opt = options if options is not None else spp_default_options(1)
+        if self._x.size != int(np.sum(self.n + 1)) or self.eps.size != self.n.size:
+            raise ValueError("batch: x must hold sum(N_p + 1) coordinates and eps one value per problem")
+        _check_arrays([("c", c), ("r", r)], self.total)
         pc, mem, kc = _ptr(c)
         pr, _, kr = _ptr(r)
         h = _vp()
@@ -299,6 +333,7 @@ class Batch1D:
         return _lib.spp_batch1d_launches(self.h)
 
     def setup(self, c, r):
+        _check_arrays([("c", c), ("r", r)], self.total)
         pc, mem, kc = _ptr(c)
         pr, _, kr = _ptr(r)
         rc = _lib.spp_batch1d_setup(self.h, pc, pr, mem)
@@ -313,6 +348,7 @@ class Batch1D:
             else:
                 import torch
                 u = torch.zeros_like(f)
+        _check_arrays([("f", f), ("u", u)], self.total)
         pu, memu, ku = _ptr(u)
         if memu != mem:
             raise ValueError("f and u must have the same residency")

@@ -432,6 +432,21 @@ static void parse_tune(Ctx *c)
     }
 }
 
+// spp.h "Option validation": the combinations a dim does not implement are rejected, never
+// silently replaced by other stopping semantics.
+static spp_status check_options(const spp_options *o, int dim, Ctx *c)
+{
+    if (o->restart != 0) FAIL(c, SPP_E_ARG, "restart = %d: only restart = 0 (no restarts, P:831) is implemented", o->restart);
+    if (!(o->tol > 0.0) || !std::isfinite(o->tol)) FAIL(c, SPP_E_ARG, "tol must be finite and > 0");
+    if (o->side != SPP_RIGHT_FLEXIBLE && o->side != SPP_LEFT) FAIL(c, SPP_E_ARG, "unknown side %d", (int)o->side);
+    if ((int)o->stop < 0 || (int)o->stop > 3) FAIL(c, SPP_E_ARG, "unknown stop %d", (int)o->stop);
+    if (dim == 2 && (o->side == SPP_LEFT || o->stop == SPP_STOP_ABS_MAX))
+        FAIL(c, SPP_E_ARG, "2D solves are right/flexible FGMRES with a recurrence stop (SPP_LEFT / SPP_STOP_ABS_MAX are 1D only)");
+    if (dim == 1 && ((o->side == SPP_LEFT) != (o->stop == SPP_STOP_ABS_MAX)))
+        FAIL(c, SPP_E_ARG, "1D: side = SPP_LEFT goes with stop = SPP_STOP_ABS_MAX and only with it (P:828-833)");
+    return SPP_OK;
+}
+
 static spp_status check_mesh(const double *x, int N, double *tau, Ctx *c)
 {
     if (!x) FAIL(c, SPP_E_ARG, "mesh coordinates are NULL");
@@ -491,9 +506,9 @@ static spp_status alloc_all(Ctx *c)
         const char *yf = getenv("SPP_MG_YFORM");
         c->mg_zform = (yf && yf[0] == '1') ? 0 : 1;
     }
-    {   // exact chained sweep: one progress flag and one inflow row per CTA
-        const int W = std::max(1, std::min(c->tune.sweep_warps, 8));
-        const long ncta = (n + 32L * W - 1) / (32L * W) + 1;
+    {   // exact chained sweep: one progress flag and one inflow row per CTA (the launch's CTA
+        // count, wave_chain_ctas, plus one slot)
+        const long ncta = wave_chain_ctas(c, n) + 1;
         c->chain_ld = n + 32;
         CK(c, cudaMalloc(&c->chain, sizeof(double) * (size_t)(ncta * c->chain_ld)));
         CK(c, cudaMalloc(&c->chain_flags, sizeof(int) * (size_t)(ncta + 1)));
@@ -617,24 +632,33 @@ spp_status spp_setup(spp_ctx *cx, const double *c1, const double *c2, const doub
     return do_setup_2d(c, c1, c2, r, mem);
 }
 
-spp_status spp_create(const spp_problem *p, const spp_options *o, void *stream, spp_ctx **out)
+// Host-side validation of a problem + options and a fresh (unallocated) context with the mesh
+// widths set.  Everything here runs without a device, so argument errors are reported the same
+// way with or without a GPU.
+static spp_status ctx_new(const spp_problem *p, const spp_options *o, void *stream, Ctx **out)
 {
-    if (!p || !out) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_create: NULL argument");
     *out = nullptr;
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-        FAIL((Ctx *)nullptr, SPP_E_CUDA, "spp_create: no CUDA device (this library has no CPU path)");
     const int N = p->n;
     if (p->dim != 1 && p->dim != 2) FAIL((Ctx *)nullptr, SPP_E_ARG, "dim must be 1 or 2");
     if (N < 4 || (N % 2)) FAIL((Ctx *)nullptr, SPP_E_ARG, "N must be even and >= 4 (got %d)", N);
     if (p->dim == 2 && (N < 8 || ((N / 2) & (N / 2 - 1))))
         FAIL((Ctx *)nullptr, SPP_E_ARG, "2D needs N >= 8 with N/2 a power of two (got %d)", N);
     if (!(p->eps > 0.0) || p->eps > 1.0) FAIL((Ctx *)nullptr, SPP_E_ARG, "eps must be in (0,1]");
+    spp_options opt;
+    if (o) opt = *o; else spp_default_options(p->dim, &opt);
+    spp_status s = check_options(&opt, p->dim, nullptr);
+    if (s != SPP_OK) return s;
+    double tx = 0, ty = 0;
+    if ((s = check_mesh(p->x, N, &tx, nullptr)) != SPP_OK) return s;
+    if (p->dim == 2 && (s = check_mesh(p->y, N, &ty, nullptr)) != SPP_OK) return s;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        FAIL((Ctx *)nullptr, SPP_E_CUDA, "spp_create: no CUDA device (this library has no CPU path)");
     Ctx *c = new (std::nothrow) Ctx();
     if (!c) FAIL((Ctx *)nullptr, SPP_E_NOMEM, "host allocation failed");
     c->dim = p->dim; c->N = N; c->n = N / 2; c->m = N - 1; c->eps = p->eps;
     c->st = (cudaStream_t)stream;
-    if (o) c->opt = *o; else spp_default_options(p->dim, &c->opt);
+    c->opt = opt;
     if (c->opt.max_iters < 1) c->opt.max_iters = 1;
     if (c->opt.mg_max_cycles < 1) c->opt.mg_max_cycles = 20;
     if (!(c->opt.mg_reduction > 0.0)) c->opt.mg_reduction = 1e-3;
@@ -644,14 +668,21 @@ spp_status spp_create(const spp_problem *p, const spp_options *o, void *stream, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev);
     if (wave_init() != cudaSuccess || lines_init() != cudaSuccess) { delete c; FAIL((Ctx *)nullptr, SPP_E_CUDA, "kernel attribute setup failed"); }
-    spp_status s;
-    double tx = 0, ty = 0;
-    if ((s = check_mesh(p->x, N, &tx, c)) != SPP_OK) { g_err = c->err; delete c; return s; }
-    if (p->dim == 2 && (s = check_mesh(p->y, N, &ty, c)) != SPP_OK) { g_err = c->err; delete c; return s; }
     c->tx = tx; c->ty = ty;
     c->hx = tx / c->n; c->Hx = (1.0 - tx) / c->n;
     c->hy = ty / c->n; c->Hy = (1.0 - ty) / c->n;
     c->xh.assign(p->x, p->x + N + 1);
+    *out = c;
+    return SPP_OK;
+}
+
+spp_status spp_create(const spp_problem *p, const spp_options *o, void *stream, spp_ctx **out)
+{
+    if (!p || !out) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_create: NULL argument");
+    *out = nullptr;
+    Ctx *c = nullptr;
+    spp_status s = ctx_new(p, o, stream, &c);
+    if (s != SPP_OK) return s;
     if ((s = alloc_all(c)) != SPP_OK) { g_err = c->err; spp_destroy((spp_ctx *)c); return s; }
     if ((s = spp_setup((spp_ctx *)c, p->c1, p->c2, p->r, p->mem)) != SPP_OK) {
         g_err = c->err;
@@ -748,6 +779,7 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
     double bsq = 0;
     CK(c, fetch_sum(c, part_slot(c, 0), &bsq));
     const double beta = std::sqrt(bsq);
+    if (!std::isfinite(beta)) FAIL(c, SPP_E_NONFINITE, "||W f|| is not finite (NaN/Inf in the right-hand side)");
     std::vector<double> H((size_t)(maxit + 1) * (maxit + 1), 0.0), cs(maxit + 1), sn(maxit + 1),
         g(maxit + 2, 0.0), yv(maxit + 1);
     if (hist && hcap > 0) hist[0] = beta;
@@ -802,7 +834,13 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
                 mg_tot += cyc; mg_min = std::min(mg_min, cyc); mg_max = std::max(mg_max, cyc); caps += cap;
             }
             double *h = &H[(size_t)k * (maxit + 1)];
-            for (int j = 0; j <= k + 1; ++j) h[j] = c->hpin[j];
+            for (int j = 0; j <= k + 1; ++j) {
+                h[j] = c->hpin[j];
+                // SURVEY 5 "NaN/Inf guard on h_{k+1,k}": a non-finite Hessenberg entry is a
+                // failure (non-finite data or a preconditioner blow-up), never a breakdown
+                if (!std::isfinite(h[j]))
+                    FAIL(c, SPP_E_NONFINITE, "Hessenberg entry h(%d,%d) is not finite at iteration %d", j, k, k + 1);
+            }
             // Givens (Saad 2003)
             for (int i = 0; i < k; ++i) {
                 const double t = cs[i] * h[i] + sn[i] * h[i + 1];
@@ -812,7 +850,7 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
             const double den = std::hypot(h[k], h[k + 1]);
             if (den == 0.0) { cs[k] = 1.0; sn[k] = 0.0; }
             else { cs[k] = h[k] / den; sn[k] = h[k + 1] / den; }
-            const bool brk = !(h[k + 1] > 0.0);
+            const bool brk = h[k + 1] == 0.0;            // happy breakdown: w in span(V)
             h[k] = den; h[k + 1] = 0.0;
             g[k + 1] = -sn[k] * g[k];
             g[k] = cs[k] * g[k];
@@ -820,7 +858,7 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
             iters = k + 1;
             resf = res;
             if (hist && k + 1 < hcap) hist[k + 1] = res;
-            if (brk) { converged = 1; break; }
+            if (brk) { converged = res <= target; break; }
             if (c->opt.fixed_iters > 0) {
                 if (k + 1 >= c->opt.fixed_iters) { converged = res <= target; break; }
             } else if (res <= target) { converged = 1; break; }
@@ -1093,6 +1131,12 @@ spp_status spp_batch1d_create(int32_t nprob, const int32_t *n, const double *eps
 {
     if (!out || !n || !eps || !x || !c || !r || nprob < 1) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_batch1d_create: bad argument");
     *out = nullptr;
+    {
+        spp_options oc;
+        if (o) oc = *o; else spp_default_options(1, &oc);
+        const spp_status so = check_options(&oc, 1, nullptr);
+        if (so != SPP_OK) return so;
+    }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         FAIL((Ctx *)nullptr, SPP_E_CUDA, "spp_batch1d_create: no CUDA device (this library has no CPU path)");

@@ -537,19 +537,27 @@ void launch_wave(Ctx *c, WaveArgs a, long rows_v, long rows_c, int warps, bool y
     dbg_sync(c, "k_wave tiled");
 }
 
+static int chain_warps(const Ctx *c) { return std::max(1, std::min(c->tune.sweep_warps, WMAXW)); }
+// CTAs (row strips of 32 W rows) of an exact chained sweep over `rows` rows; the chain buffer is
+// sized from this (capi.cu alloc_all)
+long wave_chain_ctas(const Ctx *c, long rows) { const long r = 32L * chain_warps(c); return (rows + r - 1) / r; }
+
 // Exact sweep: row strips of 32*W rows chained top-to-bottom across CTAs (cooperative launch).
 void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform, int cls, double bytes)
 {
     WaveMaps m;
     if (!wave_maps(c, a, rows_v, rows_c, &m)) { c->sticky = cudaErrorInvalidValue; return; }
-    const int W = std::max(1, std::min(c->tune.sweep_warps, WMAXW));
+    const int W = chain_warps(c);
     a.rows_out = 32 * W; a.halo_y = 0;
     a.cols_out = a.nl; a.halo_x = 0;
-    const int ncta = (a.nl + a.rows_out - 1) / a.rows_out;
+    const int ncta = (int)wave_chain_ctas(c, a.nl);
     a.chain_flags = c->chain_flags;
     a.chain_buf = c->chain;
     a.chain_ld = c->chain_ld;
-    cudaMemsetAsync(c->chain, 0xff, sizeof(double) * (size_t)ncta * c->chain_ld, c->st);   // kChainSentinel
+    {
+        const cudaError_t e = cudaMemsetAsync(c->chain, 0xff, sizeof(double) * (size_t)ncta * c->chain_ld, c->st);   // kChainSentinel
+        if (e != cudaSuccess && c->sticky == cudaSuccess) c->sticky = e;
+    }
     const size_t sm = wave_smem(W, yform);
     void *args[] = {(void *)&a, (void *)&m};
     ProfScope ps(c, cls, bytes);
@@ -558,8 +566,10 @@ void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform,
     if (!prof) cudaMalloc(&prof, sizeof(long long) * 8 * 4 * 8192);
     a.prof = prof;
 #endif
-    if (yform) cudaLaunchCooperativeKernel((void *)k_wave<true, true>, dim3(1, ncta), dim3(32 * (2 * W + 1)), args, sm, c->st);
-    else cudaLaunchCooperativeKernel((void *)k_wave<false, true>, dim3(1, ncta), dim3(32 * (2 * W + 1)), args, sm, c->st);
+    const cudaError_t le = yform
+        ? cudaLaunchCooperativeKernel((void *)k_wave<true, true>, dim3(1, ncta), dim3(32 * (2 * W + 1)), args, sm, c->st)
+        : cudaLaunchCooperativeKernel((void *)k_wave<false, true>, dim3(1, ncta), dim3(32 * (2 * W + 1)), args, sm, c->st);
+    if (le != cudaSuccess && c->sticky == cudaSuccess) c->sticky = le;
     c->launches++;
 #ifdef SPP_WAVE_PROF
     wave_prof_dump(c, prof, "chain", ncta);

@@ -184,6 +184,7 @@ void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double
 void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, double *enew, const double *ec,
                bool bscaled = false);
 void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform, int cls, double bytes);
+long wave_chain_ctas(const Ctx *c, long rows);
 void launch_ycoef(Ctx *c, int nl, long pc, const double *aE, const double *aN, const double *cd, double *ya, double *yn);
 cudaError_t wave_init();
 cudaError_t lines_init();

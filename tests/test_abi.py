@@ -75,3 +75,48 @@ def test_batch1d_no_cpu_fallback_and_argument_checks():
     with pytest.raises(spp.SppError) as ei:
         spp.Batch1D([16], [1e-3], x, np.ones(15), np.ones(15))
     assert ei.value.code == -6
+
+
+def test_options_validated_before_any_device_work():
+    """spp.h "Option validation": unsupported option combinations are SPP_E_ARG (with or
+    without a GPU), never silently replaced by other stopping semantics."""
+    import paper_2108_13468_b200 as spp
+    x = spp.spp_shishkin_mesh(16, 1e-3)
+    ones = np.ones(225)
+
+    def opts(dim, **kw):
+        o = spp.spp_default_options(dim)
+        for k, v in kw.items():
+            setattr(o, k, v)
+        return o
+    bad2d = [opts(2, restart=10), opts(2, side=spp.SPP_LEFT), opts(2, stop=spp.SPP_STOP_ABS_MAX), opts(2, tol=0.0),
+             opts(2, tol=float("nan"))]
+    for o in bad2d:
+        with pytest.raises(spp.SppError) as ei:
+            spp.Solver(2, 16, 1e-3, x, x, ones, ones, ones, options=o)
+        assert ei.value.code == -1, spp._lib.spp_last_error(None)
+    bad1d = [opts(1, side=spp.SPP_LEFT), opts(1, stop=spp.SPP_STOP_ABS_MAX), opts(1, restart=5)]
+    for o in bad1d:
+        with pytest.raises(spp.SppError) as ei:
+            spp.Solver(1, 16, 1e-3, x, None, np.ones(15), None, np.ones(15), options=o)
+        assert ei.value.code == -1
+        with pytest.raises(spp.SppError) as ei:
+            spp.Batch1D([16], [1e-3], x, np.ones(15), np.ones(15), options=o)
+        assert ei.value.code == -1
+
+
+def test_binding_checks_sizes_dtypes_and_residency():
+    import paper_2108_13468_b200 as spp
+    x = spp.spp_shishkin_mesh(16, 1e-3)
+    ones = np.ones(225)
+    with pytest.raises(ValueError):
+        spp.Solver(2, 16, 1e-3, x, x, ones, ones, np.ones(224))
+    with pytest.raises(TypeError):
+        spp.Solver(2, 16, 1e-3, x, x, ones, ones, np.ones(225, dtype=np.float32))
+    with pytest.raises(ValueError):
+        spp.Solver(2, 16, 1e-3, x[:-1], x, ones, ones, ones)
+    with pytest.raises(ValueError):
+        spp.Batch1D([16], [1e-3], x, np.ones(14), np.ones(15))
+    import torch
+    with pytest.raises(ValueError):   # a host tensor and numpy arrays are one residency; sizes still checked
+        spp.Solver(2, 16, 1e-3, x, x, torch.ones(224, dtype=torch.float64), ones, ones)

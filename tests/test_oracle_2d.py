@@ -334,3 +334,23 @@ def test_baseline_iteration_counts_small_eps_robust():
             cfg, x, y, (c1, c2, r, f), P = _mk("cfg4", N, eps)
             its.append(P.solve(f, weighted=1, tol=1e-8, maxit=100)["iters"])
     assert max(its) - min(its) <= 1 and max(its) <= 4
+
+
+def test_fgmres_nonfinite_guard():
+    """SURVEY 5 "NaN/Inf guard on h_{k+1,k}": a NaN right-hand side is an error (rc -10), not a
+    breakdown reported as convergence."""
+    import pytest
+    N, eps = 16, 1e-3
+    x = oracle.mesh(N, eps)
+    m = N - 1
+    P = oracle.Oracle2D(N, eps, x, x, np.ones(m * m), np.ones(m * m), np.ones(m * m))
+    f = np.ones(m * m)
+    f[7] = np.nan
+    with pytest.raises(RuntimeError, match="rc=-10"):
+        P.solve(f, weighted=1, tol=1e-8)
+    f[7] = np.inf
+    with pytest.raises(RuntimeError, match="rc=-10"):
+        P.solve(f, weighted=0, tol=1e-8)
+    # an exact zero rhs is not an error: x = 0 after zero iterations
+    res = P.solve(np.zeros(m * m), weighted=1, tol=1e-8)
+    assert res["iters"] == 0 and res["converged"]
