@@ -222,6 +222,53 @@ SPP_API int64_t spp_batch1d_launches(const spp_batch1d *b);
 SPP_API const char *spp_batch1d_last_error(const spp_batch1d *b);
 SPP_API void spp_batch1d_destroy(spp_batch1d *b);
 
+/* ---- Row strips across GPUs --------------------------------------
+ * A 2D problem split into row strips: strip r owns the interior rows [J[r], J[r+1]) of every grid
+ * function (J[0] = 1, J[P] = N), with one strip boundary at row N/2+1 (the X/I | C/Y split of
+ * eq:2D blocks).  The solve computes the same method as spp_create/spp_solve (same
+ * iterations and corner cycles; results equal to rounding): halos of one row for
+ * the stencil, the certified warm-up / smoothing halos of the strip above for the line chains
+ * and the corner multigrid strips, the exact M_II sweep relayed strip to strip, the vertical
+ * M_YY lines solved as column blocks, and every dot product as all-gathered per-strip partial
+ * sums.  spp_setup / spp_solve / spp_destroy take a strip context like any other;
+ * spp_apply_stage returns SPP_E_STATE for it.
+ *
+ * spp_strip_partition: the default J (host, nranks+1 entries): ceil(P/2) strips share rows
+ *   1..N/2 and the others rows N/2+1..N-1, evenly.  SPP_E_ARG if they do not fit.
+ * spp_create_strips: nstrips strips of a whole problem on the calling device with a loopback
+ *   transport (device copies between the strips' buffers): the decomposition's own test and
+ *   validation mode.  p and spp_solve's f / u are whole ((N-1)^2 compact).  nstrips = 1 is
+ *   spp_create.
+ * spp_create_dist: one strip per process (one GPU each), NCCL over `nccl_comm` (an ncclComm_t of
+ *   nranks ranks, rank = this process; see spp_nccl_*).  local->c1, c2, r and spp_solve's f / u
+ *   hold this rank's rows j0 .. j1-1 only ((j1-j0)(N-1) compact values, row j0 first); x, y are
+ *   the whole meshes.  Every rank must pass its own [j0, j1): they must tile 1..N-1 in rank order
+ *   with a boundary at N/2+1 (SPP_E_ARG otherwise).  Collective: every rank calls it, and every
+ *   later spp_setup / spp_solve, in the same order.  The caller keeps the communicator alive
+ *   until spp_destroy.  SPP_E_NCCL if NCCL cannot be loaded or fails.
+ * spp_nccl_unique_id / spp_nccl_comm_create / spp_nccl_comm_destroy: an NCCL communicator for
+ *   spp_create_dist (rank 0 makes the 128-byte id, the caller broadcasts it, every rank
+ *   creates).  NCCL is loaded at run time (SPP_NCCL_LIB, else the libnccl.so.2 in the process).
+ * spp_dist_info: ranks, corner levels smoothed on strips, and the transfers / bytes / exchange
+ *   steps this rank took part in since create (1, 0, 0 ... for a one-GPU context).
+ * spp_dist_plan: host-only exchange schedule of one FGMRES iteration for a synthetic geometry
+ *   (partition j, D strip levels of certified halo `halo`, line warm-up `warm`): 11 int64 per
+ *   block (step, src, dst, role, slot, src offset, dst offset, width, rows, pitch, 0) for the
+ *   blocks `rank` sends or receives (rank < 0: all), at most cap written; returns the count or
+ *   SPP_E_ARG.  For testing the multi-process orchestration without GPUs. */
+SPP_API spp_status spp_strip_partition(int32_t n, int32_t nranks, int32_t *j);
+SPP_API spp_status spp_create_strips(const spp_problem *p, int32_t nstrips, const spp_options *o, void *cuda_stream,
+                                     spp_ctx **out);
+SPP_API spp_status spp_create_dist(const spp_problem *local, int32_t j0, int32_t j1, void *nccl_comm, int32_t rank,
+                                   int32_t nranks, const spp_options *o, void *cuda_stream, spp_ctx **out);
+SPP_API spp_status spp_nccl_unique_id(uint8_t *id);
+SPP_API spp_status spp_nccl_comm_create(const uint8_t *id, int32_t nranks, int32_t rank, void **comm);
+SPP_API void spp_nccl_comm_destroy(void *comm);
+SPP_API spp_status spp_dist_info(const spp_ctx *c, int32_t *nranks, int32_t *strip_levels, int64_t *xfers,
+                                 double *bytes, int64_t *exchanges);
+SPP_API int32_t spp_dist_plan(int32_t n, int32_t nranks, const int32_t *j, int32_t d_levels, int32_t halo, int32_t warm,
+                              int32_t rank, int64_t *out, int32_t cap);
+
 /* Last error message for this context (or the thread-local one when c == NULL). */
 SPP_API const char *spp_last_error(const spp_ctx *c);
 

@@ -59,7 +59,9 @@ ABI_FUNCTIONS = ["spp_default_options", "spp_shishkin_mesh", "spp_create", "spp_
                  "spp_profile_enable", "spp_profile_reset", "spp_profile_get", "spp_profile_name",
                  "spp_destroy", "spp_last_error", "spp_version",
                  "spp_batch1d_create", "spp_batch1d_setup", "spp_batch1d_solve", "spp_batch1d_nprob", "spp_batch1d_launches",
-                 "spp_batch1d_last_error", "spp_batch1d_destroy"]
+                 "spp_batch1d_last_error", "spp_batch1d_destroy",
+                 "spp_strip_partition", "spp_create_strips", "spp_create_dist", "spp_nccl_unique_id",
+                 "spp_nccl_comm_create", "spp_nccl_comm_destroy", "spp_dist_info", "spp_dist_plan"]
 
 if not LIB_PATH.exists():
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
@@ -101,12 +103,32 @@ _lib.spp_batch1d_last_error.argtypes = [_vp]
 _lib.spp_batch1d_last_error.restype = ctypes.c_char_p
 _lib.spp_batch1d_destroy.argtypes = [_vp]
 _lib.spp_batch1d_destroy.restype = None
+_lib.spp_strip_partition.argtypes = [ctypes.c_int32, ctypes.c_int32, _ip]
+_lib.spp_create_strips.argtypes = [ctypes.POINTER(spp_problem), ctypes.c_int32, ctypes.POINTER(spp_options), _vp,
+                                   ctypes.POINTER(_vp)]
+_lib.spp_create_dist.argtypes = [ctypes.POINTER(spp_problem), ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_int32,
+                                 ctypes.c_int32, ctypes.POINTER(spp_options), _vp, ctypes.POINTER(_vp)]
+_lib.spp_nccl_unique_id.argtypes = [ctypes.c_char_p]
+_lib.spp_nccl_comm_create.argtypes = [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_vp)]
+_lib.spp_nccl_comm_destroy.argtypes = [_vp]
+_lib.spp_nccl_comm_destroy.restype = None
+_lib.spp_dist_info.argtypes = [_vp, _ip, _ip, ctypes.POINTER(ctypes.c_int64), _dp, ctypes.POINTER(ctypes.c_int64)]
+_lib.spp_dist_plan.argtypes = [ctypes.c_int32, ctypes.c_int32, _ip, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                               ctypes.c_int32, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32]
 
 
 class SppError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"spp error {code}: {msg}")
         self.code = code
+
+
+class SppArgError(SppError, ValueError, TypeError):
+    """An argument the binding rejects before calling the library (sizes, dtypes, residency):
+    SPP_E_ARG, as the library would report it."""
+
+    def __init__(self, msg):
+        super().__init__(-1, msg)
 
 
 def _check(rc, ctx=None):
@@ -123,6 +145,56 @@ def spp_default_options(dim: int) -> spp_options:
     o = spp_options()
     _lib.spp_default_options(dim, ctypes.byref(o))
     return o
+
+
+def spp_strip_partition(n: int, nranks: int) -> np.ndarray:
+    """Default row strips (spp.h): rank r owns interior rows J[r] .. J[r+1]-1."""
+    j = np.zeros(nranks + 1, np.int32)
+    _check(_lib.spp_strip_partition(n, nranks, j.ctypes.data_as(_ip)))
+    return j
+
+
+def spp_dist_plan(n: int, nranks: int, j, d_levels: int, halo: int, warm: int, rank: int = -1) -> np.ndarray:
+    """Host-only exchange schedule of one FGMRES iteration (spp.h): rows of
+    (step, src, dst, role, slot, soff, doff, width, rows, pitch, 0)."""
+    j = np.ascontiguousarray(j, dtype=np.int32)
+    cnt = _check(_lib.spp_dist_plan(n, nranks, j.ctypes.data_as(_ip), d_levels, halo, warm, rank, None, 0))
+    out = np.zeros((max(cnt, 1), 11), np.int64)
+    _lib.spp_dist_plan(n, nranks, j.ctypes.data_as(_ip), d_levels, halo, warm, rank,
+                       out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), cnt)
+    return out[:cnt]
+
+
+def nccl_unique_id() -> bytes:
+    _nccl_env()
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.spp_nccl_unique_id(buf))
+    return buf.raw
+
+
+def nccl_comm_create(uid: bytes, nranks: int, rank: int):
+    _nccl_env()
+    h = _vp()
+    _check(_lib.spp_nccl_comm_create(uid, nranks, rank, ctypes.byref(h)))
+    return h
+
+
+def nccl_comm_destroy(comm):
+    _lib.spp_nccl_comm_destroy(comm)
+
+
+def _nccl_env():
+    """Point the library at the libnccl torch uses (one NCCL per process)."""
+    import os
+    if os.environ.get("SPP_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl
+        cand = Path(list(nvidia.nccl.__path__)[0]) / "lib" / "libnccl.so.2"
+        if cand.exists():
+            os.environ["SPP_NCCL_LIB"] = str(cand)
+    except Exception:
+        pass
 
 
 def spp_shishkin_mesh(n: int, eps: float, sigma: float = 2.0, beta: float = 1.0) -> np.ndarray:
@@ -160,14 +232,14 @@ def _check_arrays(named, count):
             continue
         n = a.size if isinstance(a, np.ndarray) else a.numel()
         if n != count:
-            raise ValueError(f"{name}: {n} elements, expected {count}")
+            raise SppArgError(f"{name}: {n} elements, expected {count}")
         if str(getattr(a, "dtype", "")) not in ("float64", "torch.float64"):
-            raise TypeError(f"{name}: dtype {a.dtype}, expected float64")
+            raise SppArgError(f"{name}: dtype {a.dtype}, expected float64")
         w = _where(a)
         if where is None:
             where = w
         elif w != where:
-            raise ValueError(f"{name} lives on {w}, the other arrays on {where}: one residency per call")
+            raise SppArgError(f"{name} lives on {w}, the other arrays on {where}: one residency per call")
 
 
 def _stream_handle(stream):
@@ -194,13 +266,14 @@ class Solver:
     """One spp_ctx.  Coefficients/right-hand sides may be numpy arrays (host) or torch CUDA
     float64 tensors (device), in the compact layout (N-1)^dim, x fastest."""
 
-    def __init__(self, dim, n, eps, x, y, c1, c2, r, options: spp_options | None = None, stream=None):
+    def __init__(self, dim, n, eps, x, y, c1, c2, r, options: spp_options | None = None, stream=None, strips=1):
+        """strips > 1: the row-strip decomposition (spp_create_strips) on this device."""
         self.dim, self.n, self.eps = dim, n, eps
         self.opt = options if options is not None else spp_default_options(dim)
         self._x = np.ascontiguousarray(x, dtype=np.float64)
         self._y = None if y is None else np.ascontiguousarray(y, dtype=np.float64)
         if self._x.size != n + 1 or (dim == 2 and (self._y is None or self._y.size != n + 1)):
-            raise ValueError(f"mesh coordinates: need {n + 1} values per axis")
+            raise SppArgError(f"mesh coordinates: need {n + 1} values per axis")
         _check_arrays([("c1", c1), ("c2", c2), ("r", r)], (n - 1) ** dim)
         p1, mem, k1 = _ptr(c1)
         p2, _, k2 = _ptr(c2)
@@ -209,7 +282,10 @@ class Solver:
                            p1, p2, p3, mem)
         h = _vp()
         self._stream = _stream_handle(stream)
-        rc = _lib.spp_create(ctypes.byref(prob), ctypes.byref(self.opt), self._stream, ctypes.byref(h))
+        if strips > 1:
+            rc = _lib.spp_create_strips(ctypes.byref(prob), strips, ctypes.byref(self.opt), self._stream, ctypes.byref(h))
+        else:
+            rc = _lib.spp_create(ctypes.byref(prob), ctypes.byref(self.opt), self._stream, ctypes.byref(h))
         _check(rc)
         self.h = h
         self._keep = (k1, k2, k3)
@@ -276,6 +352,13 @@ class Solver:
     def profile_reset(self):
         _check(_lib.spp_profile_reset(self.h), self.h)
 
+    def dist_info(self):
+        nr, dl = ctypes.c_int32(), ctypes.c_int32()
+        nx, ne, by = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
+        _check(_lib.spp_dist_info(self.h, ctypes.byref(nr), ctypes.byref(dl), ctypes.byref(nx), ctypes.byref(by),
+                                  ctypes.byref(ne)), self.h)
+        return dict(nranks=nr.value, strip_levels=dl.value, xfers=nx.value, bytes=by.value, exchanges=ne.value)
+
     def profile(self):
         out = {}
         for k in range(PROF_CLASSES):
@@ -307,7 +390,7 @@ class Batch1D:
         self.total = int(np.sum(self.n - 1))
         self.opt = options if options is not None else spp_default_options(1)
         if self._x.size != int(np.sum(self.n + 1)) or self.eps.size != self.n.size:
-            raise ValueError("batch: x must hold sum(N_p + 1) coordinates and eps one value per problem")
+            raise SppArgError("batch: x must hold sum(N_p + 1) coordinates and eps one value per problem")
         _check_arrays([("c", c), ("r", r)], self.total)
         pc, mem, kc = _ptr(c)
         pr, _, kr = _ptr(r)
@@ -361,3 +444,57 @@ class Batch1D:
             raise SppError(rc, (_lib.spp_batch1d_last_error(self.h) or b"").decode())
         return BatchResult(u=ku if mem == SPP_HOST else u, iters=it, converged=cv.astype(bool), res=res,
                            status=rc, stats=st.asdict())
+
+
+class DistSolver(Solver):
+    """One row strip of a 2D problem per process (spp_create_dist): c1, c2, r (and f, u at
+    solve) hold this rank's interior rows j0 .. j1-1 only; x, y are the whole meshes; comm is an
+    NCCL communicator handle (nccl_comm_create).  Collective: every rank constructs and solves
+    in the same order."""
+
+    def __init__(self, n, eps, x, y, c1, c2, r, j0, j1, comm, rank, nranks, options: spp_options | None = None,
+                 stream=None):
+        _nccl_env()
+        self.dim, self.n, self.eps, self.j0, self.j1 = 2, n, eps, j0, j1
+        self.opt = options if options is not None else spp_default_options(2)
+        self._x = np.ascontiguousarray(x, dtype=np.float64)
+        self._y = np.ascontiguousarray(y, dtype=np.float64)
+        if self._x.size != n + 1 or self._y.size != n + 1:
+            raise SppArgError(f"mesh coordinates: need {n + 1} values per axis")
+        _check_arrays([("c1", c1), ("c2", c2), ("r", r)], (j1 - j0) * (n - 1))
+        p1, mem, k1 = _ptr(c1)
+        p2, _, k2 = _ptr(c2)
+        p3, _, k3 = _ptr(r)
+        prob = spp_problem(2, n, eps, self._x.ctypes.data, self._y.ctypes.data, p1, p2, p3, mem)
+        h = _vp()
+        self._stream = _stream_handle(stream)
+        _check(_lib.spp_create_dist(ctypes.byref(prob), j0, j1, comm, rank, nranks, ctypes.byref(self.opt), self._stream,
+                                    ctypes.byref(h)))
+        self.h = h
+        self._keep = (k1, k2, k3)
+
+    def setup(self, c1, c2, r):
+        _check_arrays([("c1", c1), ("c2", c2), ("r", r)], (self.j1 - self.j0) * (self.n - 1))
+        p1, mem, k1 = _ptr(c1)
+        p2, _, k2 = _ptr(c2)
+        p3, _, k3 = _ptr(r)
+        _check(_lib.spp_setup(self.h, p1, p2, p3, mem), self.h)
+
+    def solve(self, f, u=None, hist_cap=256) -> SolveResult:
+        cnt = (self.j1 - self.j0) * (self.n - 1)
+        pf, mem, kf = _ptr(f)
+        if u is None:
+            if mem == SPP_HOST:
+                u = np.zeros(cnt)
+            else:
+                import torch
+                u = torch.zeros_like(f)
+        _check_arrays([("f", f), ("u", u)], cnt)
+        pu, memu, ku = _ptr(u)
+        if memu != mem:
+            raise ValueError("f and u must have the same residency")
+        hist = np.zeros(hist_cap)
+        st = spp_stats()
+        rc = _check(_lib.spp_solve(self.h, pf, pu, mem, hist.ctypes.data_as(_dp), hist_cap, ctypes.byref(st)), self.h)
+        d = st.asdict()
+        return SolveResult(u=ku if mem == SPP_HOST else u, hist=hist[: d["iters"] + 1].copy(), status=rc, stats=d)

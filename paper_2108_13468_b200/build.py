@@ -10,8 +10,10 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 SRC = PKG / "csrc"
 LIB = PKG / "lib" / "libspp.so"
-SOURCES = ["capi.cu", "k_core.cu", "k_lines.cu", "k_1d.cu", "k_mg.cu"]
+SOURCES = ["capi.cu", "k_core.cu", "k_lines.cu", "k_1d.cu", "k_mg.cu", "dist.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+# <nccl.h> (system include path) for the types only: the library resolves NCCL at run time
+# (dlopen), so libspp.so has no link dependency on it
 FLAGS = [*(["-DSPP_WAVE_PROF"] if os.environ.get("SPP_WAVE_PROF") else []),
     *(["-DSPP_LINES_PROF"] if os.environ.get("SPP_LINES_PROF") else []),
     *(["-DSPP_COARSE_PROF"] if os.environ.get("SPP_COARSE_PROF") else []),
@@ -42,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs.append(str(o))
     tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(tmp), *objs,
-           "-Xcompiler", "-fPIC", "-cudart", "static"]
+           "-Xcompiler", "-fPIC", "-cudart", "static", "-ldl"]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     for o in objs:

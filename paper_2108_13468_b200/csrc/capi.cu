@@ -10,6 +10,7 @@
 #include <cstring>
 #include <new>
 
+#include "dist.cuh"
 #include "kernels.cuh"
 
 using namespace spp;
@@ -102,7 +103,7 @@ static cudaError_t fetch_sum(Ctx *c, const double *part, double *out)
     return cudaSuccess;
 }
 
-static double *part_slot(Ctx *c, int k) { return c->part + (size_t)k * kRedBlocks; }
+static double *part_slot(Ctx *c, int k) { return c->part + (size_t)k * c->nparts * kRedBlocks; }
 
 // ------------------------------------------------------------------------------------------ corner MG
 // V(1,1) cycle for A_l e = R, zero initial guess ("standard V(1,1) cycling", one
@@ -110,7 +111,7 @@ static double *part_slot(Ctx *c, int k) { return c->part + (size_t)k * kRedBlock
 // P:1208-1209 / P:1281-1283).  Returns the buffer holding e (lev[l].e or lev[l].q).
 // rs: R holds R / D (the z-form V-cycle stores every level's right-hand side divided by D; the
 // caller's R may be plain, e.g. the test hooks).
-static double *vcycle(Ctx *c, int l, const double *R, bool rs)
+double *vcycle(Ctx *c, int l, const double *R, bool rs)
 {
     Level &L = c->lev[l];
     const bool zf = c->mg_zform;
@@ -331,12 +332,12 @@ static int apply_precond(Ctx *c, const double *v, double *z, int *cap_hit, cudaE
         ProfScope ps(c, 9, 40.0 * (double)n * n);
         k_corner_rhs<<<red_grid((long)n * n), kRedThreads, 0, c->st>>>(N, c->P, L0.pitch, v, z, c->aE, c->aN, c->rr, c->aW,
                                                             c->aS, L0.hb, L0.kb, c->weighted, c->Bc, part_slot(c, 1),
-                                                            L0.rho, c->cd, c->mg_zform);
+                                                            L0.rho, c->cd, c->mg_zform, 1, n);
         c->launches++;
     }
     if (gm) {                                           // cycles known after the caller's next sync
         *err = corner_solve_graph(c);
-        k_corner_out<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, nullptr, c->P, z, c->mgs);
+        k_corner_out<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, nullptr, c->P, z, c->mgs, 1, n);
         c->launches++;
         return -1;
     }
@@ -351,7 +352,7 @@ static int apply_precond(Ctx *c, const double *v, double *z, int *cap_hit, cudaE
         *err = cudaMemsetAsync(c->Zc, 0, sizeof(double) * L0.elems, c->st);
         zc = c->Zc;
     }
-    k_corner_out<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, zc, c->P, z, nullptr);
+    k_corner_out<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, zc, c->P, z, nullptr, 1, n);
     c->launches++;
     return cyc;
 }
@@ -427,6 +428,7 @@ static void parse_tune(Ctx *c)
             else if (k == "sweep_warps") c->tune.sweep_warps = v;
             else if (k == "coarse_max") c->tune.coarse_max = v;
             else if (k == "gs_lag") c->tune.gs_lag = v;
+            else if (k == "dist_levels") c->tune.dist_levels = v;
         }
         pos = end + 1;
     }
@@ -490,9 +492,10 @@ static spp_status alloc_all(Ctx *c)
     CK(c, cudaMemsetAsync(c->w, 0, sizeof(double) * (4 * G + kTmaSlack), c->st));
     c->F = c->w + G; c->U = c->F + G; c->T1 = c->U + G;
     const int maxit = c->opt.max_iters;
-    CK(c, cudaMalloc(&c->part, sizeof(double) * (size_t)(std::max(maxit, kMaxLevels) + 8) * kRedBlocks));
+    // reduction partials: one kRedBlocks segment per strip (nparts) in every slot
+    CK(c, cudaMalloc(&c->part, sizeof(double) * (size_t)(std::max(maxit, kMaxLevels) + 8) * kRedBlocks * c->nparts));
     CK(c, cudaMalloc(&c->dscal, sizeof(double) * (size_t)(3 * maxit + 64)));
-    CK(c, cudaMallocHost(&c->hpin, sizeof(double) * std::max<size_t>(4 * kRedBlocks + 3 * (size_t)maxit + 64,
+    CK(c, cudaMallocHost(&c->hpin, sizeof(double) * std::max<size_t>(8 * (size_t)kRedBlocks * c->nparts + 4 * (size_t)maxit + 64,
                                                                       (size_t)kMaxLevels * kRedBlocks)));
     CK(c, cudaMalloc(&c->flags, sizeof(int) * 256));
     CK(c, cudaMemsetAsync(c->flags, 0, sizeof(int) * 256, c->st));
@@ -507,8 +510,8 @@ static spp_status alloc_all(Ctx *c)
         c->mg_zform = (yf && yf[0] == '1') ? 0 : 1;
     }
     {   // exact chained sweep: one progress flag and one inflow row per CTA (the launch's CTA
-        // count, wave_chain_ctas, plus one slot)
-        const long ncta = wave_chain_ctas(c, n) + 1;
+        // count, wave_chain_ctas), plus the inflow slot of a row strip's chain
+        const long ncta = wave_chain_ctas(c, n) + 2;
         c->chain_ld = n + 32;
         CK(c, cudaMalloc(&c->chain, sizeof(double) * (size_t)(ncta * c->chain_ld)));
         CK(c, cudaMalloc(&c->chain_flags, sizeof(int) * (size_t)(ncta + 1)));
@@ -522,6 +525,7 @@ static spp_status alloc_all(Ctx *c)
     for (int l = 0; l < L; ++l) {
         Level &Lv = c->lev[l];
         Lv.n = n >> l;
+        Lv.slo = 1; Lv.shi = Lv.n; Lv.shalo = 0; Lv.sdist = false;
         Lv.pitch = round_up(Lv.n + 2, 16);
         Lv.elems = (size_t)(Lv.n + 2) * Lv.pitch;
         tot += 5 * Lv.elems + 4 * (size_t)(Lv.n + 2) + (l > 0 ? 6 * Lv.elems : 0);
@@ -553,7 +557,9 @@ static spp_status alloc_all(Ctx *c)
     return SPP_OK;
 }
 
-static cudaError_t ensure_vectors(Ctx *c, int k)
+}  // extern "C"
+namespace spp {
+cudaError_t ensure_vectors(Ctx *c, int k)
 {
     // V[0..k], Z[0..k-1]
     while ((int)c->V.size() <= k) {
@@ -575,7 +581,7 @@ static cudaError_t ensure_vectors(Ctx *c, int k)
     return cudaSuccess;
 }
 
-static spp_status do_setup_2d(Ctx *c, const double *c1, const double *c2, const double *r, spp_mem mem)
+spp_status setup_2d_ctx(Ctx *c, const double *c1, const double *c2, const double *r, spp_mem mem)
 {
     const int N = c->N, m = c->m;
     const size_t mm = (size_t)m * m;
@@ -623,13 +629,17 @@ static spp_status do_setup_2d(Ctx *c, const double *c1, const double *c2, const 
     return SPP_OK;
 }
 
+}  // namespace spp
+extern "C" {
+
 spp_status spp_setup(spp_ctx *cx, const double *c1, const double *c2, const double *r, spp_mem mem)
 {
     Ctx *c = (Ctx *)cx;
     if (!c) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_setup: NULL context");
     if (!c1 || !r || (c->dim == 2 && !c2)) FAIL(c, SPP_E_ARG, "spp_setup: NULL coefficient array");
     if (c->dim == 1) return (spp_status)setup_1d(c, c1, r, mem);
-    return do_setup_2d(c, c1, c2, r, mem);
+    if (c->dist) return setup_dist(c, c1, c2, r, mem);
+    return setup_2d_ctx(c, c1, c2, r, mem);
 }
 
 // Host-side validation of a problem + options and a fresh (unallocated) context with the mesh
@@ -693,10 +703,24 @@ spp_status spp_create(const spp_problem *p, const spp_options *o, void *stream, 
     return SPP_OK;
 }
 
+static void ctx_free(Ctx *c);
 void spp_destroy(spp_ctx *cx)
 {
     Ctx *c = (Ctx *)cx;
     if (!c) return;
+    if (c->dist) {                                      // row strips: every local strip, then the decomposition
+        Dist *d = c->dist;
+        std::vector<Ctx *> all = d->cx;
+        if (d->st) cudaStreamSynchronize(d->st);
+        destroy_dist(c);
+        for (Ctx *x : all) { x->dist = nullptr; ctx_free(x); }
+        return;
+    }
+    ctx_free(c);
+}
+
+static void ctx_free(Ctx *c)
+{
     if (c->st) cudaStreamSynchronize(c->st); else cudaDeviceSynchronize();
     for (double *p : c->V) cudaFree(p);
     for (double *p : c->Z) cudaFree(p);
@@ -764,7 +788,7 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
         CK(c, cudaMemcpyAsync(c->cbuf, f, sizeof(double) * mm, cudaMemcpyHostToDevice, c->st));
         fd = c->cbuf;
     }
-    k_pack<<<nblk((long)mm), 256, 0, c->st>>>(m, c->P, fd, c->F);
+    k_pack<<<nblk((long)mm), 256, 0, c->st>>>(m, c->P, fd, c->F, 1, m);
     c->launches++;
     CK(c, ensure_vectors(c, 1));
     const int weighted = c->weighted;
@@ -773,7 +797,7 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
     {
         ProfScope ps(c, 7, 48.0 * mm);
         k_rhs<<<red_grid((long)m * m), kRedThreads, 0, c->st>>>(m, c->P, c->F, c->aE, c->aN, c->rr, c->aW, c->aS, weighted,
-                                                     c->V[0], part_slot(c, 0));
+                                                     c->V[0], part_slot(c, 0), 1, m);
         c->launches++;
     }
     double bsq = 0;
@@ -806,22 +830,22 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
             {
                 ProfScope ps(c, 0, 48.0 * mm);
                 k_spmv<<<red_grid((long)m * m), kRedThreads, 0, c->st>>>(m, c->P, c->Z[k], c->aE, c->aN, c->rr, c->aW, c->aS,
-                                                              weighted, c->w, c->V[0], part_slot(c, 0));
+                                                              weighted, c->w, c->V[0], part_slot(c, 0), 1, m);
                 c->launches++;
             }
             // modified Gram-Schmidt: h_{j,k} for j = 0..k, then ||w||
             for (int j = 1; j <= k; ++j) {
                 ProfScope ps(c, 7, 32.0 * G);
                 k_mgs<<<red_grid(G), kRedThreads, 0, c->st>>>(G, c->w, c->V[j - 1], part_slot(c, j - 1),
-                                                             c->dscal + (j - 1), c->V[j], part_slot(c, j));
+                                                             c->dscal + (j - 1), c->V[j], part_slot(c, j), 1);
                 c->launches++;
             }
             {
                 ProfScope ps(c, 7, 24.0 * G + 16.0 * G);
                 k_mgs<<<red_grid(G), kRedThreads, 0, c->st>>>(G, c->w, c->V[k], part_slot(c, k), c->dscal + k,
-                                                             c->w, part_slot(c, k + 1));
+                                                             c->w, part_slot(c, k + 1), 1);
                 k_normalize<<<red_grid(G), kRedThreads, 0, c->st>>>(G, c->w, part_slot(c, k + 1), c->dscal + k + 1,
-                                                                   c->V[k + 1]);
+                                                                   c->V[k + 1], 1);
                 c->launches += 2;
             }
             if (cyc < 0) CK(c, cudaMemcpyAsync(c->hmgs, c->mgs, sizeof(MGState), cudaMemcpyDeviceToHost, c->st));
@@ -888,10 +912,10 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
     // output
     if (u) {
         if (mem == SPP_HOST) {
-            k_unpack<<<nblk((long)mm), 256, 0, c->st>>>(m, c->P, c->U, c->cbuf);
+            k_unpack<<<nblk((long)mm), 256, 0, c->st>>>(m, c->P, c->U, c->cbuf, 1, m);
             CK(c, cudaMemcpyAsync(u, c->cbuf, sizeof(double) * mm, cudaMemcpyDeviceToHost, c->st));
         } else {
-            k_unpack<<<nblk((long)mm), 256, 0, c->st>>>(m, c->P, c->U, u);
+            k_unpack<<<nblk((long)mm), 256, 0, c->st>>>(m, c->P, c->U, u, 1, m);
         }
         c->launches++;
     }
@@ -902,9 +926,9 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
     if (st) {
         memset(st, 0, sizeof(*st));
         k_spmv<<<kRedBlocks, kRedThreads, 0, c->st>>>(m, c->P, c->U, c->aE, c->aN, c->rr, c->aW, c->aS, 0, c->w,
-                                                      nullptr, nullptr);
+                                                      nullptr, nullptr, 1, m);
         k_resid_stats<<<kRedBlocks, kRedThreads, 0, c->st>>>(m, c->P, c->F, c->w, c->aE, c->aN, c->rr, c->aW, c->aS,
-                                                             c->part);
+                                                             c->part, kRedBlocks, 1, m);
         CK(c, cudaMemcpyAsync(c->hpin, c->part, sizeof(double) * 4 * kRedBlocks, cudaMemcpyDeviceToHost, c->st));
         CK(c, cudaStreamSynchronize(c->st));
         const double s0 = host_sum(c->hpin, kRedBlocks), s1 = host_sum(c->hpin + kRedBlocks, kRedBlocks);
@@ -932,6 +956,7 @@ spp_status spp_solve(spp_ctx *cx, const double *f, double *u, spp_mem mem, doubl
     if (!c) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_solve: NULL context");
     if (!f) FAIL(c, SPP_E_ARG, "spp_solve: NULL rhs");
     if (c->dim == 1) return (spp_status)solve_1d_abi(c, f, u, mem, hist, hcap, st);
+    if (c->dist) return solve_dist(c, f, u, mem, hist, hcap, st);
     return solve_2d(c, f, u, mem, hist, hcap, st);
 }
 
@@ -941,16 +966,17 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
     Ctx *c = (Ctx *)cx;
     if (!c || !in || !out) FAIL(c, SPP_E_ARG, "spp_apply_stage: NULL argument");
     if (c->dim != 2) FAIL(c, SPP_E_STATE, "spp_apply_stage: 2D contexts only");
+    if (c->dist) FAIL(c, SPP_E_STATE, "spp_apply_stage: single-GPU contexts only (not row strips)");
     const int m = c->m, n = c->n;
     const long mm = (long)m * m;
     const long G = (long)c->G;
     CK(c, ensure_vectors(c, 1));
     double *A = c->V[0], *B = c->Z[0];
-    auto pk = [&](const double *src, double *dst) { k_pack<<<nblk(mm), 256, 0, c->st>>>(m, c->P, src, dst); };
-    auto up = [&](const double *src, double *dst) { k_unpack<<<nblk(mm), 256, 0, c->st>>>(m, c->P, src, dst); };
+    auto pk = [&](const double *src, double *dst) { k_pack<<<nblk(mm), 256, 0, c->st>>>(m, c->P, src, dst, 1, m); };
+    auto up = [&](const double *src, double *dst) { k_unpack<<<nblk(mm), 256, 0, c->st>>>(m, c->P, src, dst, 1, m); };
     if (s == SPP_STAGE_MATVEC) {
         pk(in, A);
-        k_spmv<<<kRedBlocks, kRedThreads, 0, c->st>>>(m, c->P, A, c->aE, c->aN, c->rr, c->aW, c->aS, 0, B, nullptr, nullptr);
+        k_spmv<<<kRedBlocks, kRedThreads, 0, c->st>>>(m, c->P, A, c->aE, c->aN, c->rr, c->aW, c->aS, 0, B, nullptr, nullptr, 1, m);
         up(B, out);
     } else if (s == SPP_STAGE_PRECOND) {
         pk(in, A);
@@ -997,7 +1023,7 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
         pk(in + mm, B);
         Level &L0 = c->lev[0];
         k_corner_rhs<<<kRedBlocks, kRedThreads, 0, c->st>>>(c->N, c->P, L0.pitch, A, B, c->aE, c->aN, c->rr, c->aW,
-                                                            c->aS, L0.hb, L0.kb, 0, c->Bc, part_slot(c, 0), nullptr, c->cd, 0);
+                                                            c->aS, L0.hb, L0.kb, 0, c->Bc, part_slot(c, 0), nullptr, c->cd, 0, 1, n);
         k_unpack_level<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, c->Bc, out);
     } else if (s == SPP_STAGE_CORNER_SOLVE) {
         Level &L0 = c->lev[0];
@@ -1220,5 +1246,159 @@ int32_t spp_batch1d_nprob(const spp_batch1d *b) { return b ? ((const Batch1 *)b)
 int64_t spp_batch1d_launches(const spp_batch1d *b) { return b ? ((const Batch1 *)b)->launches : 0; }
 const char *spp_batch1d_last_error(const spp_batch1d *b) { return b ? ((const Batch1 *)b)->err.c_str() : g_err.c_str(); }
 void spp_batch1d_destroy(spp_batch1d *b) { batch1d_free((Batch1 *)b); }
+
+}  // extern "C"
+
+// =========================================================================== row strips
+extern "C" {
+
+spp_status spp_strip_partition(int32_t n, int32_t nranks, int32_t *j)
+{
+    if (!j || nranks < 1 || n < 8 || (n % 2)) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_strip_partition: bad arguments");
+    std::vector<int> J;
+    if (!strip_partition(n, nranks, J)) FAIL((Ctx *)nullptr, SPP_E_ARG, "%d strips do not fit N = %d", nranks, n);
+    for (int r = 0; r <= nranks; ++r) j[r] = J[r];
+    return SPP_OK;
+}
+
+// strip contexts share the problem's validation and setup; the decomposition is finished by the
+// first spp_setup (setup_dist)
+static spp_status strip_ctx(const spp_problem *p, const spp_options *o, void *stream, int rank, int nranks,
+                            const std::vector<int> &J, int Pb, Ctx **out)
+{
+    Ctx *c = nullptr;
+    spp_status s = ctx_new(p, o, stream, &c);
+    if (s != SPP_OK) return s;
+    if (p->dim != 2) { delete c; FAIL((Ctx *)nullptr, SPP_E_ARG, "row strips are a 2D decomposition"); }
+    c->rank = rank; c->nparts = nranks;
+    c->use_graph = 0;
+    const int N = c->N;
+    if (rank >= Pb) { c->line_lo[0] = N - J[rank + 1]; c->line_hi[0] = N - 1 - J[rank]; c->line_lo[1] = 0; c->line_hi[1] = -1; }
+    else {
+        const int nl = c->n - 1;
+        c->line_lo[0] = 0; c->line_hi[0] = -1;
+        c->line_lo[1] = (int)((long)nl * rank / Pb); c->line_hi[1] = (int)((long)nl * (rank + 1) / Pb) - 1;
+    }
+    if ((s = alloc_all(c)) != SPP_OK) { g_err = c->err; ctx_free(c); return s; }
+    *out = c;
+    return SPP_OK;
+}
+
+spp_status spp_create_strips(const spp_problem *p, int32_t nstrips, const spp_options *o, void *stream, spp_ctx **out)
+{
+    if (!p || !out) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_create_strips: NULL argument");
+    *out = nullptr;
+    if (nstrips == 1) return spp_create(p, o, stream, out);
+    std::vector<int> J;
+    if (nstrips < 1 || p->dim != 2 || !strip_partition(p->n, nstrips, J))
+        FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_create_strips: %d strips of a %s N = %d problem", nstrips,
+             p->dim == 2 ? "2D" : "1D", p->n);
+    int Pb = 0;
+    std::string why;
+    if (!check_partition(p->n, J, &Pb, &why)) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_create_strips: %s", why.c_str());
+    Dist *d = new (std::nothrow) Dist();
+    if (!d) FAIL((Ctx *)nullptr, SPP_E_NOMEM, "host allocation failed");
+    d->me = -1; d->st = (cudaStream_t)stream;
+    d->g.P = nstrips; d->g.Pb = Pb; d->g.J = J;
+    for (int r = 0; r < nstrips; ++r) {
+        Ctx *c = nullptr;
+        const spp_status s = strip_ctx(p, o, stream, r, nstrips, J, Pb, &c);
+        if (s != SPP_OK) {
+            const std::string m = g_err;
+            for (Ctx *x : d->cx) ctx_free(x);
+            delete d;
+            g_err = m;
+            return s;
+        }
+        c->dist = d;
+        d->cx.push_back(c);
+    }
+    const spp_status s = spp_setup((spp_ctx *)d->cx[0], p->c1, p->c2, p->r, p->mem);
+    if (s != SPP_OK) { g_err = d->cx[0]->err; spp_destroy((spp_ctx *)d->cx[0]); return s; }
+    *out = (spp_ctx *)d->cx[0];
+    return SPP_OK;
+}
+
+spp_status spp_create_dist(const spp_problem *local, int32_t j0, int32_t j1, void *nccl_comm, int32_t rank,
+                           int32_t nranks, const spp_options *o, void *stream, spp_ctx **out)
+{
+    if (!local || !out) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_create_dist: NULL argument");
+    *out = nullptr;
+    if (nranks < 1 || rank < 0 || rank >= nranks) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_create_dist: rank %d of %d", rank, nranks);
+    if (nranks == 1) {
+        if (j0 != 1 || j1 != local->n) FAIL((Ctx *)nullptr, SPP_E_ARG, "one rank owns rows 1..N-1");
+        return spp_create(local, o, stream, out);
+    }
+    if (!nccl_comm) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_create_dist: NULL NCCL communicator");
+    // gather every rank's [j0, j1) through a provisional strip context (its partial-sum buffer)
+    std::vector<int> J0(nranks + 1, 0);
+    Ctx *c = nullptr;
+    {   // validate the problem and options before any communication
+        spp_status s = ctx_new(local, o, stream, &c);
+        if (s != SPP_OK) return s;
+        delete c;
+        c = nullptr;
+        if (local->dim != 2) FAIL((Ctx *)nullptr, SPP_E_ARG, "row strips are a 2D decomposition");
+    }
+    Dist *d = new (std::nothrow) Dist();
+    if (!d) FAIL((Ctx *)nullptr, SPP_E_NOMEM, "host allocation failed");
+    d->me = rank; d->comm = nccl_comm; d->st = (cudaStream_t)stream; d->g.P = nranks;
+    {
+        double *buf = nullptr, hb[2] = {(double)j0, (double)j1};
+        std::vector<double> all(2 * (size_t)nranks);
+        if (cudaMalloc(&buf, sizeof(double) * 2 * nranks) != cudaSuccess) { delete d; FAIL((Ctx *)nullptr, SPP_E_NOMEM, "device allocation"); }
+        cudaMemcpyAsync(buf + 2 * rank, hb, sizeof(hb), cudaMemcpyHostToDevice, d->st);
+        // a throw-away context whose part buffer is `buf`: the exchange addresses buffers by role
+        Ctx tmp;
+        tmp.part = buf; tmp.st = d->st;
+        d->cx.push_back(&tmp);
+        std::vector<Xfer> xs;
+        for (int s = 0; s < nranks; ++s)
+            for (int t = 0; t < nranks; ++t)
+                if (s != t) xs.push_back({s, t, R_PART, 0, 2L * s, 2L * s, 2, 1, 2});
+        const spp_status s = exchange_rows(d, xs);
+        d->cx.clear();
+        tmp.part = nullptr;
+        if (s == SPP_OK) cudaMemcpyAsync(all.data(), buf, sizeof(double) * 2 * nranks, cudaMemcpyDeviceToHost, d->st);
+        cudaStreamSynchronize(d->st);
+        cudaFree(buf);
+        if (s != SPP_OK) { delete d; FAIL((Ctx *)nullptr, s, "spp_create_dist: gathering the strips failed (%s)", g_err.c_str()); }
+        for (int r = 0; r < nranks; ++r) {
+            J0[r] = (int)all[2 * r];
+            if (r + 1 < nranks && (int)all[2 * r + 1] != (int)all[2 * r + 2]) {
+                delete d;
+                FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_create_dist: strip %d ends at %d but strip %d starts at %d", r,
+                     (int)all[2 * r + 1], r + 1, (int)all[2 * r + 2]);
+            }
+        }
+        J0[nranks] = (int)all[2 * nranks - 1];
+    }
+    int Pb = 0;
+    std::string why;
+    if (!check_partition(local->n, J0, &Pb, &why)) { delete d; FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_create_dist: %s", why.c_str()); }
+    d->g.Pb = Pb; d->g.J = J0;
+    spp_status s = strip_ctx(local, o, stream, rank, nranks, J0, Pb, &c);
+    if (s != SPP_OK) { delete d; return s; }
+    c->dist = d;
+    d->cx.push_back(c);
+    s = spp_setup((spp_ctx *)c, local->c1, local->c2, local->r, local->mem);
+    if (s != SPP_OK) { g_err = c->err; spp_destroy((spp_ctx *)c); return s; }
+    *out = (spp_ctx *)c;
+    return SPP_OK;
+}
+
+spp_status spp_dist_info(const spp_ctx *cx, int32_t *nranks, int32_t *strip_levels, int64_t *xfers, double *bytes,
+                         int64_t *exchanges)
+{
+    const Ctx *c = (const Ctx *)cx;
+    if (!c) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_dist_info: NULL context");
+    const Dist *d = c->dist;
+    if (nranks) *nranks = d ? d->g.P : 1;
+    if (strip_levels) *strip_levels = d ? d->g.D : 0;
+    if (xfers) *xfers = d ? d->nxfer : 0;
+    if (bytes) *bytes = d ? d->xbytes : 0.0;
+    if (exchanges) *exchanges = d ? d->nexch : 0;
+    return SPP_OK;
+}
 
 }  // extern "C"

@@ -107,19 +107,20 @@ __global__ void k_level0_1d(int N, double hx, double Hx, double hy, double Hy, c
 }
 
 // ===================================================================================== layout
-__global__ void k_pack(int m, long P, const double *src, double *dst)   // compact -> padded
+// rows j0 .. j0+nrows-1 of the grid; the compact side holds exactly those rows (row j0 first)
+__global__ void k_pack(int m, long P, const double *src, double *dst, int j0, int nrows)   // compact -> padded
 {
-    const long tot = (long)m * m;
+    const long tot = (long)m * nrows;
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
+        const int j = (int)(p / m) + j0, i = (int)(p % m) + 1;
         dst[(long)j * P + i] = src[p];
     }
 }
-__global__ void k_unpack(int m, long P, const double *src, double *dst)  // padded -> compact
+__global__ void k_unpack(int m, long P, const double *src, double *dst, int j0, int nrows)  // padded -> compact
 {
-    const long tot = (long)m * m;
+    const long tot = (long)m * nrows;
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
+        const int j = (int)(p / m) + j0, i = (int)(p % m) + 1;
         dst[p] = src[(long)j * P + i];
     }
 }
@@ -147,13 +148,14 @@ __device__ __forceinline__ double block_sum(double v, double *sm)
     return v;
 }
 
-// every block re-sums the kRedBlocks partials in the same order
-__device__ __forceinline__ double sum_partials(const double *part, double *sm)
+// every block re-sums the nparts * kRedBlocks partials (one kRedBlocks segment per row strip of a
+// distributed solve; nparts = 1 on one GPU) in the same order
+__device__ __forceinline__ double sum_partials(const double *part, double *sm, int nparts)
 {
     __shared__ double s_res;
     if (threadIdx.x < 32) {
         double v = 0.0;
-        for (int b = threadIdx.x; b < kRedBlocks; b += 32) v += part[b];
+        for (int b = threadIdx.x; b < nparts * kRedBlocks; b += 32) v += part[b];
         v = warp_sum(v);
         if (threadIdx.x == 0) s_res = v;
     }
@@ -165,19 +167,20 @@ __device__ __forceinline__ double sum_partials(const double *part, double *sm)
 // ===================================================================================== stencil
 // w = A z (difference form; R12); weighted: w = (A z)/D.
 // Fused: partial of <w, v0> (first MGS dot) when v0 != nullptr.
+// rows j0 .. j0+nrows-1 (a row strip: DESIGN.md §9; j0 = 1, nrows = m on one GPU)
 __global__ void __launch_bounds__(kRedThreads) k_spmv(int m, long P, const double *__restrict__ z,
     const double *__restrict__ aE, const double *__restrict__ aN, const double *__restrict__ rr,
     const double *__restrict__ aW, const double *__restrict__ aS, int weighted, double *w,
-    const double *__restrict__ v0, double *part)
+    const double *__restrict__ v0, double *part, int j0, int nrows)
 {
     __shared__ double sm[32];
     double acc = 0.0;
-    const long rows = m;
+    const long rows = nrows;
     // one block-iteration = one row segment of 2*blockDim columns, double2 stores
     const int segw = 2 * blockDim.x;
     const long nseg = (P + segw - 1) / segw;
     for (long it = blockIdx.x; it < rows * nseg; it += gridDim.x) {
-        const int j = (int)(it / nseg) + 1;
+        const int j = (int)(it / nseg) + j0;
         const int i0 = (int)(it % nseg) * segw + 2 * threadIdx.x;
         const long g = (long)j * P + i0;
         if (i0 >= P) continue;
@@ -211,13 +214,13 @@ __global__ void __launch_bounds__(kRedThreads) k_spmv(int m, long P, const doubl
 // true residual statistics: sums of (f-Au)^2, ((f-Au)/D)^2, f^2, (f/D)^2
 __global__ void __launch_bounds__(kRedThreads) k_resid_stats(int m, long P, const double *f,
     const double *Au, const double *aE, const double *aN, const double *rr, const double *aW,
-    const double *aS, double *part4)
+    const double *aS, double *part4, long pstride, int j0, int nrows)
 {
     __shared__ double sm[32];
     double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-    const long tot = (long)m * m;
+    const long tot = (long)m * nrows;
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
+        const int j = (int)(p / m) + j0, i = (int)(p % m) + 1;
         const long g = (long)j * P + i;
         const double D = ((aW[i] + aE[g]) + (aS[j] + aN[g])) + rr[g];
         const double r = f[g] - Au[g];
@@ -225,23 +228,23 @@ __global__ void __launch_bounds__(kRedThreads) k_resid_stats(int m, long P, cons
     }
     double t;
     t = block_sum(s0, sm); if (threadIdx.x == 0) part4[blockIdx.x] = t;
-    t = block_sum(s1, sm); if (threadIdx.x == 0) part4[kRedBlocks + blockIdx.x] = t;
-    t = block_sum(s2, sm); if (threadIdx.x == 0) part4[2 * kRedBlocks + blockIdx.x] = t;
-    t = block_sum(s3, sm); if (threadIdx.x == 0) part4[3 * kRedBlocks + blockIdx.x] = t;
-    for (int a4 = 0; a4 < 4; ++a4) zero_tail(part4 + (size_t)a4 * kRedBlocks);
+    t = block_sum(s1, sm); if (threadIdx.x == 0) part4[pstride + blockIdx.x] = t;
+    t = block_sum(s2, sm); if (threadIdx.x == 0) part4[2 * pstride + blockIdx.x] = t;
+    t = block_sum(s3, sm); if (threadIdx.x == 0) part4[3 * pstride + blockIdx.x] = t;
+    for (int a4 = 0; a4 < 4; ++a4) zero_tail(part4 + (size_t)a4 * pstride);
 }
 
 // ===================================================================================== Krylov vectors
 // out = f / D (weighted) or f, partial ||out||^2
 __global__ void __launch_bounds__(kRedThreads) k_rhs(int m, long P, const double *f, const double *aE,
     const double *aN, const double *rr, const double *aW, const double *aS, int weighted, double *out,
-    double *part)
+    double *part, int j0, int nrows)
 {
     __shared__ double sm[32];
     double acc = 0.0;
-    const long tot = (long)m * m;
+    const long tot = (long)m * nrows;
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
+        const int j = (int)(p / m) + j0, i = (int)(p % m) + 1;
         const long g = (long)j * P + i;
         double v = f[g];
         if (weighted) v /= ((aW[i] + aE[g]) + (aS[j] + aN[g])) + rr[g];
@@ -268,10 +271,10 @@ __global__ void k_scale(long n2, double *x, double alpha)
 // MGS step: h = sum(part_in) (stored to hslot by block 0);
 // w -= h * x;  part_out = <w, y>  (y == w gives ||w||^2).
 __global__ void __launch_bounds__(kRedThreads) k_mgs(long n2, double *w, const double *__restrict__ x,
-    const double *part_in, double *hslot, const double *y, double *part_out)
+    const double *part_in, double *hslot, const double *y, double *part_out, int nparts)
 {
     __shared__ double sm[32];
-    const double h = sum_partials(part_in, sm);
+    const double h = sum_partials(part_in, sm, nparts);
     if (blockIdx.x == 0 && threadIdx.x == 0) *hslot = h;
     double acc = 0.0;
     const long n = n2 / 2;
@@ -293,10 +296,10 @@ __global__ void __launch_bounds__(kRedThreads) k_mgs(long n2, double *w, const d
 
 // h = sqrt(sum(part_in)) -> hslot;  v = w / h (0 if h == 0)
 __global__ void __launch_bounds__(kRedThreads) k_normalize(long n2, const double *w, const double *part_in,
-                                                           double *hslot, double *v)
+                                                           double *hslot, double *v, int nparts)
 {
     __shared__ double sm[32];
-    const double h = sqrt(sum_partials(part_in, sm));
+    const double h = sqrt(sum_partials(part_in, sm, nparts));
     if (blockIdx.x == 0 && threadIdx.x == 0) *hslot = h;
     const double inv = h > 0.0 ? 1.0 / h : 0.0;
     const long n = n2 / 2;
@@ -329,14 +332,14 @@ __global__ void k_update_x(long n2, int k, const double *const *Z, const double 
 __global__ void __launch_bounds__(kRedThreads) k_corner_rhs(int N, long P, long P0, const double *v,
     const double *z, const double *aE, const double *aN, const double *rr, const double *aW,
     const double *aS, const double *hb, const double *kb, int weighted, double *bc, double *part, double *bc2,
-    const double *cd, int scale2)
+    const double *cd, int scale2, int j0, int j1)
 {
     __shared__ double sm[32];
     const int n = N / 2;
     double acc = 0.0;
-    const long tot = (long)n * n;
+    const long tot = (long)n * (j1 - j0 + 1);           // corner rows j0 .. j1
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / n) + 1, i = (int)(p % n) + 1;
+        const int j = (int)(p / n) + j0, i = (int)(p % n) + 1;
         const long g = (long)j * P + i;
         double s = 1.0;
         if (weighted) s = ((aW[i] + aE[g]) + (aS[j] + aN[g])) + rr[g];
@@ -411,12 +414,12 @@ __global__ void k_prolong_add(int nl, long Pv, double *e, const double *ec, long
 }
 
 // copy the corner iterate into the global preconditioned vector
-__global__ void k_corner_out(int n, long P0, const double *zc, long P, double *z, const MGState *ms)
+__global__ void k_corner_out(int n, long P0, const double *zc, long P, double *z, const MGState *ms, int j0, int j1)
 {
     if (ms) zc = ms->zcur;                          // corner graph: nullptr when no cycle ran (z = 0)
-    const long tot = (long)n * n;
+    const long tot = (long)n * (j1 - j0 + 1);
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / n) + 1, i = (int)(p % n) + 1;
+        const int j = (int)(p / n) + j0, i = (int)(p % n) + 1;
         z[(long)j * P + i] = zc ? zc[(long)j * P0 + i] : 0.0;
     }
 }

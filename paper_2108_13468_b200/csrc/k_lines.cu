@@ -506,42 +506,54 @@ __global__ void __launch_bounds__(256) k_lines_tma(LineChain cx, LineChain cy, c
 }
 
 // ------------------------------------------------------------------------------ host
-void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double> &ky)
+// Chunks of the owned lines [l0, l1] of one chain (all lines on one GPU; a row strip's X lines
+// or a bottom strip's share of the Y lines in a distributed solve; l1 < l0: none).
+// A chunk starts `warm-up` lines upstream of its first owned line, where prod kappa over the
+// warm-up is <= 1e-17 (so it equals the sequential chain to rounding); those lines' operands are
+// a row strip's halo.  budget: CTAs for the chain.  Pure host function of the contractions.
+std::vector<LineChunk> plan_chain_chunks(int chain, const std::vector<double> &k, int l0, int l1, int budget)
+{
+    std::vector<LineChunk> out;
+    const int nl = (int)k.size(), cnt = l1 - l0 + 1;
+    if (cnt <= 0) return out;
+    const double target = std::log(1e-17);   // below fp64 rounding, as the MG halos (DESIGN.md)
+    budget = std::max(1, budget);
+    std::vector<double> lg(nl + 1, 0.0);                 // prefix sums of log kappa
+    for (int l = 0; l < nl; ++l) lg[l + 1] = lg[l] + std::log(std::max(k[l], 1e-300));
+    // warm-up start of a chunk beginning at line f: the largest st <= f with
+    // lg[f] - lg[st] <= target (prod kappa small enough), or 0.  lg decreases, so st(f) is
+    // nondecreasing in f: one two-pointer pass (the plan runs inside every setup).
+    std::vector<int> wst(nl + 1, 0);
+    for (int f = 0, st = 0; f <= nl; ++f) {
+        while (st < f && lg[f] - lg[st + 1] <= target) ++st;  // advance while st+1 still suffices
+        wst[f] = (lg[f] - lg[st] <= target) ? st : 0;
+    }
+    int bestG = cnt; long bestCost = 1L << 40;
+    for (int G = (cnt + budget - 1) / budget; G <= cnt; ++G) {   // smallest chunks that fit the budget first
+        const int P = (cnt + G - 1) / G;
+        if (P > budget) continue;
+        long worst = 0;
+        for (int f = l0; f <= l1; f += G) {
+            const int last = std::min(l1, f + G - 1);
+            worst = std::max<long>(worst, last - wst[f] + 1);
+        }
+        if (worst < bestCost) { bestCost = worst; bestG = G; }
+    }
+    for (int f = l0; f <= l1; f += bestG) out.push_back({chain, f, std::min(l1, f + bestG - 1), wst[f]});
+    if (getenv("SPP_DEBUG_LINES"))
+        fprintf(stderr, "[spp] line chain %d: lines %d..%d of %d, chunk %d lines, %d chunks, worst %ld lines (kappa %.6g .. %.6g)\n",
+                chain, l0, l1, nl, bestG, (cnt + bestG - 1) / bestG, bestCost, *std::min_element(k.begin(), k.end()),
+                *std::max_element(k.begin(), k.end()));
+    return out;
+}
+
+void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double> &ky, const int lo[2],
+                 const int hi[2], int budget)
 {
     c->chunks.clear();
-    const int nl = c->n - 1;
-    const double target = std::log(1e-17);   // below fp64 rounding, as the MG halos (DESIGN.md)
-    const int budget = std::max(1, c->sm_count / 2);      // CTAs per chain: one resident CTA per SM
     for (int chain = 0; chain < 2; ++chain) {
-        const std::vector<double> &k = chain == 0 ? kx : ky;
-        std::vector<double> lg(nl + 1, 0.0);                 // prefix sums of log kappa
-        for (int l = 0; l < nl; ++l) lg[l + 1] = lg[l] + std::log(std::max(k[l], 1e-300));
-        // warm-up start of a chunk beginning at line f: the largest st <= f with
-        // lg[f] - lg[st] <= target (prod kappa small enough), or 0.  lg decreases, so st(f) is
-        // nondecreasing in f: one two-pointer pass (the plan runs inside every setup).
-        std::vector<int> wst(nl + 1, 0);
-        for (int f = 0, st = 0; f <= nl; ++f) {
-            while (st < f && lg[f] - lg[st + 1] <= target) ++st;  // advance while st+1 still suffices
-            wst[f] = (lg[f] - lg[st] <= target) ? st : 0;
-        }
-        auto warm = [&](int first) { return wst[first]; };
-        int bestG = nl; long bestCost = nl;
-        for (int G = (nl + budget - 1) / budget; G <= nl; ++G) {     // smallest chunks that fit the budget first
-            const int P = (nl + G - 1) / G;
-            if (P > budget) continue;
-            long worst = 0;
-            for (int f = 0; f < nl; f += G) {
-                const int last = std::min(nl - 1, f + G - 1);
-                worst = std::max<long>(worst, last - warm(f) + 1);
-            }
-            if (worst < bestCost) { bestCost = worst; bestG = G; }
-        }
-        for (int f = 0; f < nl; f += bestG)
-            c->chunks.push_back({chain, f, std::min(nl - 1, f + bestG - 1), warm(f)});
-        if (getenv("SPP_DEBUG_LINES"))
-            fprintf(stderr, "[spp] line chain %d: %d lines, chunk %d lines, %d chunks, worst %ld lines (kappa %.6g .. %.6g)\n",
-                    chain, nl, bestG, (nl + bestG - 1) / bestG, bestCost, *std::min_element(k.begin(), k.end()),
-                    *std::max_element(k.begin(), k.end()));
+        const auto v = plan_chain_chunks(chain, chain == 0 ? kx : ky, lo[chain], hi[chain], budget);
+        c->chunks.insert(c->chunks.end(), v.begin(), v.end());
     }
 }
 
@@ -568,11 +580,16 @@ cudaError_t setup_lines(Ctx *c)
     else k_line_factor_scan<16><<<dim3(nl, 2), TF, 0, c->st>>>(N, c->P, c->aE, c->aN, c->rr, c->aW, c->aS, c->weighted, ox, oy);
     c->launches++;
     SPP_CUDA_TRY(cudaGetLastError());
-    std::vector<double> kx(nl), ky(nl);
-    SPP_CUDA_TRY(cudaMemcpyAsync(kx.data(), c->kapX, sizeof(double) * nl, cudaMemcpyDeviceToHost, c->st));
-    SPP_CUDA_TRY(cudaMemcpyAsync(ky.data(), c->kapY, sizeof(double) * nl, cudaMemcpyDeviceToHost, c->st));
+    c->kx.assign(nl, 0.0); c->ky.assign(nl, 0.0);
+    SPP_CUDA_TRY(cudaMemcpyAsync(c->kx.data(), c->kapX, sizeof(double) * nl, cudaMemcpyDeviceToHost, c->st));
+    SPP_CUDA_TRY(cudaMemcpyAsync(c->ky.data(), c->kapY, sizeof(double) * nl, cudaMemcpyDeviceToHost, c->st));
     SPP_CUDA_TRY(cudaStreamSynchronize(c->st));
-    plan_chunks(c, kx, ky);
+    if (c->line_lo[0] < 0) {                            // one GPU: every line, the GPU shared by both chains
+        const int lo[2] = {0, 0}, hi[2] = {nl - 1, nl - 1};
+        plan_chunks(c, c->kx, c->ky, lo, hi, c->sm_count / 2);
+    } else {
+        plan_chunks(c, c->kx, c->ky, c->line_lo, c->line_hi, c->sm_count);
+    }
     // chains
     const long P = c->P;
     c->chX = LineChain{nl, n, 1, -P, (long)(N - 1) * P + 1, 1, xp, xe, xa, xb, c->tX};
@@ -582,8 +599,9 @@ cudaError_t setup_lines(Ctx *c)
         SPP_CUDA_TRY(cudaMalloc(&c->d_chunks, sizeof(LineChunk) * c->chunks.size()));
         c->nchunks_alloc = (int)c->chunks.size();
     }
-    SPP_CUDA_TRY(cudaMemcpyAsync(c->d_chunks, c->chunks.data(), sizeof(LineChunk) * c->chunks.size(),
-                                 cudaMemcpyHostToDevice, c->st));
+    if (!c->chunks.empty())
+        SPP_CUDA_TRY(cudaMemcpyAsync(c->d_chunks, c->chunks.data(), sizeof(LineChunk) * c->chunks.size(),
+                                     cudaMemcpyHostToDevice, c->st));
     int T = n / 8;
     if (T < 32) T = 32;
     if (T > 256) T = 256;
@@ -607,11 +625,12 @@ static size_t lines_tma_smem(int len, int nst)
     return ((size_t)nst * 6 * len + len) * sizeof(double) + 1024;   // stages + z staging (+ alignment)
 }
 
-// z (Y region) <- scratch: line l (column i = N-1-l), element k (row j = k+1); 32x32 tiles
-__global__ void k_ysc_transpose(int nl, int len, long P, int N, const double *__restrict__ ysc, double *z)
+// z (Y region) <- scratch: line l (column i = N-1-l), element k (row j = k+1); 32x32 tiles; lines
+// la .. nl-1 (la > 0: a bottom strip's share of the Y lines)
+__global__ void k_ysc_transpose(int nl, int len, long P, int N, const double *__restrict__ ysc, double *z, int la)
 {
     __shared__ double t[32][33];
-    const int l0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    const int l0 = la + blockIdx.x * 32, k0 = blockIdx.y * 32;
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         const int l = l0 + r, k = k0 + threadIdx.x;
         if (l < nl && k < len) t[r][threadIdx.x] = ysc[(long)l * len + k];
@@ -654,8 +673,16 @@ static bool launch_lines_tma(Ctx *c, const double *v, double *z)
     double *ysc = c->cbuf;                              // free during the FGMRES iterations
     if (K == 8) k_lines_tma<8><<<nb, T, sm, c->st>>>(c->chX, c->chY, c->d_chunks, z, ysc, c->N, c->P, nst, m);
     else k_lines_tma<16><<<nb, T, sm, c->st>>>(c->chX, c->chY, c->d_chunks, z, ysc, c->N, c->P, nst, m);
-    k_ysc_transpose<<<dim3((nl + 31) / 32, (len + 31) / 32), dim3(32, 8), 0, c->st>>>(nl, len, c->P, c->N, ysc, z);
-    c->launches += 2;
+    c->launches++;
+    // the owned Y lines (a contiguous range) back into z
+    int ya = nl, yb = -1;
+    for (const auto &ck : c->chunks)
+        if (ck.chain == 1) { ya = std::min(ya, ck.first); yb = std::max(yb, ck.last); }
+    if (yb >= ya) {
+        k_ysc_transpose<<<dim3((yb - ya + 32) / 32, (len + 31) / 32), dim3(32, 8), 0, c->st>>>(yb + 1, len, c->P, c->N,
+                                                                                         ysc, z, ya);
+        c->launches++;
+    }
     return true;
 }
 
@@ -663,8 +690,9 @@ void launch_lines(Ctx *c, const double *v, double *z)
 {
     const int T = c->lines_threads, K = (c->n + T - 1) / T;
     const int nb = (int)c->chunks.size();
-    double bytes = 0;   // algorithmic: v + 4 factors read, z written, per node of X and Y
-    bytes = 2.0 * (c->n - 1) * c->n * 48.0;
+    if (nb == 0) return;
+    double bytes = 0;   // algorithmic: v + 4 factors read, z written, per owned node of X and Y
+    for (const auto &ck : c->chunks) bytes += (double)(ck.last - ck.first + 1) * c->n * 48.0;
     ProfScope ps(c, 2, bytes);
     if (launch_lines_tma(c, v, z)) return;
     if (K <= 1) k_lines<1><<<nb, T, 0, c->st>>>(c->chX, c->chY, c->d_chunks, v, z);

@@ -153,10 +153,11 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     const int nl = a.nl;
-    // tile (CHAIN: blockIdx.y = row strip block, full width)
-    const int out_top = nl - (int)blockIdx.y * a.rows_out;
+    // tile (CHAIN: blockIdx.y = row strip block, full width); rows 1..nr_out are output rows,
+    // the block's rows above them (up to nr) only halo
+    const int out_top = a.nr_out - (int)blockIdx.y * a.rows_out;
     const int out_bot = max(1, out_top - a.rows_out + 1);
-    const int top = min(nl, out_top + a.halo_y);
+    const int top = min(a.nr, out_top + a.halo_y);
     const int out_right = nl - (int)blockIdx.x * a.cols_out;
     const int out_left = max(1, out_right - a.cols_out + 1);
     // The TMA box origin X0 = right + ioff + 2(wtop + joff) - 15 - 16c must be even (16-byte
@@ -258,8 +259,8 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
     // ---- sweeping warp ----
     const int nwa = min(W, (top - out_bot) / 32 + 1);
     const bool has_consumer = w + 1 < nwa;
-    const bool chain_in = CHAIN && w == 0 && blockIdx.y > 0;
-    const bool chain_out = CHAIN && w == nwa - 1 && (int)blockIdx.y + 1 < (int)gridDim.y;
+    const bool chain_in = CHAIN && w == 0 && (blockIdx.y > 0 || a.ext_in != nullptr);
+    const bool chain_out = CHAIN && w == nwa - 1 && ((int)blockIdx.y + 1 < (int)gridDim.y || a.chain_last);
     // this lane's row; element (box row 31-t, column x') lives at double offset
     // (31-t)*16 + ((x'/2) ^ ((31-t)&7))*2 + (x'&1)   (128B swizzle)
     const int rowoff = (31 - lane) * WCW, sw = (31 - lane) & 7;
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
             // (the load for chunk c was issued during chunk c-1: vin, so the L2 round trip overlaps
             // the steps; only a value not yet published is polled again)
             const unsigned long long *src = reinterpret_cast<const unsigned long long *>(
-                a.chain_buf + (long)(blockIdx.y - 1) * a.chain_ld) + c * WCW + (lane & 15);
+                blockIdx.y > 0 ? a.chain_buf + (long)(blockIdx.y - 1) * a.chain_ld : a.ext_in) + c * WCW + (lane & 15);
             const bool mine = lane < 16 && c * WCW + lane < ncols;
             if (c == 0 && mine) vin = ld_relaxed_u64(src);
             for (unsigned spins = 0; !__all_sync(0xffffffffu, !mine || vin != kChainSentinel); ++spins) {
@@ -520,7 +521,8 @@ void launch_wave(Ctx *c, WaveArgs a, long rows_v, long rows_c, int warps, bool y
 {
     WaveMaps m;
     if (!wave_maps(c, a, rows_v, rows_c, &m)) { c->sticky = cudaErrorInvalidValue; return; }
-    const dim3 grid((a.nl + a.cols_out - 1) / a.cols_out, (a.nl + a.rows_out - 1) / a.rows_out);
+    if (a.nr <= 0) { a.nr = a.nl; a.nr_out = a.nl; }
+    const dim3 grid((a.nl + a.cols_out - 1) / a.cols_out, (a.nr_out + a.rows_out - 1) / a.rows_out);
     const size_t sm = wave_smem(warps, yform);
     ProfScope ps(c, cls, bytes);
 #ifdef SPP_WAVE_PROF
@@ -550,7 +552,8 @@ void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform,
     const int W = chain_warps(c);
     a.rows_out = 32 * W; a.halo_y = 0;
     a.cols_out = a.nl; a.halo_x = 0;
-    const int ncta = (int)wave_chain_ctas(c, a.nl);
+    if (a.nr <= 0) { a.nr = a.nl; a.nr_out = a.nl; }
+    const int ncta = (int)wave_chain_ctas(c, a.nr_out);
     a.chain_flags = c->chain_flags;
     a.chain_buf = c->chain;
     a.chain_ld = c->chain_ld;
@@ -594,11 +597,11 @@ __device__ __forceinline__ double interp_c(const double *ec, long Pc, int i, int
 __global__ void __launch_bounds__(256) k_gs_prep(int nl, long pv, const double *__restrict__ e,
     const double *__restrict__ ec, long pcv, const double *__restrict__ b,
     const double *__restrict__ aW, const double *__restrict__ aS, double *g,
-    const double *__restrict__ cd, long pc, int bscaled)
+    const double *__restrict__ cd, long pc, int bscaled, int j0, int j1)
 {
-    const long tot = (long)nl * nl;
+    const long tot = (long)nl * (j1 - j0 + 1);         // rows j0 .. j1 of the level
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
+        const int j = (int)(p / nl) + j0, i = (int)(p % nl) + 1;
         const long v = (long)j * pv + i;
         double ew = e[v - 1], es = e[v - pv];
         if (ec) {
@@ -636,35 +639,62 @@ void launch_scale_cd(Ctx *c, int l, const double *b, double *q)
 // with q = rhs/D; inside the V-cycle the level right-hand sides are stored divided by D
 // (bscaled), so mode 0 streams b itself; a caller's plain rhs is scaled here.  y-form:
 // y = q + ya y_E + yn y_N, z = y/D at write-back.
-void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, double *enew, const double *ec,
-               bool bscaled)
+// The parallel part of a GS sweep from e_old (+ P ec): q = prep(e_old [+ P ec]) into L.g on the
+// level's rows (a row strip's own rows in a distributed solve).
+void launch_gs_prep(Ctx *c, int l, const double *b, const double *eold, const double *ec, bool bscaled)
 {
     Level &L = c->lev[l];
-    const double nn = (double)L.n * L.n;
+    const bool zf = c->mg_zform;
+    const int j0 = L.sdist ? L.slo : 1, j1 = L.sdist ? L.shi : L.n;
+    ProfScope ps(c, 5, (double)L.n * (j1 - j0 + 1) * (zf ? 32.0 : 24.0));
+    k_gs_prep<<<gblocks((long)L.n * (j1 - j0 + 1)), 256, 0, c->st>>>(L.n, L.pitch, eold, ec,
+        ec ? c->lev[l + 1].pitch : 0, b, L.aW, L.aS, L.g, zf ? L.cd : nullptr, L.cpitch, bscaled ? 1 : 0, j0, j1);
+    c->launches++;
+    dbg_sync(c, "k_gs_prep");
+}
+
+// The downstream recurrence of a GS sweep of level l for the right-hand side q (already in the
+// sweep's form): tiled with certified halos, one exact CTA, or the exact chain; on a row strip
+// the own rows plus L.shalo halo rows above.
+void launch_gs_sweep(Ctx *c, int l, const double *q, double *enew)
+{
+    Level &L = c->lev[l];
     const bool zf = c->mg_zform;
     WaveArgs a{};
     a.nl = L.n; a.pv = L.pitch; a.pc = L.cpitch;
     if (zf) { a.ca = l == 0 ? c->ca : L.ya; a.cn = l == 0 ? c->cn : L.yn; }   // levels >= 1 keep aE/D, aN/D in ya, yn
     else { a.ca = L.ya; a.cn = L.yn; }
-    a.cd = L.cd; a.z = enew;
-    if (mode == 0) {
-        if (!zf || bscaled) a.q = b;
-        else { launch_scale_cd(c, l, b, L.g); a.q = L.g; }
-    } else {
-        {
-            ProfScope ps(c, 5, nn * (zf ? 32.0 : 24.0));
-            k_gs_prep<<<gblocks((long)L.n * L.n), 256, 0, c->st>>>(L.n, L.pitch, eold, ec,
-                ec ? c->lev[l + 1].pitch : 0, b, L.aW, L.aS, L.g, zf ? L.cd : nullptr, L.cpitch, bscaled ? 1 : 0);
-            c->launches++;
-            dbg_sync(c, "k_gs_prep");
-        }
-        a.q = L.g;
+    a.cd = L.cd; a.z = enew; a.q = q;
+    if (L.sdist) {                                  // row strip: own rows + halo rows above
+        a.joff = L.slo - 1;
+        a.nr_out = L.shi - L.slo + 1;
+        a.nr = a.nr_out + L.shalo;
     }
-    const double bytes = nn * (zf ? 32.0 : 40.0);   // q, couplings (+ 1/D in y-form) read; z written
+    const double bytes = (double)L.n * (a.nr_out > 0 ? a.nr_out : L.n) * (zf ? 32.0 : 40.0);   // q, couplings (+ 1/D in y-form) read; z written
     const long rows_v = L.n + 2, rows_c = l == 0 ? c->N + 1 : L.n + 2;   // level 0 shares the global coefficients
     if (L.tile_warps == 0) { launch_wave_chain(c, a, rows_v, rows_c, !zf, 3, bytes); return; }
     a.rows_out = L.tile_rows; a.cols_out = L.tile_cols; a.halo_y = L.halo_y; a.halo_x = L.halo_x;
     launch_wave(c, a, rows_v, rows_c, L.tile_warps, !zf, 3, bytes);
+}
+
+// One downstream GS sweep on level l: mode 0 from zero (q = b); mode 1 from e_old (+ P ec when
+// ec != null): q = prep(e_old [+ P ec]).  z-form (c->mg_zform): z = q + (aE/D) z_E + (aN/D) z_N
+// with q = rhs/D; inside the V-cycle the level right-hand sides are stored divided by D
+// (bscaled), so mode 0 streams b itself; a caller's plain rhs is scaled here.  y-form:
+// y = q + ya y_E + yn y_N, z = y/D at write-back.
+void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, double *enew, const double *ec,
+               bool bscaled)
+{
+    Level &L = c->lev[l];
+    const bool zf = c->mg_zform;
+    const double *q = b;
+    if (mode == 0) {
+        if (zf && !bscaled) { launch_scale_cd(c, l, b, L.g); q = L.g; }
+    } else {
+        launch_gs_prep(c, l, b, eold, ec, bscaled);
+        q = L.g;
+    }
+    launch_gs_sweep(c, l, q, enew);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -868,11 +898,12 @@ __global__ void __launch_bounds__(256, 7) k_resid_restrict(int nf, long pv, long
     const double *__restrict__ rr, const double *__restrict__ aW, const double *__restrict__ aS,
     const double *__restrict__ hbf, const double *__restrict__ kbf, int nc, long pvc,
     const double *__restrict__ hbc, const double *__restrict__ kbc, double *bc,
-    const double *__restrict__ cdc, long pcc, int rs_in, int scale_out)
+    const double *__restrict__ cdc, long pcc, int rs_in, int scale_out, int jc0, int jc1)
 {
     constexpr int RFW = 2 * RT + 1;
     __shared__ double s[RFW * RFW];
-    const int I0 = (int)blockIdx.x * RT + 1, J0 = (int)blockIdx.y * RT + 1;
+    // coarse rows jc0 .. jc1 (a row strip's rows of level l+1; 1 .. nc on one GPU)
+    const int I0 = (int)blockIdx.x * RT + 1, J0 = (int)blockIdx.y * RT + jc0;
     const int fi0 = 2 * I0 - 1, fj0 = 2 * J0 - 1;
 #pragma unroll 4
     for (int p = threadIdx.x; p < RFW * RFW; p += blockDim.x) {
@@ -893,7 +924,7 @@ __global__ void __launch_bounds__(256, 7) k_resid_restrict(int nf, long pv, long
     __syncthreads();
     for (int p = threadIdx.x; p < RT * RT; p += blockDim.x) {
         const int I = I0 + p % RT, J = J0 + p / RT;
-        if (I > nc || J > nc) continue;
+        if (I > nc || J > jc1) continue;
         const int li = 2 * (I - I0) + 1, lj = 2 * (J - J0) + 1;
         double acc = 0.0;
 #pragma unroll
@@ -914,10 +945,12 @@ void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e, bool
     // coarse tile edge: enough CTAs to fill the GPU on the small levels, and several waves of
     // CTAs on the large ones (one wave plus a small remainder leaves most SMs idle in the tail)
     const int RTn = C.n >= 128 ? 16 : 8;
-    const dim3 grid((C.n + RTn - 1) / RTn, (C.n + RTn - 1) / RTn);
+    // coarse rows: this rank's strip of level l+1 when level l runs on strips
+    const int jc0 = F.sdist ? C.slo : 1, jc1 = F.sdist ? C.shi : C.n;
+    const dim3 grid((C.n + RTn - 1) / RTn, (jc1 - jc0 + RTn) / RTn);
 #define SPP_RR(T) k_resid_restrict<T><<<grid, T >= 32 ? 256 : (T >= 16 ? 256 : 128), 0, c->st>>>(F.n, F.pitch, \
         F.cpitch, e, R, F.aE, F.aN, F.rr, F.aW, F.aS, F.hb, F.kb, C.n, C.pitch, C.hb, C.kb, C.b, C.cd, C.cpitch, \
-        rs_in ? 1 : 0, scale_out ? 1 : 0)
+        rs_in ? 1 : 0, scale_out ? 1 : 0, jc0, jc1)
     if (RTn == 32) SPP_RR(32);
     else if (RTn == 16) SPP_RR(16);
     else SPP_RR(8);
@@ -935,20 +968,26 @@ __global__ void __launch_bounds__(kRedThreads) k_cycle_update(int nl, long pv, l
     const double *__restrict__ e, double *znew, const double *__restrict__ b, const double *__restrict__ aE,
     const double *__restrict__ aN, const double *__restrict__ rr, const double *__restrict__ aW,
     const double *__restrict__ aS, const double *__restrict__ hb, const double *__restrict__ kb, double *rho,
-    double *part, const MGState *ms, const double *__restrict__ cd, int scale_rho)
+    double *part, const MGState *ms, const double *__restrict__ cd, int scale_rho, int jz0, int jz1, int j0, int j1)
 {
     __shared__ double sm[32];
     if (ms) { z = ms->zcur; znew = ms->znext; }        // corner graph: buffers from the device state
     double acc = 0.0;
-    const long tot = (long)nl * nl;
+    // z' = z + e on rows jz0 .. jz1; rho and the norm on the owned rows j0 .. j1 (a row strip
+    // also carries z' on its one-row halos; everything 1 .. nl on one GPU)
+    const long tot = (long)nl * (jz1 - jz0 + 1);
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
+        const int j = (int)(p / nl) + jz0, i = (int)(p % nl) + 1;
         const long g = (long)j * pv + i, q = (long)j * pc + i;
-        double zc = e[g], zw = e[g - 1], ze = e[g + 1], zs = e[g - pv], zn = e[g + pv];
-        if (z) { zc += z[g]; zw += z[g - 1]; ze += z[g + 1]; zs += z[g - pv]; zn += z[g + pv]; }
+        const bool own = j >= j0 && j <= j1;
+        double zc = e[g];
+        if (z) zc += z[g];
+        znew[g] = zc;
+        if (!own) continue;
+        double zw = e[g - 1], ze = e[g + 1], zs = e[g - pv], zn = e[g + pv];
+        if (z) { zw += z[g - 1]; ze += z[g + 1]; zs += z[g - pv]; zn += z[g + pv]; }
         const double Az = aW[i] * (zc - zw) + aE[q] * (zc - ze) + aS[j] * (zc - zs) + aN[q] * (zc - zn) + rr[q] * zc;
         const double r = b[g] - Az;
-        znew[g] = zc;
         rho[g] = scale_rho ? r * cd[q] : r;             // the next V-cycle's input (rho/D in z-form)
         const double t = (hb[i] * kb[j]) * r;
         acc += t * t;
@@ -973,9 +1012,12 @@ void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew,
     Level &L = c->lev[0];
     const double nn = (double)L.n * L.n;
     ProfScope ps(c, 6, nn * ((z ? 64.0 : 56.0) + (c->mg_zform ? 8.0 : 0.0)));
-    k_cycle_update<<<red_grid((long)L.n * L.n), kRedThreads, 0, c->st>>>(L.n, L.pitch, L.cpitch, z, e, znew, b, L.aE, L.aN, L.rr,
-                                                          L.aW, L.aS, L.hb, L.kb, rho, part, ms, L.cd,
-                                                          c->mg_zform ? 1 : 0);
+    // a row strip updates z on its one-row halos too (their e came from the neighbours)
+    const int j0 = L.sdist ? L.slo : 1, j1 = L.sdist ? L.shi : L.n;
+    const int jz0 = std::max(1, j0 - (L.sdist ? 1 : 0)), jz1 = std::min(L.n, j1 + (L.sdist ? 1 : 0));
+    k_cycle_update<<<red_grid((long)L.n * (jz1 - jz0 + 1)), kRedThreads, 0, c->st>>>(L.n, L.pitch, L.cpitch, z, e, znew, b,
+                                                          L.aE, L.aN, L.rr, L.aW, L.aS, L.hb, L.kb, rho, part, ms, L.cd,
+                                                          c->mg_zform ? 1 : 0, jz0, jz1, j0, j1);
     c->launches++;
 }
 
@@ -1027,6 +1069,56 @@ void launch_ycoef(Ctx *c, int nl, long pc, const double *aE, const double *aN, c
     c->launches++;
 }
 
+// Tile plan of a sweep over `rows` output rows x n columns of a level with certified halo
+// `halo`.  whole: the block is the whole level (no rows above it);
+// otherwise it is a row strip of a distributed solve whose top tile recomputes `halo` rows of the
+// strip above.  A tile's sweep takes about (chunks + 5 (W - 1)) chunk-times: each of its W warps
+// starts 5 chunks after the one above (62-column lane skew + one chunk of granularity), and a warp
+// sweeps (tile columns + halo + 62) / 16 chunks.  Picks the warps per tile (3..Wt; the halo rows
+// are part of the tile) and the column tiling with the smallest such time among the plans that
+// run as one wave of one CTA per SM.  Returns false when no plan exists.
+bool plan_tiles(const Ctx *c, int n, int rows, int halo, bool whole, Level &L)
+{
+    const Tune &T = c->tune;
+    const int Wt = std::max(1, std::min(T.gs_warps, c->mg_zform ? WMAXW : 4));   // 5 warps only fit in z-form
+    const int lag = T.gs_lag;
+    auto cost = [lag](int W, int cols) { return (cols + WLAG * 31 + WCW - 1) / WCW + lag * (W - 1); };
+    int bestW = 0, bestRows = 0, bestCols = 0, bestT = 1 << 30, bestN = 1 << 30;
+    if (whole && n <= 32 * Wt) {                               // candidate: one exact CTA
+        bestW = (n + 31) / 32; bestRows = n; bestCols = n; bestT = cost(bestW, n); bestN = 1;
+    }
+    for (int W = std::min(3, Wt); W <= Wt; ++W) {
+        const int rows_out = 32 * W - halo;
+        if (rows_out < 16 || (whole && rows_out >= n)) continue;
+        const int nrt = (rows + rows_out - 1) / rows_out;
+        if (nrt > c->sm_count) continue;
+        const int maxct = std::max(1, std::min(c->sm_count / nrt, n / 64));
+        for (int nct = 1; nct <= maxct; ++nct) {
+            int tc = (n + nct - 1) / nct;
+            tc = (tc + 15) / 16 * 16;
+            if (T.gs_tile_cols > 0) tc = std::min(n, T.gs_tile_cols);
+            const bool full = tc >= n;
+            const int t = cost(W, (full ? n : tc + halo));
+            const int ncta = nrt * ((n + tc - 1) / tc);
+            if (t < bestT || (t == bestT && ncta < bestN)) {
+                bestT = t; bestN = ncta; bestW = W; bestRows = rows_out; bestCols = full ? n : tc;
+            }
+        }
+    }
+    if (bestW == 0) return false;
+    L.tile_warps = bestW;
+    L.tile_rows = bestRows;
+    L.tile_cols = bestCols;
+    const bool exact1 = whole && bestRows >= n;
+    L.halo_y = exact1 ? 0 : halo;
+    L.halo_x = bestCols >= n ? 0 : halo;
+    if (getenv("SPP_DEBUG_TILES"))
+        fprintf(stderr, "[spp] level n=%d rows=%d%s halo=%d: warps %d tile %dx%d (+%d,%d) cost %d chunks, %d CTAs\n",
+                n, rows, whole ? "" : " (strip)", halo, L.tile_warps, L.tile_rows, L.tile_cols, L.halo_y, L.halo_x, bestT,
+                bestN);
+    return true;
+}
+
 cudaError_t setup_mg_tiles(Ctx *c)
 {
     const Tune &T = c->tune;
@@ -1048,14 +1140,8 @@ cudaError_t setup_mg_tiles(Ctx *c)
         if (rho < 1.0)
             for (int h = 8; h <= T.gs_max_halo; h += 8)
                 if (h * std::log(rho) <= std::log(1e-17)) { halo = h; break; }
+        L.halo_cert = halo;
         const int n = L.n;
-        // A tile's sweep takes about (chunks + 5 (W - 1)) chunk-times: each of its W warps starts
-        // 5 chunks after the one above (62-column lane skew + one chunk of granularity), and a
-        // warp sweeps (tile columns + halo + 62) / 16 chunks.  Pick the warps per tile (3 or 4;
-        // the halo rows are part of the tile) and the column tiling with the smallest such time
-        // among the plans that run as one wave of one CTA per SM.
-        const int lag = T.gs_lag;
-        auto cost = [lag](int W, int cols) { return (cols + WLAG * 31 + WCW - 1) / WCW + lag * (W - 1); };
         if (halo < 0 || halo + 16 > 32 * Wt) {
             if (n <= 32 * Wt) {                                // one CTA, exact
                 L.tile_warps = (n + 31) / 32;
@@ -1063,37 +1149,7 @@ cudaError_t setup_mg_tiles(Ctx *c)
             } else L.tile_warps = 0;                           // no certified halo: exact chain
             continue;
         }
-        int bestW = 0, bestRows = 0, bestCols = 0, bestT = 1 << 30, bestN = 1 << 30;
-        if (n <= 32 * Wt) {                                    // candidate: one exact CTA
-            bestW = (n + 31) / 32; bestRows = n; bestCols = n; bestT = cost(bestW, n); bestN = 1;
-        }
-        for (int W = std::min(3, Wt); W <= Wt; ++W) {
-            const int rows_out = 32 * W - halo;
-            if (rows_out < 16 || rows_out >= n) continue;
-            const int nrt = (n + rows_out - 1) / rows_out;
-            if (nrt > c->sm_count) continue;
-            const int maxct = std::max(1, std::min(c->sm_count / nrt, n / 64));
-            for (int nct = 1; nct <= maxct; ++nct) {
-                int tc = (n + nct - 1) / nct;
-                tc = (tc + 15) / 16 * 16;
-                if (T.gs_tile_cols > 0) tc = std::min(n, T.gs_tile_cols);
-                const bool full = tc >= n;
-                const int t = cost(W, (full ? n : tc + halo));
-                const int ncta = nrt * ((n + tc - 1) / tc);
-                if (t < bestT || (t == bestT && ncta < bestN)) {
-                    bestT = t; bestN = ncta; bestW = W; bestRows = rows_out; bestCols = full ? n : tc;
-                }
-            }
-        }
-        L.tile_warps = bestW;
-        L.tile_rows = bestRows;
-        L.tile_cols = bestCols;
-        const bool exact1 = bestRows >= n;
-        L.halo_y = exact1 ? 0 : halo;
-        L.halo_x = bestCols >= n ? 0 : halo;
-        if (getenv("SPP_DEBUG_TILES"))
-            fprintf(stderr, "[spp] level %d n=%d rho=%.4f halo=%d: warps %d tile %dx%d (+%d,%d) cost %d chunks, %d CTAs\n",
-                    l, n, rho, halo, L.tile_warps, L.tile_rows, L.tile_cols, L.halo_y, L.halo_x, bestT, bestN);
+        if (!plan_tiles(c, n, n, halo, true, L)) L.tile_warps = 0;   // no tiling: exact chain
     }
     return cudaSuccess;
 }

@@ -15,32 +15,32 @@ __global__ void k_coef_level(int N, int nl, int step, long Pl, double eps, doubl
                              double *aE, double *aN, double *rr, double *ca, double *cn, double *cd);
 __global__ void k_level0_1d(int N, double hx, double Hx, double hy, double Hy, const double *aW,
                             const double *aS, double *lW, double *lS, double *hb, double *kb);
-__global__ void k_pack(int m, long P, const double *src, double *dst);
-__global__ void k_unpack(int m, long P, const double *src, double *dst);
+__global__ void k_pack(int m, long P, const double *src, double *dst, int j0, int nrows);
+__global__ void k_unpack(int m, long P, const double *src, double *dst, int j0, int nrows);
 __global__ void k_spmv(int m, long P, const double *z, const double *aE, const double *aN,
                        const double *rr, const double *aW, const double *aS, int weighted, double *w,
-                       const double *v0, double *part);
+                       const double *v0, double *part, int j0, int nrows);
 __global__ void k_resid_stats(int m, long P, const double *f, const double *Au, const double *aE,
                               const double *aN, const double *rr, const double *aW, const double *aS,
-                              double *part4);
+                              double *part4, long pstride, int j0, int nrows);
 __global__ void k_rhs(int m, long P, const double *f, const double *aE, const double *aN,
                       const double *rr, const double *aW, const double *aS, int weighted,
-                      double *out, double *part);
+                      double *out, double *part, int j0, int nrows);
 __global__ void k_scale(long n2, double *x, double alpha);
 __global__ void k_mgs(long n2, double *w, const double *x, const double *part_in, double *hslot,
-                      const double *y, double *part_out);
-__global__ void k_normalize(long n2, const double *w, const double *part_in, double *hslot, double *v);
+                      const double *y, double *part_out, int nparts);
+__global__ void k_normalize(long n2, const double *w, const double *part_in, double *hslot, double *v, int nparts);
 __global__ void k_update_x(long n2, int k, const double *const *Z, const double *y, double *x);
 __global__ void k_corner_rhs(int N, long P, long P0, const double *v, const double *z,
                              const double *aE, const double *aN, const double *rr, const double *aW,
                              const double *aS, const double *hb, const double *kb, int weighted,
-                             double *bc, double *part, double *bc2, const double *cd, int scale2);
+                             double *bc, double *part, double *bc2, const double *cd, int scale2, int j0, int j1);
 __global__ void k_mg_resid(int nl, long Pv, long Pc, double *z, const double *e, const double *b,
                            const double *aE, const double *aN, const double *rr, const double *aW,
                            const double *aS, const double *hb, const double *kb, double *rho,
                            double *part);
 __global__ void k_prolong_add(int nl, long Pv, double *e, const double *ec, long Pcv);
-__global__ void k_corner_out(int n, long P0, const double *zc, long P, double *z, const MGState *ms);
+__global__ void k_corner_out(int n, long P0, const double *zc, long P, double *z, const MGState *ms, int j0, int j1);
 __global__ void k_pack_level(int nl, long Pv, const double *src, double *dst);
 __global__ void k_unpack_level(int nl, long Pv, const double *src, double *dst);
 

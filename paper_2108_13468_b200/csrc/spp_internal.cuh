@@ -20,6 +20,7 @@
 
 namespace spp {
 
+struct Dist;                             // row-strip decomposition (dist.cuh)
 constexpr int kMaxLevels = 24;
 constexpr int kWarp = 32;
 constexpr int kRedBlocks = 592;      // 4 x 148 SMs: fixed grid for deterministic reductions
@@ -68,19 +69,34 @@ struct Level {
     // columns recomputed above / right of each tile (-1: none certifiable -> exact chained sweep)
     int tile_rows = 0, tile_cols = 0, tile_warps = 0, halo_x = 0, halo_y = 0;
     double contraction = 0.0;            // max (aE + aN) / D over the level
+    int halo_cert = -1;                  // certified halo depth of the level (-1: none)
+    // row strip of a distributed solve: this rank owns rows slo..shi of the level
+    // (1..n on one GPU).  sdist: the level's GS sweeps run on the strip (own rows plus shalo
+    // halo rows above, whose right-hand side comes from the strip above) with the tile plan
+    // above; otherwise the level runs whole on every rank.
+    int slo = 1, shi = 0, shalo = 0;
+    bool sdist = false;
 };
 
 // corner GS sweep arguments (k_mg.cu)
 // downstream sweep on [1, nl]^2 (k_mg.cu): y = q + ca y_E + cn y_N, z = cd y (y-form) or z = y
 struct WaveArgs {
-    int nl; long pv, pc;
+    int nl; long pv, pc;                 // nl: columns 1..nl of the swept block
     int ioff, joff;                      // node (i, j) lives at array index (i+ioff, j+joff)
     const double *q, *ca, *cn, *cd;
     double *z;
     int rows_out, cols_out, halo_y, halo_x;
     int *chain_flags; double *chain_buf; long chain_ld;   // exact chained mode
     long long *prof;                     // SPP_WAVE_PROF builds only
-
+    // rows of the block: 1..nr_out are output rows, nr_out+1..nr the halo rows above them that a
+    // row strip of a distributed solve recomputes from the strip above's right-hand side
+    // (DESIGN.md §9); nr = nr_out = nl for a whole level (0 = that default)
+    int nr, nr_out;
+    // exact chained mode across row strips: the first CTA strip's North inflow (the bottom row of
+    // the strip above, in the chain buffer's order; nullptr = zero inflow) and whether the last
+    // CTA strip publishes its bottom row into chain slot gridDim.y - 1
+    const double *ext_in;
+    int chain_last;
 };
 
 // tunables (defaults in spp_create; overridable through SPP_TUNE="key=val,..." for experiments)
@@ -91,6 +107,7 @@ struct Tune {
     int sweep_warps = 2;       // warps per CTA of the exact chained sweep (M_II; 2 measured best)
     int gs_lag = 5;            // tiling model: chunk-times each extra warp adds
     int coarse_max = 16;       // levels with n <= this run as one fused single-CTA V-cycle (16 measured best)
+    int dist_levels = 2;       // row strips: corner levels whose sweeps run on the strips
 };
 
 struct ProfRec { int64_t launches = 0; double ms = 0, bytes = 0; };
@@ -127,6 +144,8 @@ struct Ctx {
     double *tX = nullptr, *tY = nullptr, *kapX = nullptr, *kapY = nullptr;
     LineChain chX{}, chY{};
     std::vector<LineChunk> chunks; LineChunk *d_chunks = nullptr; int nchunks_alloc = 0;
+    std::vector<double> kx, ky;            // per-line chain contractions kappa_l (host copies)
+    int line_lo[2] = {-1, -1}, line_hi[2] = {-2, -2};   // owned lines per chain (-1: all, one GPU)
     int lines_threads = 256;
     // Krylov
     std::vector<double *> V, Z;
@@ -173,16 +192,29 @@ struct Ctx {
     int use_graph = 1;
     int no_lines_tma = 0;                  // SPP_NO_LINES_TMA=1: LSU-loaded line kernel
     int mg_zform = 1;                      // corner GS sweeps in z-form (SPP_MG_YFORM=1: y-form)
+    // row strips: the decomposition this context is one strip of (nullptr: one
+    // GPU), the strip's rank, and the partial-sum segments per reduction slot (one per strip)
+    Dist *dist = nullptr;
+    int rank = 0, nparts = 1;
 };
 
 // kernels / launchers (defined in the .cu files)
 cudaError_t setup_global(Ctx *c, const double *c1, const double *c2, const double *r);
+spp_status setup_2d_ctx(Ctx *c, const double *c1, const double *c2, const double *r, spp_mem mem);
+cudaError_t ensure_vectors(Ctx *c, int k);
+bool strip_partition(int N, int P, std::vector<int> &J);
+bool check_partition(int N, const std::vector<int> &J, int *Pb, std::string *why);
 cudaError_t setup_levels(Ctx *c, const double *c1, const double *c2, const double *r);
 cudaError_t setup_lines(Ctx *c);
-void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double> &ky);
+void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double> &ky, const int lo[2],
+                 const int hi[2], int budget);
+std::vector<LineChunk> plan_chain_chunks(int chain, const std::vector<double> &k, int l0, int l1, int budget);
 // corner multigrid (k_mg.cu)
 void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, double *enew, const double *ec,
                bool bscaled = false);
+void launch_gs_prep(Ctx *c, int l, const double *b, const double *eold, const double *ec, bool bscaled);
+void launch_gs_sweep(Ctx *c, int l, const double *q, double *enew);
+double *vcycle(Ctx *c, int l, const double *R, bool rs);
 void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform, int cls, double bytes);
 long wave_chain_ctas(const Ctx *c, long rows);
 void launch_ycoef(Ctx *c, int nl, long pc, const double *aE, const double *aN, const double *cd, double *ya, double *yn);
@@ -193,7 +225,9 @@ const CUtensorMap *tmap2d(Ctx *c, const void *base, unsigned long long d0, unsig
 void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e, bool rs_in = false, bool scale_out = false);
 void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew, const double *b, double *rho,
                          double *part, const MGState *ms = nullptr);
+void launch_lines(Ctx *c, const double *v, double *z);
 cudaError_t setup_mg_tiles(Ctx *c);
+bool plan_tiles(const Ctx *c, int n, int rows, int halo, bool whole, Level &L);
 void launch_scale_cd(Ctx *c, int l, const double *b, double *q);
 bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs = false);
 

@@ -82,3 +82,43 @@ def test_batch1d_reference_arm_and_rank_slices():
     e0, e1 = bench.batch1d_inputs(32, 0), bench.batch1d_inputs(32, 32)
     assert (e_all[:32] == e0).all() and (e_all[32:] == e1).all()
     assert (1e-8 <= e_all).all() and (e_all <= 1e-2).all()
+
+
+def _plan_worker(rank, world, port, N, out):
+    """One rank of the row-strip orchestration on CPU (gloo): it knows only its own [j0, j1) from
+    the default partition, gathers the others' like spp_create_dist does, builds its own
+    exchange schedule, and the ranks cross-check that every block one sends is the block the
+    other receives, in the same position of the same step."""
+    import numpy as np
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    import paper_2108_13468_b200 as spp
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    J = spp.spp_strip_partition(N, world)
+    mine = (int(J[rank]), int(J[rank + 1]))
+    got = [None] * world
+    dist.all_gather_object(got, mine)
+    Jg = [g[0] for g in got] + [got[-1][1]]
+    plan = spp.spp_dist_plan(N, world, np.array(Jg, np.int32), 2, 64, 56, rank)
+    plans = [None] * world
+    dist.all_gather_object(plans, plan.tolist())
+    ok = list(Jg) == list(J)
+    for a in range(world):
+        for b in range(world):
+            if a == b:
+                continue
+            sends = [tuple(x) for x in plans[a] if x[1] == a and x[2] == b]
+            recvs = [tuple(x) for x in plans[b] if x[1] == a and x[2] == b]
+            ok = ok and sends == recvs and len(sends) > 0
+    out[rank] = (ok, len(plan))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_row_strip_schedule_matches_across_ranks_gloo(world):
+    import torch.multiprocessing as mp
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_plan_worker, args=(world, _free_port(), 512, out), nprocs=world, join=True)
+    assert all(out[r][0] for r in range(world)), dict(out)
+    assert all(out[r][1] > 0 for r in range(world))
