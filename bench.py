@@ -7,7 +7,8 @@ paper's time-to-solution.
 
 Default workload: cfg4 (B:10), 4096^2 Shishkin mesh, eps = 1e-8, variable convection, seeded
 random f, Jacobi-weighted rtol 1e-8.  Prints ONE JSON line (rank 0).
-For N > 1 (torchrun) every rank solves its own replica (weak scaling).
+For N > 1 (torchrun) the one cfg4 solve is split into row strips, one per GPU, over NCCL
+(strong scaling).
 """
 from __future__ import annotations
 
@@ -131,7 +132,7 @@ def run_reference(args, rank, world):
                 "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
                 "config": {"workload": f"cfg1-batch (bounded sample of the {args.batch}-problem batch)"},
-                "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "host_cores": os.cpu_count(), "kind": "oracle",
                                  "sample": f"{done} problems of the batch in {args.steps} steps of ~10 s"},
                 "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     cfg = si.config(args.config, N=args.n, eps=args.eps)
@@ -154,10 +155,10 @@ def run_reference(args, rank, world):
     dt = (time.perf_counter() - t0) / args.steps
     val = cfg.unknowns / dt
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": _workload(cfg), "N": N, "unknowns": cfg.unknowns, "iters": res["iters"]},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "host_cores": os.cpu_count(), "kind": "oracle",
                              "sample": f"one full {cfg.name} solve (setup + FGMRES, {res['iters']} iterations) "
                                        f"per step, single-threaded C oracle"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -276,7 +277,7 @@ def run_batch1d(args, rank, world):
                              "max": int(res.iters.max())}, "converged": int(res.converged.sum()),
                    "setup_s": res.stats["setup_s"], "solve_s": res.stats["solve_s"],
                    "l2": "per-step setup + solve; per-CTA Krylov basis re-read from L1/L2",
-                   "parallelism": "independent problems per GPU" if world > 1 else "single GPU"},
+                   "parallelism": "replicas: an independent batch per GPU (weak scaling)" if world > 1 else "single GPU"},
         "roofline": {"kernel": "k_solve1d_batch", "bound": "hbm", "achieved": alg / (solve_ms * 1e-3) / 1e9,
                      "peak": peak, "unit": "GB/s", "frac": alg / (solve_ms * 1e-3) / 1e9 / peak, "traffic": None,
                      "peak_kind": peak_kind, "avg_launch_ms": solve_ms, "algorithmic_bytes_per_launch": alg},
@@ -287,7 +288,7 @@ def run_batch1d(args, rank, world):
         line["e2e"] = e2e
     if not args.no_cpu_baseline:
         done, dt, its = batch1d_oracle_sample(eps, first)
-        line["cpu_baseline"] = {"value": done * (BATCH_N - 1) / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+        line["cpu_baseline"] = {"value": done * (BATCH_N - 1) / dt, "unit": UNIT, "cores": 1, "host_cores": os.cpu_count(), "kind": "oracle",
                                 "sample": f"the first {done} problems of the batch, {dt:.1f} s"}
     return line
 
@@ -317,7 +318,7 @@ def cpu_baseline(cfg):
     res = P.solve(f, weighted=cfg.weighted, stop_abs=cfg.stop_abs, tol=cfg.tol)
     dt = time.perf_counter() - t0
     P.close()
-    return {"value": cfg.unknowns / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+    return {"value": cfg.unknowns / dt, "unit": UNIT, "cores": 1, "host_cores": os.cpu_count(), "kind": "oracle",
             "sample": f"one full {cfg.name} solve (setup + FGMRES, {res['iters']} iterations), {dt:.2f} s"}
 
 
@@ -397,12 +398,32 @@ def run_sweep(args, rank, world):
                                    f"(eps {CFG5_EPS}), round-robin over ranks", "N": N,
                        "unknowns": total, "max_iters": args.max_iters,
                        "iters_per_eps": {k: iters[k] for k in sorted(iters, key=float, reverse=True)},
-                       "parallelism": f"independent problems over {world} GPU(s)",
+                       "parallelism": f"task-parallel: independent eps problems over {world} GPU(s) (not the "
+                                      f"row-strip decomposition of one solve; that is the default --config cfg4)",
                        "l2": "inputs larger than L2"},
             "clocks": clocks}
 
 
+def nccl_comm(rank, world):
+    """An NCCL communicator for the row strips: rank 0 makes the id, torch.distributed carries it."""
+    import torch.distributed as dist
+    import paper_2108_13468_b200 as spp
+    obj = [spp.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return spp.nccl_comm_create(obj[0], world, rank)
+
+
+def strip_rows(N, rank, world):
+    """This rank's interior rows [j0, j1) of the default row strips (spp_strip_partition)."""
+    import paper_2108_13468_b200 as spp
+    J = spp.spp_strip_partition(N, world)
+    return int(J[rank]), int(J[rank + 1])
+
+
 def run_ours(args, rank, world):
+    """One GPU: spp_create + spp_solve.  N GPUs (torchrun): the row-strip decomposition of the
+    same solve, one strip per rank over NCCL (strong scaling: the
+    job solves the one cfg4 problem)."""
     import torch
     import paper_2108_13468_b200 as spp
 
@@ -413,36 +434,63 @@ def run_ours(args, rank, world):
     x = spp.spp_shishkin_mesh(N, cfg.eps, cfg.sigma, cfg.beta_x)
     y = spp.spp_shishkin_mesh(N, cfg.eps, cfg.sigma, cfg.beta_y)
     c1, c2, r, f = si.sample_2d(cfg, x, y)
-    host = [np.ascontiguousarray(a).ravel() for a in (c1, c2, r, f)]
+    j0, j1 = strip_rows(N, rank, world) if world > 1 else (1, N)
+    rows = slice(j0 - 1, j1 - 1)                         # this rank's rows of the (N-1)^2 grid
+    host = [np.ascontiguousarray(a[rows]).ravel() for a in (c1, c2, r, f)]
+    nloc = (j1 - j0) * m
     d_c1, d_c2, d_r, d_f = [torch.from_numpy(a).to(dev) for a in host]
     u = torch.empty_like(d_f)
     o = spp.spp_default_options(2)
     o.stop = spp.SPP_STOP_REL_JACOBI if cfg.weighted else (spp.SPP_STOP_ABS_L2 if cfg.stop_abs else spp.SPP_STOP_REL_L2)
     o.tol = cfg.tol
     stream = torch.cuda.current_stream(dev)
-    S = spp.Solver(2, N, cfg.eps, x, y, d_c1, d_c2, d_r, options=o, stream=stream)
+    comm = None
+    if world > 1:
+        comm = nccl_comm(rank, world)
+        S = spp.DistSolver(N, cfg.eps, x, y, d_c1, d_c2, d_r, j0, j1, comm, rank, world, options=o, stream=stream)
+    else:
+        S = spp.Solver(2, N, cfg.eps, x, y, d_c1, d_c2, d_r, options=o, stream=stream)
+
+    nsolves = [0]
 
     def step(c1_, c2_, r_, f_, u_):
+        nsolves[0] += 1
         S.setup(c1_, c2_, r_)
         return S.solve(f_, u_)
+
+    def check(res):
+        """every timed solve must converge (ADVICE: a non-converged solve is not a valid step)"""
+        assert res.status == spp.SPP_OK and res.stats["converged"] == 1, res.stats
 
     # warm-up exactly as the timed steps run (this also captures the corner-solve CUDA graph),
     # then one more untimed step with every kernel class profiled, to find the dominant class
     res = None
     for _ in range(args.warmup):
         res = step(d_c1, d_c2, d_r, d_f, u)
+        check(res)
+    iters_ref = res.stats["iters"]
     S.profile_reset()
     S.profile_enable(1)
     res = step(d_c1, d_c2, d_r, d_f, u)
-    prof = S.profile()
+    prof_all = S.profile()
+    prof = {k: v for k, v in prof_all.items() if k not in ("exchange",)}
     dom = max(prof, key=lambda k: prof[k]["ms"])
-    dom_idx = list(prof).index(dom)
+    dom_idx = list(prof_all).index(dom)
+    tot_ms = sum(v["ms"] for v in prof_all.values())
     if args.profile_all and rank == 0:
-        tot = sum(v["ms"] for v in prof.values())
-        for k, v in prof.items():
+        for k, v in prof_all.items():
             if v["launches"]:
-                print(f"[prof] {k:18s} launches={v['launches']:6d} ms={v['ms']:9.3f} ({100*v['ms']/tot:5.1f}%) "
+                print(f"[prof] {k:18s} launches={v['launches']:6d} ms={v['ms']:9.3f} ({100*v['ms']/tot_ms:5.1f}%) "
                       f"GB/s={v['bytes']/max(v['ms'],1e-9)/1e6:8.1f}", file=sys.stderr)
+    # per-class roofline fractions (north_star: stencil, smoother and vector kernels), from the
+    # profiled step's CUDA events: algorithmic bytes / device time
+    peak, peak_kind = _peaks()
+    classes = {}
+    for k, v in prof_all.items():
+        if v["launches"] and v["ms"] > 0:
+            gbs = v["bytes"] / (v["ms"] * 1e-3) / 1e9
+            classes[k] = {"launches": v["launches"], "ms": round(v["ms"], 4), "share": round(v["ms"] / tot_ms, 4),
+                          "achieved_gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
     S.profile_reset()
     S.profile_enable(0)          # the timed region runs exactly as a user's solve (no event brackets)
 
@@ -453,14 +501,17 @@ def run_ours(args, rank, world):
     clk.start()
     l0 = S.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    iters = []
+    results = []
     e0.record(stream)
     for _ in range(args.steps):
-        res = step(d_c1, d_c2, d_r, d_f, u)
-        iters.append(res.stats["iters"])
+        results.append(step(d_c1, d_c2, d_r, d_f, u))
     e1.record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
+    for rr in results:
+        check(rr)
+        assert rr.stats["iters"] == iters_ref, (rr.stats["iters"], iters_ref)
+    res = results[-1]
     launches = S.kernel_launches() - l0
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, dev)
     if world > 1:
@@ -480,7 +531,7 @@ def run_ours(args, rank, world):
     e2e = None
     if not args.no_e2e:
         hp = [torch.from_numpy(a).pin_memory() for a in host]
-        hu = torch.empty(m * m, dtype=torch.float64).pin_memory()
+        hu = torch.empty(nloc, dtype=torch.float64).pin_memory()
         step(hp[0], hp[1], hp[2], hp[3], hu)
         torch.cuda.synchronize()
         if world > 1:
@@ -493,37 +544,51 @@ def run_ours(args, rank, world):
         e1.record(stream)
         torch.cuda.synchronize()
         ems = max_over_ranks(max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / ne, world, dev)
-        e2e = {"value": cfg.unknowns * world / (ems * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": 4 * m * m * 8, "d2h_bytes_per_step": m * m * 8, "ms_per_step": ems}
+        e2e = {"value": cfg.unknowns / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": 4 * nloc * 8, "d2h_bytes_per_step": nloc * 8, "ms_per_step": ems}
+    info = S.dist_info()
+    S.close()
+    if comm is not None:
+        spp.nccl_comm_destroy(comm)
 
     if rank != 0:
         return None
-    peak, peak_kind = _peaks()
     avg_ms = prof["ms"] / max(prof["launches"], 1)
     avg_bytes = prof["bytes"] / max(prof["launches"], 1)
     achieved = avg_bytes / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists():
+    if tf.exists() and world == 1:
         try:
             traffic = json.loads(tf.read_text()).get(f"{cfg.name}:{dom}")
         except Exception:
             traffic = None
     line = {
-        "metric": METRIC, "value": cfg.unknowns * world / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "metric": METRIC, "value": cfg.unknowns / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": _workload(cfg), "N": N, "unknowns": cfg.unknowns,
-                   "iters_per_solve": iters[-1], "mg_cycles_per_apply": [res.stats["mg_cycles_min"], res.stats["mg_cycles_max"]],
+                   "iters_per_solve": res.stats["iters"],
+                   "mg_cycles_per_apply": [res.stats["mg_cycles_min"], res.stats["mg_cycles_max"]],
                    "time_to_solution_s": ms * 1e-3, "setup_s": res.stats["setup_s"],
+                   "true_res_jacobi_rel": res.stats["true_res_jacobi_rel"],
                    "l2": "inputs larger than L2 (each grid function 134 MB > 126 MB L2)",
-                   "parallelism": "replicas" if world > 1 else "single GPU"},
+                   "parallelism": (f"row strips over {world} GPUs (NCCL; rows [{j0},{j1}) on rank 0; "
+                                   f"{info['strip_levels']} corner levels on strips)") if world > 1 else "single GPU"},
         "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "avg_launch_ms": avg_ms, "algorithmic_bytes_per_launch": avg_bytes},
-        "gpu_launches": int(launches),
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": "profiles/traffic.json (ncu --set full capture of this kernel class)"
+                                       if traffic is not None else None,
+                     "peak_kind": peak_kind, "avg_launch_ms": avg_ms, "algorithmic_bytes_per_launch": avg_bytes,
+                     "classes": classes},
+        "gpu_launches": int(launches // max(args.steps, 1)),
         "clocks": clocks,
     }
+    if world > 1:
+        line["exchange"] = {"blocks_per_solve": info["xfers"] / nsolves[0], "MB_per_solve": info["bytes"] / nsolves[0] / 1e6,
+                            "steps_per_solve": info["exchanges"] / nsolves[0],
+                            "note": "rank 0's NCCL send/recv blocks incl. the setup's coefficient all-gather; the "
+                                    "'exchange' class in roofline.classes is its device time"}
     if e2e:
         line["e2e"] = e2e
     if not args.no_cpu_baseline:

@@ -181,8 +181,9 @@ SPP_API int32_t spp_mg_level_n(const spp_ctx *c, int32_t l);
  * algorithmic bytes moved accumulated since the last reset.
  * Classes: 0 spmv, 1 sweep_I, 2 lines_XY, 3 mg_sweep (tiled GS sweeps of the corner levels),
  * 4 mg_resid_restrict, 5 mg_prolong (GS right-hand side + prolongation), 6 mg_update,
- * 7 krylov_vec (MGS and vector ops), 8 setup, 9 other, 10 mg_coarse (fused coarse V-cycle). */
-#define SPP_PROF_CLASSES 11
+ * 7 krylov_vec (MGS and vector ops), 8 setup, 9 other, 10 mg_coarse (fused coarse V-cycle),
+ * 11 exchange (row strips: the copies / NCCL group of one exchange step, on the strip's stream). */
+#define SPP_PROF_CLASSES 12
 SPP_API spp_status spp_profile_enable(spp_ctx *c, int32_t enable);
 SPP_API spp_status spp_profile_reset(spp_ctx *c);
 SPP_API spp_status spp_profile_get(const spp_ctx *c, int32_t k, int64_t *launches, double *ms, double *bytes);

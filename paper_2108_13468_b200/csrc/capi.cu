@@ -38,7 +38,7 @@ namespace spp {
 // ------------------------------------------------------------------------------------------ profiling
 static const char *kProfNames[SPP_PROF_CLASSES] = {"spmv", "sweep_I", "lines_XY", "mg_sweep",
                                                    "mg_resid_restrict", "mg_prolong", "mg_update",
-                                                   "krylov_vec", "setup", "other", "mg_coarse"};
+                                                   "krylov_vec", "setup", "other", "mg_coarse", "exchange"};
 
 ProfScope::ProfScope(Ctx *c_, int cls_, double bytes_) : c(c_), cls(cls_), bytes(bytes_)
 {
@@ -61,7 +61,7 @@ ProfScope::~ProfScope()
     c->pend.push_back({cls, a, b, bytes});
 }
 
-static void prof_collect(Ctx *c)
+void prof_collect(Ctx *c)
 {
     if (c->pend.empty()) { c->ev_used = 0; return; }
     cudaEventSynchronize(c->pend.back().b);
@@ -750,7 +750,7 @@ spp_status spp_profile_enable(spp_ctx *cx, int32_t en)
 {
     Ctx *c = (Ctx *)cx;
     if (!c) return SPP_E_ARG;
-    c->prof_on = en ? (en == 1 ? 0x7ff : en) : 0;
+    c->prof_on = en ? (en == 1 ? 0xfff : en) : 0;
     return SPP_OK;
 }
 spp_status spp_profile_reset(spp_ctx *cx)

@@ -299,6 +299,10 @@ spp_status exchange_rows(Dist *d, const std::vector<Xfer> &xs)
 {
     d->nexch++;
     if (xs.empty()) return SPP_OK;
+    double bytes = 0;
+    for (const Xfer &x : xs)
+        if (d->me < 0 || x.src == d->me || x.dst == d->me) bytes += 8.0 * x.width * x.rows;
+    ProfScope ps(d->cx[0], 11, bytes);
     if (d->me < 0) {
         for (const Xfer &x : xs) {
             double *sp = role_ptr(d->cx[x.src], x.role, x.slot) + x.soff;
@@ -736,6 +740,7 @@ spp_status solve_dist(Ctx *c0, const double *f, double *u, spp_mem mem, double *
                 if (Ctx *c = d->ctx_of(r)) {
                     int j0, nr;
                     own(r, j0, nr);
+                    ProfScope ps(c, 0, 48.0 * m * nr);
                     k_spmv<<<red_grid((long)m * nr), kRedThreads, 0, c->st>>>(m, c->P, c->Z[k], c->aE, c->aN, c->rr,
                         c->aW, c->aS, weighted, c->w, c->V[0], pseg(c, 0), j0, nr);
                     c->launches++;
@@ -750,6 +755,7 @@ spp_status solve_dist(Ctx *c0, const double *f, double *u, spp_mem mem, double *
                         long off, cnt;
                         flat(r, off, cnt);
                         const double *y = j <= k ? c->V[j] + off : c->w + off;
+                        ProfScope ps(c, 7, 32.0 * cnt);
                         k_mgs<<<red_grid(cnt), kRedThreads, 0, c->st>>>(cnt, c->w + off, c->V[j - 1] + off, pslot(c, j - 1),
                                                                        c->dscal + (j - 1), y, pseg(c, j), P);
                         c->launches++;
@@ -873,11 +879,9 @@ spp_status solve_dist(Ctx *c0, const double *f, double *u, spp_mem mem, double *
         st->res0 = beta; st->res_final = resf;
         st->setup_s = lead->setup_ms * 1e-3; st->solve_s = ms * 1e-3;
     }
-    for (Ctx *c : d->cx) {
-        const cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return dfail(d, SPP_E_CUDA, std::string("solve: ") + cudaGetErrorString(e));
-        (void)c;
-    }
+    for (Ctx *c : d->cx) prof_collect(c);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return dfail(d, SPP_E_CUDA, std::string("solve: ") + cudaGetErrorString(e));
     return converged ? SPP_OK : SPP_NOT_CONVERGED;
 }
 

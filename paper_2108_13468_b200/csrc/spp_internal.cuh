@@ -232,6 +232,7 @@ void launch_scale_cd(Ctx *c, int l, const double *b, double *q);
 bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs = false);
 
 // profiling helpers
+void prof_collect(Ctx *c);
 struct ProfScope {
     Ctx *c; int cls; double bytes; cudaEvent_t a = nullptr;
     ProfScope(Ctx *c_, int cls_, double bytes_);
