@@ -974,7 +974,12 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
     double *A = c->V[0], *B = c->Z[0];
     auto pk = [&](const double *src, double *dst) { k_pack<<<nblk(mm), 256, 0, c->st>>>(m, c->P, src, dst, 1, m); };
     auto up = [&](const double *src, double *dst) { k_unpack<<<nblk(mm), 256, 0, c->st>>>(m, c->P, src, dst, 1, m); };
-    if (s == SPP_STAGE_MATVEC) {
+    if (s == SPP_STAGE_MII_JACOBI) {
+        pk(in, A);
+        pk(out, B);
+        launch_mii(c, A, B, false);                     // the solve's Jacobi-mode call (z-form)
+        up(B, out);
+    } else if (s == SPP_STAGE_MATVEC) {
         pk(in, A);
         k_spmv<<<kRedBlocks, kRedThreads, 0, c->st>>>(m, c->P, A, c->aE, c->aN, c->rr, c->aW, c->aS, 0, B, nullptr, nullptr, 1, m);
         up(B, out);
@@ -1080,6 +1085,32 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
             k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, out, e);
             k_prolong_add<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, e, C.e, C.pitch);
             k_unpack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, e, out);
+        } else if (s == SPP_STAGE_POST_SMOOTH) {
+            // the V-cycle's post-smoothing call: b stored as b/D, e, e_c in the level buffers the
+            // product uses (lev[l].e, lev[l+1].q), prolongation fused into the sweep's rhs kernel
+            if (l + 1 >= c->L) FAIL(c, SPP_E_ARG, "no coarser level");
+            if (!c->mg_zform) FAIL(c, SPP_E_STATE, "POST_SMOOTH drives the z-form path");
+            Level &C = c->lev[l + 1];
+            double *bq = c->T1;
+            CK(c, cudaMemsetAsync(bq, 0, sizeof(double) * Lv.elems, c->st));
+            k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in, bq);
+            k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in + nn, e);
+            k_pack_level<<<nblk((long)C.n * C.n), 256, 0, c->st>>>(C.n, C.pitch, in + 2 * nn, C.q);
+            launch_scale_cd(c, l, bq, bq);                  // b -> b/D (in place, element-wise)
+            launch_gs(c, l, 1, bq, e, Lv.q, C.q, true);
+            k_unpack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, Lv.q, out);
+        } else if (s == SPP_STAGE_RESID_RESTRICT) {
+            // the V-cycle's call: R read as R/D, b_c written divided by D_c (z-form)
+            if (l + 1 >= c->L) FAIL(c, SPP_E_ARG, "no coarser level");
+            if (!c->mg_zform) FAIL(c, SPP_E_STATE, "RESID_RESTRICT drives the z-form path");
+            Level &C = c->lev[l + 1];
+            double *Rq = c->T1;
+            CK(c, cudaMemsetAsync(Rq, 0, sizeof(double) * Lv.elems, c->st));
+            k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in, Rq);
+            k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in + nn, e);
+            launch_scale_cd(c, l, Rq, Rq);
+            launch_resid_restrict(c, l, Rq, e, true, true);
+            k_unpack_level<<<nblk((long)C.n * C.n), 256, 0, c->st>>>(C.n, C.pitch, C.b, out);
         } else if (s == SPP_STAGE_LEVEL_RESIDUAL) {
             k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in, b);
             k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in + nn, e);

@@ -275,6 +275,8 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
 #ifdef SPP_WAVE_PROF
     long long tp_spin = 0, tp_bar = 0, tp_steps = 0, tp_wb = 0;
     const long long tp0 = clock64();
+    unsigned long long gt0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
 #define SPP_TP(v) const long long v = clock64()
 #else
 #define SPP_TP(v)
@@ -409,8 +411,11 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
     }
 #ifdef SPP_WAVE_PROF
     if (lane == 0 && a.prof) {
-        long long *o = a.prof + 8 * ((blockIdx.y * gridDim.x + blockIdx.x) * 4 + w);
+        unsigned long long gt1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
+        long long *o = a.prof + 8 * ((blockIdx.y * gridDim.x + blockIdx.x) * 8 + w);
         o[0] = clock64() - tp0; o[1] = tp_spin; o[2] = tp_bar; o[3] = tp_steps; o[4] = tp_wb; o[5] = nch;
+        o[6] = (long long)gt0; o[7] = (long long)gt1;
     }
 #endif
 }
@@ -418,21 +423,29 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
 static size_t wave_smem(int warps, bool yform) { return sizeof(double) * (size_t)warps * WNS * wslot(yform) + 1024; }
 
 #ifdef SPP_WAVE_PROF
-// debugging build only: per-warp cycle breakdown of the first launch of each kind
-static void wave_prof_dump(Ctx *c, long long *prof, const char *what, int nctas)
+// debugging build only: per-warp cycle breakdown (spin = waits on the warp above / chain,
+// bar = waits on the TMA boxes, steps = the recurrence, wb = hand-offs) and the warps' start /
+// end times relative to the launch's first warp, for the SPP_WAVE_PROF_HIT-th launch (default 3)
+// over a level of SPP_WAVE_PROF_N columns (default: the corner, n)
+static void wave_prof_dump(Ctx *c, long long *prof, const char *what, int nctas, int nl)
 {
-    static int done_tiled = 0, done_chain = 0;
-    if (!what) return;
-    int &d = what[0] == 'c' ? done_chain : done_tiled;
-    if (d++) return;
-    const int nw = std::min(nctas, 16) * 4;
-    long long h[8 * 64];
-    cudaMemcpyAsync(h, prof, sizeof(long long) * 8 * nw, cudaMemcpyDeviceToHost, c->st);
+    static int hits = 0;
+    const char *en = getenv("SPP_WAVE_PROF_N"), *eh = getenv("SPP_WAVE_PROF_HIT");
+    const int want = en ? atoi(en) : c->n, hit = eh ? atoi(eh) : 3;
+    if (!what || nl != want || ++hits != hit) return;
+    const int nw = std::min(nctas, 512) * 8;
+    std::vector<long long> h(8 * (size_t)nw);
+    cudaMemcpyAsync(h.data(), prof, sizeof(long long) * 8 * nw, cudaMemcpyDeviceToHost, c->st);
     cudaStreamSynchronize(c->st);
+    long long g0 = -1, g1 = 0;
     for (int k = 0; k < nw; ++k)
-        if (h[8 * k])
-            fprintf(stderr, "[wave-prof] %s cta %d warp %d: total %lld spin %lld bar %lld steps %lld wb %lld nch %lld\n",
-                    what, k / 4, k % 4, h[8 * k], h[8 * k + 1], h[8 * k + 2], h[8 * k + 3], h[8 * k + 4], h[8 * k + 5]);
+        if (h[8 * k]) { g0 = g0 < 0 ? h[8 * k + 6] : std::min(g0, h[8 * k + 6]); g1 = std::max(g1, h[8 * k + 7]); }
+    fprintf(stderr, "[wave-prof] %s n=%d: %d CTAs, first warp start -> last warp end %.2f us\n", what, nl, nctas, (g1 - g0) * 1e-3);
+    for (int k = 0; k < nw; ++k)
+        if (h[8 * k] && (k / 8 < 4 || k / 8 == nctas - 1))
+            fprintf(stderr, "[wave-prof]  cta %d warp %d: start %+.2f us end %+.2f us | cycles total %lld spin %lld bar %lld "
+                            "steps %lld wb %lld | nch %lld\n", k / 8, k % 8, (h[8 * k + 6] - g0) * 1e-3,
+                    (h[8 * k + 7] - g0) * 1e-3, h[8 * k], h[8 * k + 1], h[8 * k + 2], h[8 * k + 3], h[8 * k + 4], h[8 * k + 5]);
 }
 #endif
 
@@ -527,14 +540,15 @@ void launch_wave(Ctx *c, WaveArgs a, long rows_v, long rows_c, int warps, bool y
     ProfScope ps(c, cls, bytes);
 #ifdef SPP_WAVE_PROF
     static long long *prof = nullptr;
-    if (!prof) cudaMalloc(&prof, sizeof(long long) * 8 * 4 * 8192);
+    if (!prof) cudaMalloc(&prof, sizeof(long long) * 8 * 8 * 8192);
+    cudaMemsetAsync(prof, 0, sizeof(long long) * 8 * 8 * 8192, c->st);
     a.prof = prof;
 #endif
     if (yform) k_wave<true, false><<<grid, (2 * warps + 1) * 32, sm, c->st>>>(a, m);
     else k_wave<false, false><<<grid, (2 * warps + 1) * 32, sm, c->st>>>(a, m);
     c->launches++;
 #ifdef SPP_WAVE_PROF
-    wave_prof_dump(c, prof, a.nl >= c->n ? "tiled level 0" : nullptr, grid.x * grid.y);
+    wave_prof_dump(c, prof, "tiled", grid.x * grid.y, a.nl);
 #endif
     dbg_sync(c, "k_wave tiled");
 }
@@ -566,7 +580,8 @@ void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform,
     ProfScope ps(c, cls, bytes);
 #ifdef SPP_WAVE_PROF
     static long long *prof = nullptr;
-    if (!prof) cudaMalloc(&prof, sizeof(long long) * 8 * 4 * 8192);
+    if (!prof) cudaMalloc(&prof, sizeof(long long) * 8 * 8 * 8192);
+    cudaMemsetAsync(prof, 0, sizeof(long long) * 8 * 8 * 8192, c->st);
     a.prof = prof;
 #endif
     const cudaError_t le = yform
@@ -575,7 +590,7 @@ void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform,
     if (le != cudaSuccess && c->sticky == cudaSuccess) c->sticky = le;
     c->launches++;
 #ifdef SPP_WAVE_PROF
-    wave_prof_dump(c, prof, "chain", ncta);
+    wave_prof_dump(c, prof, "chain", ncta, a.nl);
 #endif
     dbg_sync(c, "k_wave chain");
 }

@@ -121,6 +121,33 @@ def test_multigrid_pieces(name, N, eps):
             assert relmax(host(out), P.prolong_add(l, ec, e0)) <= 1e-14, l
 
 
+@pytest.mark.parametrize("name,N,eps", [("cfg4", 128, 1e-8), ("cfg5", 256, 1e-2), ("cfg3", 256, 1e-6)])
+def test_product_path_hooks(name, N, eps):
+    """The hooks that drive exactly the BASELINE-mode kernels and arguments (spp.h): the z-form
+    M_II chain of the Jacobi-weighted solve (input D v, reading R11), the post-smoothing with the
+    prolongation fused into the sweep's right-hand-side kernel, and the fused residual +
+    restriction with the V-cycle's z-form scalings -- each against the oracle's definition."""
+    cfg, x, y, ins, S, P = make(name, N, eps)
+    m = N - 1
+    D = P.coef()["D"]
+    q = si.random_field(3, (m, m))
+    zi = torch.zeros(m * m, dtype=torch.float64, device="cuda")
+    S.apply_stage("MII_JACOBI", dev(q), zi)
+    assert relmax(host(zi), P.stage_I(D * q)) <= 1e-12
+    for l in range(P.levels - 1):
+        nl, nc = P.level_n(l), P.level_n(l + 1)
+        b = si.random_field(50 + l, (nl, nl))
+        e0 = si.random_field(60 + l, (nl, nl))
+        ec = si.random_field(70 + l, (nc, nc))
+        out = torch.zeros(nl * nl, dtype=torch.float64, device="cuda")
+        S.apply_stage("POST_SMOOTH", torch.cat([dev(b), dev(e0), dev(ec)]), out, level=l)
+        assert relmax(host(out), P.gs_sweep(l, b, P.prolong_add(l, ec, e0))) <= 1e-12, l
+        out = torch.zeros(nc * nc, dtype=torch.float64, device="cuda")
+        S.apply_stage("RESID_RESTRICT", torch.cat([dev(b), dev(e0)]), out, level=l)
+        want = P.restrict(l, P.level_residual(l, b, e0)) / P.level_coef(l + 1)["D"]
+        assert relmax(host(out), want) <= 1e-12, l
+
+
 @pytest.mark.parametrize("name,N,eps", [("cfg4", 256, 1e-8), ("exp2d", 128, 1e-4), ("cfg2", 128, 1e-2)])
 def test_corner_solve_and_precond(name, N, eps):
     kw = dict(sigma=2.5, bx=1.99, by=2.99) if name == "exp2d" else {}
@@ -183,10 +210,40 @@ def test_paper_mode_table7_on_gpu(N):
         assert res.stats["mg_cycles_min"] == 5 and res.stats["mg_cycles_max"] == 5
         err = np.max(np.abs(u.reshape(N - 1, N - 1) - si.exact_solution(cfg, x, y)))
         assert rounds_to(err, t6[eps][col])
-        # Paper mode minimises the UNWEIGHTED residual, whose rows scale like eps/h^2 ~ 1e12:
-        # rounding differences are amplified (reading R11), so the
-        # loosely-stopped paper iterate is compared at 1e-7; the BASELINE (Jacobi) mode keeps 1e-9.
-        assert rel(u, ores["u"]) <= 1e-7
+        # Paper mode minimises the UNWEIGHTED residual, whose rows scale like eps/h^2 (~1e13 at
+        # eps = 1e-7): the loosely stopped iterate (||R|| <= 10 ln N / N) amplifies rounding
+        # (reading R11).  The bar is 1e-9, or -- where the oracle itself is less stable
+        # than that -- 10x the oracle's own response to a 1e-15 relative perturbation of f
+        # (measured: the GPU gap tracks it, 6e-9 at N = 256, eps = 1e-7).
+        assert rel(u, ores["u"]) <= max(1e-9, 10 * _oracle_sensitivity("exp2d", N, eps, ores["u"]))
+
+
+def _oracle_sensitivity(name, N, eps, u_ref):
+    """Relative change of the oracle's paper-mode iterate when f is perturbed by 1e-15 (relative,
+    seeded): the rounding amplification of the unweighted problem, measured on the oracle alone."""
+    cfg = si.config(name, N=N, eps=eps)
+    x = oracle.mesh(N, cfg.eps, 2.5, 1.99)
+    y = oracle.mesh(N, cfg.eps, 2.5, 2.99)
+    c1, c2, r, f = si.sample_2d(cfg, x, y)
+    fp = f * (1.0 + 1e-15 * si.random_field(99, f.shape))
+    P = oracle.Oracle2D(N, cfg.eps, x, y, c1, c2, r)
+    res = P.solve(fp, weighted=0, stop_abs=1, tol=cfg.tol)
+    P.close()
+    return rel(res["u"], u_ref)
+
+
+def test_paper_mode_sensitivity_is_conditioning():
+    """The paper-mode gaps are the problem's conditioning, not an implementation difference: at
+    eps = 1e-4 the oracle's response to a 1e-15 perturbation of f is tiny and the GPU matches
+    to 1e-12; at eps = 1e-7 both are orders of magnitude larger, and of the same size."""
+    out = {}
+    for eps in (1e-4, 1e-7):
+        cfg, x, y, f, res, ores, u = _solve_pair("exp2d", 256, eps, stop=spp.SPP_STOP_ABS_L2, sigma=2.5, bx=1.99,
+                                                 by=2.99)
+        out[eps] = (rel(u, ores["u"]), _oracle_sensitivity("exp2d", 256, eps, ores["u"]))
+    assert out[1e-4][0] <= 1e-12
+    assert out[1e-7][1] > 100 * out[1e-4][1]
+    assert out[1e-7][0] <= 10 * out[1e-7][1]
 
 
 def test_host_and_device_buffers_agree():
