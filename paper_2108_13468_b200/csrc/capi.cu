@@ -429,6 +429,7 @@ static void parse_tune(Ctx *c)
             else if (k == "coarse_max") c->tune.coarse_max = v;
             else if (k == "gs_lag") c->tune.gs_lag = v;
             else if (k == "dist_levels") c->tune.dist_levels = v;
+            else if (k == "rho_halo") c->tune.rho_halo = v;
         }
         pos = end + 1;
     }
@@ -493,7 +494,7 @@ static spp_status alloc_all(Ctx *c)
     c->F = c->w + G; c->U = c->F + G; c->T1 = c->U + G;
     const int maxit = c->opt.max_iters;
     // reduction partials: one kRedBlocks segment per strip (nparts) in every slot
-    CK(c, cudaMalloc(&c->part, sizeof(double) * (size_t)(std::max(maxit, kMaxLevels) + 8) * kRedBlocks * c->nparts));
+    CK(c, cudaMalloc(&c->part, sizeof(double) * (size_t)(std::max(maxit, 3 * kMaxLevels) + 8) * kRedBlocks * c->nparts));
     CK(c, cudaMalloc(&c->dscal, sizeof(double) * (size_t)(3 * maxit + 64)));
     CK(c, cudaMallocHost(&c->hpin, sizeof(double) * std::max<size_t>(8 * (size_t)kRedBlocks * c->nparts + 4 * (size_t)maxit + 64,
                                                                       (size_t)kMaxLevels * kRedBlocks)));

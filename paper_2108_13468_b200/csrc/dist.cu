@@ -423,7 +423,7 @@ static spp_status dist_finish(Dist *d)
             for (int l = 0; ok && l < D; ++l)
                 for (int r = 0; ok && r < P; ++r) {
                     Level tmp = c->lev[l];
-                    ok = plan_tiles(c, g.nl[l], g.lrow1(l, r) - g.lrow0(l, r), g.halo[l], false, tmp);
+                    ok = plan_tiles(c, g.nl[l], g.lrow1(l, r) - g.lrow0(l, r), g.halo[l], c->lev[l].halo_certx, false, tmp);
                 }
         }
         if (ok) break;
@@ -465,7 +465,7 @@ static spp_status dist_finish(Dist *d)
             else { Lv.slo = 1; Lv.shi = Lv.n; }
             Lv.sdist = l < D;
             Lv.shalo = l < D ? g.shalo(l, r) : 0;
-            if (l < D) plan_tiles(cr, Lv.n, Lv.shi - Lv.slo + 1, g.halo[l], false, Lv);
+            if (l < D) plan_tiles(cr, Lv.n, Lv.shi - Lv.slo + 1, g.halo[l], Lv.halo_certx, false, Lv);
         }
     }
     return SPP_OK;

@@ -55,7 +55,7 @@ constexpr int WBOX = 32 * WCW;   // doubles per box (4 KB)
 // doubles per staging slot: 4 boxes in y-form (16 KB), 3 in z-form (12 KB; no 1/D box)
 __host__ __device__ constexpr int wslot(bool yform) { return (yform ? WNA : WNA - 1) * WBOX; }
 constexpr int WMAXW = 5;         // sweeping warps per CTA (max; 5 only in z-form); +W write-back +1 TMA
-constexpr int WEB = 128;         // edge ring (columns)
+constexpr int WEB = 512;         // edge ring (columns): slack between a warp and the one below it
 // L2 prefetch distance (chunks; 0 = none).  Measured: none is best -- at cfg5's 4096^2 level 0
 // the prefetched boxes of 129 tiles (8 chunks ahead: ~60 MB in flight) were evicted before use
 // (cfg5 41.0 -> 39.1 ms per solve without them, cfg4 20.66 -> 20.43 ms).  L2 eviction-priority
@@ -1037,32 +1037,46 @@ void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew,
 }
 
 // ------------------------------------------------------------------------------------------
-// Setup: rho_l = max over the level of (aE + aN) / D, the contraction factor of the downstream
-// recurrence in z-form (z = q/D + (aE/D) z_E + (aN/D) z_N).  The y-form sweep (y = D z) computes
-// the same z, so the truncation error of a zero-inflow halo of depth d is <= rho^d max|z|.
-// Couplings to the block boundary (i = nl East, j = nl North) multiply a zero inflow and are
-// excluded.  Partial maxima per block.
-__global__ void k_level_rho(int nl, long pc, const double *aE, const double *aN, const double *cd, double *part)
+// Setup: the contraction factors of the downstream recurrence z = q/D + ca z_E + cn z_N (z-form,
+// ca = aE/D, cn = aN/D) over level l, couplings to the block boundary (i = nl East, j = nl North;
+// they multiply a zero inflow) excluded.  Three partial maxima per block:
+//   rho     = max (ca + cn)                 (y-form bound)
+//   gamma_y = max cn / (1 - ca)             (row decay of a north-boundary error)
+//   gamma_x = max ca / (1 - cn)             (column decay of an east-boundary error)
+// gamma_y: with M_j = max_i |e(i,j)| of an error e = ca e_E + cn e_N that vanishes on the east
+// edge, the node attaining M_j gives M_j <= ca M_j + cn M_{j+1}, so M_j <= gamma_y M_{j+1};
+// gamma_x likewise per column.  Both are <= rho (cn/(1-ca) <= ca + cn iff ca (1 - ca - cn) >= 0).
+__global__ void k_level_rho(int nl, long pc, const double *aE, const double *aN, const double *cd, double *part,
+                            double *partgy, double *partgx)
 {
-    __shared__ double sm[32];
-    double mx = 0.0;
+    __shared__ double sm[3][32];
+    double mx = 0.0, gy = 0.0, gx = 0.0;
     const long tot = (long)nl * nl;
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
         const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
         const long q = (long)j * pc + i;
-        mx = fmax(mx, ((i < nl ? aE[q] : 0.0) + (j < nl ? aN[q] : 0.0)) * cd[q]);
+        const double ca = (i < nl ? aE[q] : 0.0) * cd[q], cn = (j < nl ? aN[q] : 0.0) * cd[q];
+        mx = fmax(mx, ca + cn);
+        gy = fmax(gy, cn / (1.0 - ca));
+        gx = fmax(gx, ca / (1.0 - cn));
     }
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+    for (int d = 16; d > 0; d >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+        gy = fmax(gy, __shfl_xor_sync(0xffffffffu, gy, d));
+        gx = fmax(gx, __shfl_xor_sync(0xffffffffu, gx, d));
+    }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwp = blockDim.x >> 5;
-    if (lane == 0) sm[wid] = mx;
+    if (lane == 0) { sm[0][wid] = mx; sm[1][wid] = gy; sm[2][wid] = gx; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int k = 0; k < nwp; ++k) s = fmax(s, sm[k]);
-        part[blockIdx.x] = s;
+        double a = 0.0, b = 0.0, c2 = 0.0;
+        for (int k = 0; k < nwp; ++k) { a = fmax(a, sm[0][k]); b = fmax(b, sm[1][k]); c2 = fmax(c2, sm[2][k]); }
+        part[blockIdx.x] = a; partgy[blockIdx.x] = b; partgx[blockIdx.x] = c2;
     }
     zero_tail(part);
+    zero_tail(partgy);
+    zero_tail(partgx);
 }
 
 // ya = aE / D_E = aE(i,j) cd(i+1,j), yn = aN / D_N = aN(i,j) cd(i,j+1) on [1, nl]^2 (the ghost
@@ -1092,7 +1106,7 @@ void launch_ycoef(Ctx *c, int nl, long pc, const double *aE, const double *aN, c
 // sweeps (tile columns + halo + 62) / 16 chunks.  Picks the warps per tile (3..Wt; the halo rows
 // are part of the tile) and the column tiling with the smallest such time among the plans that
 // run as one wave of one CTA per SM.  Returns false when no plan exists.
-bool plan_tiles(const Ctx *c, int n, int rows, int halo, bool whole, Level &L)
+bool plan_tiles(const Ctx *c, int n, int rows, int halo, int halox, bool whole, Level &L)
 {
     const Tune &T = c->tune;
     const int Wt = std::max(1, std::min(T.gs_warps, c->mg_zform ? WMAXW : 4));   // 5 warps only fit in z-form
@@ -1102,7 +1116,7 @@ bool plan_tiles(const Ctx *c, int n, int rows, int halo, bool whole, Level &L)
     if (whole && n <= 32 * Wt) {                               // candidate: one exact CTA
         bestW = (n + 31) / 32; bestRows = n; bestCols = n; bestT = cost(bestW, n); bestN = 1;
     }
-    for (int W = std::min(3, Wt); W <= Wt; ++W) {
+    for (int W = std::min(2, Wt); W <= Wt; ++W) {
         const int rows_out = 32 * W - halo;
         if (rows_out < 16 || (whole && rows_out >= n)) continue;
         const int nrt = (rows + rows_out - 1) / rows_out;
@@ -1113,7 +1127,7 @@ bool plan_tiles(const Ctx *c, int n, int rows, int halo, bool whole, Level &L)
             tc = (tc + 15) / 16 * 16;
             if (T.gs_tile_cols > 0) tc = std::min(n, T.gs_tile_cols);
             const bool full = tc >= n;
-            const int t = cost(W, (full ? n : tc + halo));
+            const int t = cost(W, (full ? n : tc + halox));
             const int ncta = nrt * ((n + tc - 1) / tc);
             if (t < bestT || (t == bestT && ncta < bestN)) {
                 bestT = t; bestN = ncta; bestW = W; bestRows = rows_out; bestCols = full ? n : tc;
@@ -1126,11 +1140,11 @@ bool plan_tiles(const Ctx *c, int n, int rows, int halo, bool whole, Level &L)
     L.tile_cols = bestCols;
     const bool exact1 = whole && bestRows >= n;
     L.halo_y = exact1 ? 0 : halo;
-    L.halo_x = bestCols >= n ? 0 : halo;
+    L.halo_x = bestCols >= n ? 0 : halox;
     if (getenv("SPP_DEBUG_TILES"))
-        fprintf(stderr, "[spp] level n=%d rows=%d%s halo=%d: warps %d tile %dx%d (+%d,%d) cost %d chunks, %d CTAs\n",
-                n, rows, whole ? "" : " (strip)", halo, L.tile_warps, L.tile_rows, L.tile_cols, L.halo_y, L.halo_x, bestT,
-                bestN);
+        fprintf(stderr, "[spp] level n=%d rows=%d%s halo=%d,%d: warps %d tile %dx%d (+%d,%d) cost %d chunks, %d CTAs\n",
+                n, rows, whole ? "" : " (strip)", halo, halox, L.tile_warps, L.tile_rows, L.tile_cols, L.halo_y, L.halo_x,
+                bestT, bestN);
     return true;
 }
 
@@ -1138,24 +1152,42 @@ cudaError_t setup_mg_tiles(Ctx *c)
 {
     const Tune &T = c->tune;
     const int Wt = std::max(1, std::min(T.gs_warps, c->mg_zform ? WMAXW : 4));   // 5 warps only fit in z-form
+    const size_t S = (size_t)c->L * kRedBlocks;
     for (int l = 0; l < c->L; ++l) {
+        double *p = c->part + (size_t)l * kRedBlocks;
         k_level_rho<<<kRedBlocks, kRedThreads, 0, c->st>>>(c->lev[l].n, c->lev[l].cpitch, c->lev[l].aE,
-                                                           c->lev[l].aN, c->lev[l].cd, c->part + (size_t)l * kRedBlocks);
+                                                           c->lev[l].aN, c->lev[l].cd, p, p + S, p + 2 * S);
         c->launches++;
     }
-    SPP_CUDA_TRY(cudaMemcpyAsync(c->hpin, c->part, sizeof(double) * kRedBlocks * c->L, cudaMemcpyDeviceToHost, c->st));
+    std::vector<double> h(3 * S);
+    SPP_CUDA_TRY(cudaMemcpyAsync(h.data(), c->part, sizeof(double) * 3 * S, cudaMemcpyDeviceToHost, c->st));
     SPP_CUDA_TRY(cudaStreamSynchronize(c->st));
     for (int l = 0; l < c->L; ++l) {
         Level &L = c->lev[l];
-        double rho = 0.0;
-        for (int k = 0; k < kRedBlocks; ++k) rho = std::fmax(rho, c->hpin[(size_t)l * kRedBlocks + k]);
+        double rho = 0.0, gy = 0.0, gx = 0.0;
+        for (int k = 0; k < kRedBlocks; ++k) {
+            rho = std::fmax(rho, h[(size_t)l * kRedBlocks + k]);
+            gy = std::fmax(gy, h[S + (size_t)l * kRedBlocks + k]);
+            gx = std::fmax(gx, h[2 * S + (size_t)l * kRedBlocks + k]);
+        }
         L.contraction = rho;
-        // certified halo: smallest multiple of 8 with rho^halo <= 1e-17
-        int halo = -1;
-        if (rho < 1.0)
-            for (int h = 8; h <= T.gs_max_halo; h += 8)
-                if (h * std::log(rho) <= std::log(1e-17)) { halo = h; break; }
+        // certified halos: the truncation error of a tile whose rows
+        // above / columns right of its output are recomputed from zero inflow is <= (g_y^hy +
+        // g_x^hx) max|z|; hy, hx = smallest multiples of 8 with each term <= 0.5e-17.  In y-form
+        // (y = D z, other couplings) the rho bound rho^h <= 1e-17 is used for both.
+        auto depth = [&](double g, double target) {
+            if (!(g < 1.0)) return -1;
+            if (g <= 0.0) return 8;
+            for (int d = 8; d <= T.gs_max_halo; d += 8)
+                if (d * std::log(g) <= std::log(target)) return d;
+            return -1;
+        };
+        int hy, hx;
+        if (c->mg_zform && !T.rho_halo) { hy = depth(gy, 0.5e-17); hx = depth(gx, 0.5e-17); }
+        else hy = hx = depth(rho, 1e-17);
+        const int halo = (hy < 0 || hx < 0) ? -1 : hy;
         L.halo_cert = halo;
+        L.halo_certx = halo < 0 ? -1 : hx;
         const int n = L.n;
         if (halo < 0 || halo + 16 > 32 * Wt) {
             if (n <= 32 * Wt) {                                // one CTA, exact
@@ -1164,7 +1196,7 @@ cudaError_t setup_mg_tiles(Ctx *c)
             } else L.tile_warps = 0;                           // no certified halo: exact chain
             continue;
         }
-        if (!plan_tiles(c, n, n, halo, true, L)) L.tile_warps = 0;   // no tiling: exact chain
+        if (!plan_tiles(c, n, n, hy, hx, true, L)) L.tile_warps = 0;   // no tiling: exact chain
     }
     return cudaSuccess;
 }

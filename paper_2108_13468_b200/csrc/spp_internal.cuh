@@ -69,7 +69,7 @@ struct Level {
     // columns recomputed above / right of each tile (-1: none certifiable -> exact chained sweep)
     int tile_rows = 0, tile_cols = 0, tile_warps = 0, halo_x = 0, halo_y = 0;
     double contraction = 0.0;            // max (aE + aN) / D over the level
-    int halo_cert = -1;                  // certified halo depth of the level (-1: none)
+    int halo_cert = -1, halo_certx = -1; // certified halo rows / columns of the level (-1: none)
     // row strip of a distributed solve: this rank owns rows slo..shi of the level
     // (1..n on one GPU).  sdist: the level's GS sweeps run on the strip (own rows plus shalo
     // halo rows above, whose right-hand side comes from the strip above) with the tile plan
@@ -108,6 +108,7 @@ struct Tune {
     int gs_lag = 5;            // tiling model: chunk-times each extra warp adds
     int coarse_max = 16;       // levels with n <= this run as one fused single-CTA V-cycle (16 measured best)
     int dist_levels = 2;       // row strips: corner levels whose sweeps run on the strips
+    int rho_halo = 0;          // 1: certify halos by rho = max (ca + cn) (round 1) instead of gamma_y, gamma_x
 };
 
 struct ProfRec { int64_t launches = 0; double ms = 0, bytes = 0; };
@@ -227,7 +228,7 @@ void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew,
                          double *part, const MGState *ms = nullptr);
 void launch_lines(Ctx *c, const double *v, double *z);
 cudaError_t setup_mg_tiles(Ctx *c);
-bool plan_tiles(const Ctx *c, int n, int rows, int halo, bool whole, Level &L);
+bool plan_tiles(const Ctx *c, int n, int rows, int halo, int halox, bool whole, Level &L);
 void launch_scale_cd(Ctx *c, int l, const double *b, double *q);
 bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs = false);
 
