@@ -904,7 +904,12 @@ bool strip_partition(int N, int P, std::vector<int> &J)
     const int Pb = (P + 1) / 2, Pt = P - Pb;
     if (Pb > n || Pt > n - 1) return false;
     for (int b = 0; b <= Pb; ++b) J[b] = 1 + (int)((long)n * b / Pb);
-    for (int t = 1; t <= Pt; ++t) J[Pb + t] = n + 1 + (int)((long)(n - 1) * t / Pt);
+    // top strips: every strip that hands its bottom row to the strip below (all but the lowest)
+    // spans a multiple of 32 rows (check_partition); the lowest takes the remainder
+    const int s = std::max(32, (int)std::lround((double)(n - 1) / Pt / 32.0) * 32);
+    if ((long)(Pt - 1) * s >= n - 1) return false;
+    J[P] = N;
+    for (int t = P - 1; t > Pb; --t) J[t] = J[t + 1] - s;
     return true;
 }
 
@@ -920,6 +925,14 @@ bool check_partition(int N, const std::vector<int> &J, int *Pb, std::string *why
         if (J[r] == n + 1) pb = r;
     }
     if (P > 1 && pb < 1) { *why = "a strip boundary must sit at row n+1 = N/2+1 (the X/I | C/Y split)"; return false; }
+    // the M_II relay publishes the bottom row of a strip's last CTA strip, lane 31 of its last
+    // warp: every top strip with a strip below it in the top half spans whole warps (32 rows)
+    for (int r = pb + 1; P > 1 && r < P; ++r)
+        if ((J[r + 1] - J[r]) % 32 != 0) {
+            *why = "top strip " + std::to_string(r) + " spans " + std::to_string(J[r + 1] - J[r]) +
+                   " rows: every top strip above the lowest must span a multiple of 32 rows";
+            return false;
+        }
     *Pb = P > 1 ? pb : 1;
     return true;
 }

@@ -312,10 +312,12 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
             __syncwarp();
             if (lane < 16 && (c + 1) * WCW + lane < ncols) vin = ld_relaxed_u64(src + WCW);   // chunk c+1
         }
+        SPP_TP(t1);
         if (has_consumer && !EXPF_NOSPIN) {             // back-pressure on the edge ring
             const int lim = c * WCW + WCW - WLAG * 31 - WEB;
             if (lim > 0) { while (*((volatile int *)&cons[w + 1]) < lim) __nanosleep(32); }
         }
+        SPP_TP(t2);
         // the North inflow of the chunk, loaded before the operand wait: lane 0 needs E[0] at the
         // first step, and a load queued behind the 24 operand loads delays the whole step chain
         double2 E[8];
@@ -407,6 +409,10 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
 #ifdef SPP_WAVE_PROF
         SPP_TP(te);
         tp_spin += tb - ta; tp_bar += tc - tb; tp_steps += td - tc; tp_wb += te - td;
+        if (lane == 0 && a.prof && blockIdx.x == 0 && blockIdx.y < 2 && c < 160) {
+            long long *tl = a.prof + 8 * 8 * 8192 + (((long)blockIdx.y * 8 + w) * 160 + c) * 8;
+            tl[0] = ta; tl[1] = t1; tl[2] = t2; tl[3] = tb; tl[4] = tc; tl[5] = td; tl[6] = te; tl[7] = 1;
+        }
 #endif
     }
 #ifdef SPP_WAVE_PROF
@@ -441,6 +447,21 @@ static void wave_prof_dump(Ctx *c, long long *prof, const char *what, int nctas,
     for (int k = 0; k < nw; ++k)
         if (h[8 * k]) { g0 = g0 < 0 ? h[8 * k + 6] : std::min(g0, h[8 * k + 6]); g1 = std::max(g1, h[8 * k + 7]); }
     fprintf(stderr, "[wave-prof] %s n=%d: %d CTAs, first warp start -> last warp end %.2f us\n", what, nl, nctas, (g1 - g0) * 1e-3);
+    if (getenv("SPP_WAVE_TL")) {                        // per-chunk timeline of CTA rows 0, 1 (clock64)
+        std::vector<long long> tl(2 * 8 * 160 * 8);
+        cudaMemcpy(tl.data(), prof + 8 * 8 * 8192, sizeof(long long) * tl.size(), cudaMemcpyDeviceToHost);
+        long long t0 = -1;
+        for (int w = 0; w < 8; ++w) if (tl[((0 * 8 + w) * 160) * 8 + 7]) t0 = t0 < 0 ? tl[((0 * 8 + w) * 160) * 8] : std::min(t0, tl[((0 * 8 + w) * 160) * 8]);
+        for (int y = 0; y < 2; ++y)
+            for (int w = 0; w < 8; ++w)
+                for (int cc = 0; cc < 160; ++cc) {
+                    const long long *r = &tl[((y * 8 + w) * 160 + cc) * 8];
+                    if (!r[7] || (cc > 12 && cc % 16 != 0)) continue;
+                    fprintf(stderr, "[wave-tl] y%d w%d c%3d: start %8lld | wait %6lld bp %6lld E %5lld mbar %5lld steps %5lld post %5lld\n",
+                            y, w, cc, y == 0 ? r[0] - t0 : r[0], r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[5] - r[4],
+                            r[6] - r[5]);
+                }
+    }
     for (int k = 0; k < nw; ++k)
         if (h[8 * k] && (k / 8 < 4 || k / 8 == nctas - 1))
             fprintf(stderr, "[wave-prof]  cta %d warp %d: start %+.2f us end %+.2f us | cycles total %lld spin %lld bar %lld "
@@ -540,8 +561,8 @@ void launch_wave(Ctx *c, WaveArgs a, long rows_v, long rows_c, int warps, bool y
     ProfScope ps(c, cls, bytes);
 #ifdef SPP_WAVE_PROF
     static long long *prof = nullptr;
-    if (!prof) cudaMalloc(&prof, sizeof(long long) * 8 * 8 * 8192);
-    cudaMemsetAsync(prof, 0, sizeof(long long) * 8 * 8 * 8192, c->st);
+    if (!prof) cudaMalloc(&prof, sizeof(long long) * (8 * 8 * 8192 + 2 * 8 * 160 * 8));
+    cudaMemsetAsync(prof, 0, sizeof(long long) * (8 * 8 * 8192 + 2 * 8 * 160 * 8), c->st);
     a.prof = prof;
 #endif
     if (yform) k_wave<true, false><<<grid, (2 * warps + 1) * 32, sm, c->st>>>(a, m);
@@ -580,8 +601,8 @@ void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform,
     ProfScope ps(c, cls, bytes);
 #ifdef SPP_WAVE_PROF
     static long long *prof = nullptr;
-    if (!prof) cudaMalloc(&prof, sizeof(long long) * 8 * 8 * 8192);
-    cudaMemsetAsync(prof, 0, sizeof(long long) * 8 * 8 * 8192, c->st);
+    if (!prof) cudaMalloc(&prof, sizeof(long long) * (8 * 8 * 8192 + 2 * 8 * 160 * 8));
+    cudaMemsetAsync(prof, 0, sizeof(long long) * (8 * 8 * 8192 + 2 * 8 * 160 * 8), c->st);
     a.prof = prof;
 #endif
     const cudaError_t le = yform

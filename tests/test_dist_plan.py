@@ -20,7 +20,7 @@ def test_default_partition():
             try:
                 J = spp.spp_strip_partition(N, P)
             except spp.SppError:
-                assert P > 1 and (P + 1) // 2 > n
+                assert P > 1 and ((P + 1) // 2 > n or (P - (P + 1) // 2 - 1) * 32 >= n - 1)
                 continue
             assert J[0] == 1 and J[-1] == N and np.all(np.diff(J) > 0)
             if P > 1:
@@ -28,7 +28,8 @@ def test_default_partition():
                 Pb = list(J).index(n + 1)
                 assert Pb == (P + 1) // 2
                 sizes = np.diff(J)
-                assert sizes[:Pb].max() - sizes[:Pb].min() <= 1 and sizes[Pb:].max() - sizes[Pb:].min() <= 1
+                assert sizes[:Pb].max() - sizes[:Pb].min() <= 1
+                assert all(sz % 32 == 0 for sz in sizes[Pb + 1:])             # M_II relay strips: whole warps
     with pytest.raises(spp.SppError):
         spp.spp_strip_partition(8, 9)
 
@@ -96,6 +97,11 @@ def test_schedule_blocks_and_halos(N, P, D):
 
 
 def test_schedule_rejects_bad_geometry():
+    J = spp.spp_strip_partition(512, 6)
+    bad = J.copy()
+    bad[4] += 1                                                          # a relay strip not of whole warps
+    with pytest.raises(spp.SppError):
+        spp.spp_dist_plan(512, 6, bad, 2, 64, 56, -1)
     J = spp.spp_strip_partition(256, 4)
     bad = J.copy()
     bad[2] += 1                                                          # no boundary at n+1

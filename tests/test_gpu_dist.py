@@ -53,6 +53,7 @@ def _solve(cfg, x, y, data, o, strips):
 @pytest.mark.parametrize("name,N,eps,P", [
     ("cfg4", 128, 1e-8, 2), ("cfg4", 256, 1e-8, 3), ("cfg4", 256, 1e-8, 4), ("cfg4", 512, 1e-8, 8),
     ("cfg5", 256, 1e-6, 2), ("cfg3", 512, 1e-6, 4), ("cfg2", 128, 1e-2, 2), ("cfg5", 512, 1e-4, 5),
+    ("cfg4", 512, 1e-8, 6), ("cfg4", 256, 1e-8, 7),
 ])
 def test_strips_match_one_gpu_and_oracle(name, N, eps, P):
     cfg, x, y, data, o = _inputs(name, N, eps)
