@@ -48,6 +48,7 @@ def lib():
         build()
         L = ctypes.CDLL(str(_LIB))
         L.orc_mesh.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, _dp]
+        L.orc_mesh_bs.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, _dp]
         L.orc_thomas.argtypes = [ctypes.c_int, _dp, _dp, _dp, _dp, _dp]
         L.orc1_coef.argtypes = [ctypes.c_int, ctypes.c_double, _dp, _dp, _dp, _dp, _dp, _dp]
         L.orc1_matvec.argtypes = [ctypes.c_int, _dp, _dp, _dp, _dp, _dp]
@@ -103,6 +104,15 @@ def mesh(N: int, eps: float, sigma: float = 2.0, beta: float = 1.0) -> np.ndarra
     rc = lib().orc_mesh(N, eps, sigma, beta, _p(x))
     if rc != 0:
         raise ValueError(f"orc_mesh rc={rc}")
+    return x
+
+
+def mesh_bs(N: int, eps: float, sigma: float = 2.0, beta: float = 1.0) -> np.ndarray:
+    """Bakhvalov-Shishkin graded mesh (NEXT-4, reading R21)."""
+    x = np.zeros(N + 1)
+    rc = lib().orc_mesh_bs(N, eps, sigma, beta, _p(x))
+    if rc != 0:
+        raise ValueError(f"orc_mesh_bs rc={rc}")
     return x
 
 

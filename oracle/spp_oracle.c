@@ -67,6 +67,46 @@ int orc_mesh(int N, double eps, double sigma, double beta, double *x)
     return ORC_OK;
 }
 
+/* Bakhvalov-Shishkin mesh (reading R21): the graded layer-adapted mesh the
+ * paper's Remark rem:not just S-meshes names ("graded (e.g., Bakhvalov) meshes"),
+ * with the transition point at index N/2 that the block preconditioner needs:
+ *   x_i = -(sigma eps / beta) ln(1 - 2 (1 - 1/N) i / N),  i = 0 .. N/2   (graded layer),
+ *   x_i = tau + (i - N/2) (1 - tau) / (N/2),               i = N/2 .. N   (uniform),
+ * tau = x_{N/2} = sigma eps ln(N) / beta, the Shishkin transition point.  tau > 1/2: the
+ * uniform mesh x_i = i/N (no layer to resolve). */
+int orc_mesh_bs(int N, double eps, double sigma, double beta, double *x)
+{
+    if (N < 4 || (N % 2) != 0 || !(eps > 0.0) || eps > 1.0 || !(sigma > 0.0) || !(beta > 0.0))
+        return ORC_E_ARG;
+    int n = N / 2;
+    double s = sigma * eps / beta;
+    double tau = s * log((double)N);
+    if (tau > 0.5) {
+        for (int i = 0; i <= N; i++) x[i] = (double)i / N;
+        x[N] = 1.0;
+        return ORC_OK;
+    }
+    x[0] = 0.0;
+    for (int i = 1; i < n; i++) x[i] = -s * log(1.0 - 2.0 * (1.0 - 1.0 / N) * i / N);
+    x[n] = tau;
+    double H = (1.0 - tau) / n;
+    for (int i = n + 1; i < N; i++) x[i] = tau + (i - n) * H;
+    x[N] = 1.0;
+    return ORC_OK;
+}
+
+/* 1 if x is the piecewise-uniform (Shishkin) mesh broken at N/2, to rounding. */
+static int mesh_is_shishkin(const double *x, int N)
+{
+    int n = N / 2;
+    double t = x[n], h = t / n, H = (1.0 - t) / n;
+    for (int i = 0; i <= N; i++) {
+        double want = i <= n ? i * h : t + (i - n) * H;
+        if (fabs(x[i] - want) > 1e-12 * (fabs(want) + h)) return 0;
+    }
+    return 1;
+}
+
 /* Mesh width h_i = x_i - x_{i-1} on the piecewise-uniform mesh, evaluated
  * from the formula tau/(N/2) resp. (1-tau)/(N/2) with tau = x_{N/2} (reading R12:
  * formula, not coordinate differences).  Valid for i = 1..N. */
@@ -75,6 +115,13 @@ static double mesh_h(const double *x, int N, int i)
     int n = N / 2;
     double tau = x[n];
     return (i <= n) ? tau / n : (1.0 - tau) / n;
+}
+
+/* Width h_i for the 2D operator: the Shishkin formula (reading R12) on a piecewise-uniform mesh;
+ * on any other (graded) mesh the coordinate differences h_i = x_i - x_{i-1} of P:964-968. */
+static double mesh_w(const double *x, int N, int i, int graded)
+{
+    return graded ? x[i] - x[i - 1] : mesh_h(x, N, i);
 }
 
 /* ===================================================================================== */
@@ -421,10 +468,15 @@ typedef struct {
     double *aE, *aN, *rr, *D;   /* [nl*nl], idx (l-1)*nl + (m-1)                           */
     double *hb, *kb;            /* [nl+2]: hbar_m, kbar_l -> S_l = diag(hbar_m kbar_l)     */
     double *e, *rho, *b;        /* work vectors [nl*nl]                                    */
+    /* [nl+2]: geometric interpolation weights of an odd node q of this level from the next
+     * coarser level's nodes at its left / right (x) and below / above (y): the linear
+     * interpolant on this level's 1D meshes; 1/2 on a uniform corner */
+    double *wxl, *wxr, *wyl, *wyr;
 } orc_level;
 
 typedef struct {
     int N, n, m;                /* N intervals; n = N/2 (corner size); m = N-1              */
+    int gx, gy;                 /* graded (non-Shishkin) mesh in x / y: widths from coordinates */
     double eps;
     double *aW, *aS;            /* [N+1], index 1..N-1                                      */
     double *aE, *aN, *rr, *D;   /* [m*m], idx (j-1)*m + (i-1)                              */
@@ -456,16 +508,17 @@ static void orc2_coef(orc2d *P, const double *x, const double *y, const double *
 {
     int N = P->N, m = P->m;
     double eps = P->eps;
+    int gx = P->gx, gy = P->gy;
     for (int i = 1; i <= m; i++) {
-        double hi = mesh_h(x, N, i), hi1 = mesh_h(x, N, i + 1), hb = 0.5 * (hi + hi1);
+        double hi = mesh_w(x, N, i, gx), hi1 = mesh_w(x, N, i + 1, gx), hb = 0.5 * (hi + hi1);
         P->aW[i] = eps / (hb * hi);
-        double kj = mesh_h(y, N, i), kj1 = mesh_h(y, N, i + 1), kb = 0.5 * (kj + kj1);
+        double kj = mesh_w(y, N, i, gy), kj1 = mesh_w(y, N, i + 1, gy), kb = 0.5 * (kj + kj1);
         P->aS[i] = eps / (kb * kj);
     }
     for (int j = 1; j <= m; j++) {
-        double kj = mesh_h(y, N, j), kj1 = mesh_h(y, N, j + 1), kb = 0.5 * (kj + kj1);
+        double kj = mesh_w(y, N, j, gy), kj1 = mesh_w(y, N, j + 1, gy), kb = 0.5 * (kj + kj1);
         for (int i = 1; i <= m; i++) {
-            double hi = mesh_h(x, N, i), hi1 = mesh_h(x, N, i + 1), hb = 0.5 * (hi + hi1);
+            double hi = mesh_w(x, N, i, gx), hi1 = mesh_w(x, N, i + 1, gx), hb = 0.5 * (hi + hi1);
             size_t p = IX(i, j, m);
             P->aE[p] = eps / (hb * hi1) + c1[p] / hi1;
             P->aN[p] = eps / (kb * kj1) + c2[p] / kj1;
@@ -494,7 +547,22 @@ void orc2_matvec_raw(const orc2d *P, const double *u, double *y)
 /* Level l keeps every 2^l-th layer node of the corner, plus the corner boundary nodes
  * x_0 and x_{n+1} (reading R8), and re-discretises ("rediscretization") with the same
  * stencil formula on that 1D mesh: widths 2^l * tau/(N/2) inside the corner and the first
- * coarse width (1-tau)/(N/2) for the last interval; c1, c2, r sampled at the coarse nodes. */
+ * coarse width (1-tau)/(N/2) for the last interval; c1, c2, r sampled at the coarse nodes.
+ * On a graded mesh (NEXT-4) the level's 1D mesh is X_q = x_{q 2^l} (q = 0..nl), X_{nl+1} =
+ * x_{n+1}, and the widths are its coordinate differences. */
+/* the level's 1D widths w[q] = X_q - X_{q-1}, q = 1 .. nl+1 */
+static void level_widths(const double *x, int N, int l, int graded, double *w)
+{
+    int n = N / 2, step = 1 << l, nl = n >> l;
+    if (!graded) {
+        double h = step * (x[n] / n), H = (1.0 - x[n]) / n;
+        for (int q = 1; q <= nl; q++) w[q] = h;
+        w[nl + 1] = H;
+        return;
+    }
+    for (int q = 1; q <= nl; q++) w[q] = x[q * step] - x[(q - 1) * step];
+    w[nl + 1] = x[n + 1] - x[n];
+}
 static int build_level(orc2d *P, int l, const double *x, const double *y, const double *c1,
                        const double *c2, const double *r)
 {
@@ -510,19 +578,31 @@ static int build_level(orc2d *P, int l, const double *x, const double *y, const 
     Lv->b = malloc(nn * sizeof(double));
     if (!Lv->aW || !Lv->aS || !Lv->hb || !Lv->kb || !Lv->aE || !Lv->aN || !Lv->rr || !Lv->D ||
         !Lv->e || !Lv->rho || !Lv->b) return ORC_E_NOMEM;
-    double hx = step * (x[n] / n), Hx = (1.0 - x[n]) / n;   /* level widths, x axis */
-    double hy = step * (y[n] / n), Hy = (1.0 - y[n]) / n;   /* level widths, y axis */
+    Lv->wxl = calloc(nl + 2, sizeof(double)); Lv->wxr = calloc(nl + 2, sizeof(double));
+    Lv->wyl = calloc(nl + 2, sizeof(double)); Lv->wyr = calloc(nl + 2, sizeof(double));
+    double *wx = calloc(nl + 2, sizeof(double)), *wy = calloc(nl + 2, sizeof(double));
+    if (!Lv->wxl || !Lv->wxr || !Lv->wyl || !Lv->wyr || !wx || !wy) { free(wx); free(wy); return ORC_E_NOMEM; }
+    level_widths(x, N, l, P->gx, wx);                       /* level widths, x axis */
+    level_widths(y, N, l, P->gy, wy);                       /* level widths, y axis */
+    /* odd node q lies between this level's nodes q-1 and q+1, the coarser level's (q-1)/2 and
+     * (q+1)/2: linear interpolation weights from the widths (exactly 1/2 when they are equal) */
+    for (int q = 1; q < nl; q += 2) {
+        double a = wx[q], b = wx[q + 1];
+        Lv->wxl[q] = a == b ? 0.5 : b / (a + b); Lv->wxr[q] = a == b ? 0.5 : a / (a + b);
+        a = wy[q]; b = wy[q + 1];
+        Lv->wyl[q] = a == b ? 0.5 : b / (a + b); Lv->wyr[q] = a == b ? 0.5 : a / (a + b);
+    }
     double eps = P->eps;
     for (int q = 1; q <= nl; q++) {
-        double h = hx, h1 = (q < nl) ? hx : Hx, hb = 0.5 * (h + h1);
-        double k = hy, k1 = (q < nl) ? hy : Hy, kb = 0.5 * (k + k1);
+        double h = wx[q], h1 = wx[q + 1], hb = 0.5 * (h + h1);
+        double k = wy[q], k1 = wy[q + 1], kb = 0.5 * (k + k1);
         Lv->aW[q] = eps / (hb * h);  Lv->hb[q] = hb;
         Lv->aS[q] = eps / (kb * k);  Lv->kb[q] = kb;
     }
     for (int lq = 1; lq <= nl; lq++) {
-        double k1 = (lq < nl) ? hy : Hy, kb = Lv->kb[lq];
+        double k1 = wy[lq + 1], kb = Lv->kb[lq];
         for (int q = 1; q <= nl; q++) {
-            double h1 = (q < nl) ? hx : Hx, hb = Lv->hb[q];
+            double h1 = wx[q + 1], hb = Lv->hb[q];
             size_t g = IX(q * step, lq * step, P->m), p = IX(q, lq, nl);
             Lv->aE[p] = eps / (hb * h1) + c1[g] / h1;
             Lv->aN[p] = eps / (kb * k1) + c2[g] / k1;
@@ -530,6 +610,7 @@ static int build_level(orc2d *P, int l, const double *x, const double *y, const 
             Lv->D[p] = ((Lv->aW[q] + Lv->aE[p]) + (Lv->aS[lq] + Lv->aN[p])) + r[g];
         }
     }
+    free(wx); free(wy);
     (void)N;
     return ORC_OK;
 }
@@ -564,14 +645,14 @@ static void mg_residual(const orc_level *Lv, const double *b, const double *e, d
 }
 
 /* 1D linear interpolation parents of fine node i: an even node 2I is a coarse
- * node (weight 1); an odd node 2I+1 lies between coarse nodes I and I+1 (weight 1/2 each).
- * Coarse node 0 is the Dirichlet boundary and is skipped. */
-static int parents(int i, int *I, double *w)
+ * node (weight 1); an odd node 2I+1 lies between coarse nodes I and I+1 (weights wl[i], wr[i]:
+ * 1/2 each on a uniform corner).  Coarse node 0 is the Dirichlet boundary and is skipped. */
+static int parents(int i, int *I, double *w, const double *wl, const double *wr)
 {
     if ((i & 1) == 0) { I[0] = i / 2; w[0] = 1.0; return 1; }
     int c = 0;
-    if ((i - 1) / 2 >= 1) { I[c] = (i - 1) / 2; w[c] = 0.5; c++; }
-    I[c] = (i + 1) / 2; w[c] = 0.5; c++;
+    if ((i - 1) / 2 >= 1) { I[c] = (i - 1) / 2; w[c] = wl[i]; c++; }
+    I[c] = (i + 1) / 2; w[c] = wr[i]; c++;
     return c;
 }
 
@@ -584,7 +665,7 @@ static void mg_restrict(const orc_level *F, const orc_level *C, const double *rh
     for (int j = 1; j <= nf; j++)
         for (int i = 1; i <= nf; i++) {
             int Ii[2], Jj[2]; double wi[2], wj[2];
-            int ni = parents(i, Ii, wi), nj = parents(j, Jj, wj);
+            int ni = parents(i, Ii, wi, F->wxl, F->wxr), nj = parents(j, Jj, wj, F->wyl, F->wyr);
             double sr = (F->hb[i] * F->kb[j]) * rho[IX(i, j, nf)];
             for (int a = 0; a < ni; a++)
                 for (int c = 0; c < nj; c++)
@@ -602,7 +683,7 @@ static void mg_prolong_add(const orc_level *F, const orc_level *C, const double 
     for (int j = 1; j <= nf; j++)
         for (int i = 1; i <= nf; i++) {
             int Ii[2], Jj[2]; double wi[2], wj[2];
-            int ni = parents(i, Ii, wi), nj = parents(j, Jj, wj);
+            int ni = parents(i, Ii, wi, F->wxl, F->wxr), nj = parents(j, Jj, wj, F->wyl, F->wyr);
             double s = 0.0;
             for (int a = 0; a < ni; a++)
                 for (int c = 0; c < nj; c++) s += wi[a] * wj[c] * ec[IX(Ii[a], Jj[c], nc)];
@@ -794,6 +875,7 @@ void orc2_destroy(orc2d *P)
         orc_level *Lv = &P->lev[l];
         free(Lv->aW); free(Lv->aS); free(Lv->aE); free(Lv->aN); free(Lv->rr); free(Lv->D);
         free(Lv->hb); free(Lv->kb); free(Lv->e); free(Lv->rho); free(Lv->b);
+        free(Lv->wxl); free(Lv->wxr); free(Lv->wyl); free(Lv->wyr);
     }
     free(P->cycle_log); free(P->bC); free(P->zC);
     free(P);
@@ -807,6 +889,7 @@ orc2d *orc2_create(int N, double eps, const double *x, const double *y, const do
     orc2d *P = calloc(1, sizeof(orc2d));
     if (!P) return NULL;
     P->N = N; P->n = N / 2; P->m = N - 1; P->eps = eps;
+    P->gx = !mesh_is_shishkin(x, N); P->gy = !mesh_is_shishkin(y, N);
     size_t mm = (size_t)P->m * P->m;
     P->aW = calloc(N + 1, sizeof(double)); P->aS = calloc(N + 1, sizeof(double));
     P->aE = malloc(mm * sizeof(double)); P->aN = malloc(mm * sizeof(double));
