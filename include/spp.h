@@ -82,8 +82,10 @@ typedef struct {
                                 of two (2D, full coarsening of the corner)            */
     double eps;              /* perturbation parameter, (0, 1]                               */
     const double *x, *y;     /* HOST node coordinates, N+1 each: x[0]=0, x[N]=1, uniform on
-                                [0, x[N/2]] and on [x[N/2], 1] (Shishkin); y NULL
-                                in 1D.  The library uses tau = x[N/2] (reading R12).          */
+                                [0, x[N/2]] and on [x[N/2], 1] (Shishkin; 2D also
+                                any strictly increasing mesh with 0 < x[N/2] <= 1/2, e.g.
+                                spp_bakhvalov_mesh); y NULL in 1D.  On a Shishkin mesh the
+                                library uses tau = x[N/2] and the formula widths (R12).      */
     const double *c1, *c2, *r; /* coefficient samples at interior nodes (compact layout);
                                 c2 NULL in 1D.  Residency per `mem`.                        */
     spp_mem mem;
@@ -129,6 +131,16 @@ SPP_API void spp_default_options(int32_t dim, spp_options *o);
  * tau = min(1/2, sigma*eps*ln(n)/beta); n/2 uniform intervals on [0,tau] and on [tau,1].
  * x_out: n+1 doubles (host).  SPP_E_ARG for odd n < 4, eps not in (0,1], sigma/beta <= 0. */
 SPP_API spp_status spp_shishkin_mesh(int32_t n, double eps, double sigma, double beta, double *x_out);
+
+/* Bakhvalov-Shishkin graded mesh on the host (reading R21): the
+ * graded layer-adapted mesh of Remark rem:not just S-meshes with the transition point
+ * at index n/2: x_i = -(sigma eps/beta) ln(1 - 2(1 - 1/n) i/n) for i <= n/2, uniform
+ * on [tau, 1], tau = sigma eps ln(n)/beta (the Shishkin transition point); tau > 1/2: the uniform
+ * mesh i/n.  Same arguments and errors as spp_shishkin_mesh.  2D problems accept this (or any
+ * strictly increasing mesh with x[0] = 0, x[n] = 1, 0 < x[n/2] <= 1/2): the operator then uses
+ * the coordinate differences as widths and the corner multigrid geometric interpolation weights;
+ * 1D problems need the Shishkin mesh (SPP_E_MESH otherwise). */
+SPP_API spp_status spp_bakhvalov_mesh(int32_t n, double eps, double sigma, double beta, double *x_out);
 
 /* Validate the problem, allocate the device workspace on `cuda_stream` (NULL = legacy default
  * stream) and run the setup (coefficients, corner multigrid levels, line factorisations;

@@ -55,7 +55,7 @@ class spp_stats(ctypes.Structure):
 
 
 # names declared in include/spp.h (checked against the header by tests/test_abi.py)
-ABI_FUNCTIONS = ["spp_default_options", "spp_shishkin_mesh", "spp_create", "spp_setup",
+ABI_FUNCTIONS = ["spp_default_options", "spp_shishkin_mesh", "spp_bakhvalov_mesh", "spp_create", "spp_setup",
                  "spp_solve", "spp_apply_stage", "spp_kernel_launches", "spp_mg_levels", "spp_mg_level_n",
                  "spp_profile_enable", "spp_profile_reset", "spp_profile_get", "spp_profile_name",
                  "spp_destroy", "spp_last_error", "spp_version",
@@ -72,6 +72,7 @@ _vp, _dp = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)
 _lib.spp_default_options.argtypes = [ctypes.c_int32, ctypes.POINTER(spp_options)]
 _lib.spp_default_options.restype = None
 _lib.spp_shishkin_mesh.argtypes = [ctypes.c_int32, ctypes.c_double, ctypes.c_double, ctypes.c_double, _dp]
+_lib.spp_bakhvalov_mesh.argtypes = [ctypes.c_int32, ctypes.c_double, ctypes.c_double, ctypes.c_double, _dp]
 _lib.spp_create.argtypes = [ctypes.POINTER(spp_problem), ctypes.POINTER(spp_options), _vp, ctypes.POINTER(_vp)]
 _lib.spp_setup.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int]
 _lib.spp_solve.argtypes = [_vp, _vp, _vp, ctypes.c_int, _dp, ctypes.c_int32, ctypes.POINTER(spp_stats)]
@@ -146,6 +147,13 @@ def spp_default_options(dim: int) -> spp_options:
     o = spp_options()
     _lib.spp_default_options(dim, ctypes.byref(o))
     return o
+
+
+def spp_bakhvalov_mesh(n: int, eps: float, sigma: float = 2.0, beta: float = 1.0) -> np.ndarray:
+    """Bakhvalov-Shishkin graded mesh (spp.h; NEXT-4)."""
+    x = np.zeros(n + 1)
+    _check(_lib.spp_bakhvalov_mesh(n, eps, sigma, beta, x.ctypes.data_as(_dp)))
+    return x
 
 
 def spp_strip_partition(n: int, nranks: int) -> np.ndarray:

@@ -450,21 +450,100 @@ static spp_status check_options(const spp_options *o, int dim, Ctx *c)
     return SPP_OK;
 }
 
-static spp_status check_mesh(const double *x, int N, double *tau, Ctx *c)
+// A mesh the library solves on: x[0] = 0, x[N] = 1, 0 < x[N/2] <= 1/2.  Either the piecewise-
+// uniform Shishkin mesh broken at N/2 (*graded = 0: widths from the formula, R12), or
+// -- when `allow_graded` (2D) -- any strictly increasing mesh with its transition point at index
+// N/2 (a graded layer-adapted mesh such as Bakhvalov-Shishkin; *graded = 1:
+// widths are coordinate differences, R21).
+static spp_status check_mesh(const double *x, int N, double *tau, Ctx *c, bool allow_graded = false, int *graded = nullptr)
 {
     if (!x) FAIL(c, SPP_E_ARG, "mesh coordinates are NULL");
     const int n = N / 2;
     const double t = x[n];
+    if (graded) *graded = 0;
     if (x[0] != 0.0 || x[N] != 1.0 || !(t > 0.0) || !(t <= 0.5))
         FAIL(c, SPP_E_MESH, "mesh: need x[0]=0, x[N]=1, 0 < x[N/2] <= 1/2");
     const double h = t / n, H = (1.0 - t) / n;
     for (int i = 0; i <= N; ++i) {
         const double want = i <= n ? i * h : t + (i - n) * H;
-        if (std::fabs(x[i] - want) > 1e-12 * (std::fabs(want) + h))
-            FAIL(c, SPP_E_MESH, "mesh: node %d = %.17g is not on the piecewise-uniform Shishkin mesh (want %.17g)",
-                 i, x[i], want);
+        if (std::fabs(x[i] - want) > 1e-12 * (std::fabs(want) + h)) {
+            if (!allow_graded)
+                FAIL(c, SPP_E_MESH, "mesh: node %d = %.17g is not on the piecewise-uniform Shishkin mesh (want %.17g)",
+                     i, x[i], want);
+            for (int k = 1; k <= N; ++k)
+                if (!(x[k] > x[k - 1]) || !std::isfinite(x[k]))
+                    FAIL(c, SPP_E_MESH, "mesh: nodes must increase strictly (node %d = %.17g after %.17g)", k, x[k], x[k - 1]);
+            if (graded) *graded = 1;
+            break;
+        }
     }
     *tau = t;
+    return SPP_OK;
+}
+
+// bakhvalov-shishkin mesh on the host (spp.h)
+spp_status spp_bakhvalov_mesh(int32_t n, double eps, double sigma, double beta, double *x)
+{
+    if (!x || n < 4 || (n % 2) != 0 || !(eps > 0.0) || eps > 1.0 || !(sigma > 0.0) || !(beta > 0.0))
+        FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_bakhvalov_mesh: bad arguments (n=%d eps=%g sigma=%g beta=%g)", n, eps,
+             sigma, beta);
+    const double sc = sigma * eps / beta, tau = sc * std::log((double)n);
+    if (tau > 0.5) {
+        for (int i = 0; i <= n; ++i) x[i] = (double)i / n;
+        x[n] = 1.0;
+        return SPP_OK;
+    }
+    const int h = n / 2;
+    x[0] = 0.0;
+    for (int i = 1; i < h; ++i) x[i] = -sc * std::log(1.0 - 2.0 * (1.0 - 1.0 / n) * i / n);
+    x[h] = tau;
+    const double H = (1.0 - tau) / h;
+    for (int i = h + 1; i < n; ++i) x[i] = tau + (i - h) * H;
+    x[n] = 1.0;
+    return SPP_OK;
+}
+
+// The mesh-only device arrays (once per context): the widths h_i, k_j of the 2D operator and,
+// per corner level, the widths of its 1D meshes and the geometric interpolation weights from the
+// next coarser level.  On a Shishkin mesh every value is the formula's (R8, R12: widths tau/n,
+// (1-tau)/n, 2^l tau/n; weights 1/2 exactly), so the kernels compute what they computed from the
+// scalar widths; on a graded mesh they are coordinate differences (R21), as in the oracle.
+static spp_status set_mesh_arrays(Ctx *c)
+{
+    const int N = c->N, n = c->n;
+    std::vector<double> wx(N + 2, 0.0), wy(N + 2, 0.0);
+    for (int i = 1; i <= N; ++i) {
+        wx[i] = c->gx ? c->xh[i] - c->xh[i - 1] : (i <= n ? c->hx : c->Hx);
+        wy[i] = c->gy ? c->yh[i] - c->yh[i - 1] : (i <= n ? c->hy : c->Hy);
+    }
+    CK(c, cudaMemcpy(c->wxd, wx.data(), sizeof(double) * (N + 2), cudaMemcpyHostToDevice));
+    CK(c, cudaMemcpy(c->wyd, wy.data(), sizeof(double) * (N + 2), cudaMemcpyHostToDevice));
+    for (int l = 0; l < c->L; ++l) {
+        Level &Lv = c->lev[l];
+        const int nl = Lv.n, step = 1 << l;
+        std::vector<double> lw[2] = {std::vector<double>(nl + 2, 0.0), std::vector<double>(nl + 2, 0.0)};
+        std::vector<double> wt(4 * (size_t)(nl + 2), 0.0);
+        for (int a = 0; a < 2; ++a) {
+            const bool g = a == 0 ? c->gx : c->gy;
+            const std::vector<double> &X = a == 0 ? c->xh : c->yh;
+            const double h = a == 0 ? c->hx : c->hy, H = a == 0 ? c->Hx : c->Hy;
+            for (int q = 1; q <= nl; ++q) lw[a][q] = g ? X[q * step] - X[(q - 1) * step] : h * step;
+            lw[a][nl + 1] = g ? X[n + 1] - X[n] : H;
+            double *wl = wt.data() + (size_t)(2 * a) * (nl + 2), *wr = wl + (nl + 2);
+            for (int q = 1; q < nl; q += 2) {          // odd node q between q-1 and q+1
+                const double u = lw[a][q], v = lw[a][q + 1];
+                wl[q] = u == v ? 0.5 : v / (u + v);
+                wr[q] = u == v ? 0.5 : u / (u + v);
+            }
+        }
+        CK(c, cudaMemcpy(Lv.lwx, lw[0].data(), sizeof(double) * (nl + 2), cudaMemcpyHostToDevice));
+        CK(c, cudaMemcpy(Lv.lwy, lw[1].data(), sizeof(double) * (nl + 2), cudaMemcpyHostToDevice));
+        CK(c, cudaMemcpy((double *)Lv.w.xl, wt.data(), sizeof(double) * 4 * (nl + 2), cudaMemcpyHostToDevice));
+        bool uni = true;                               // all 1/2: the kernels skip the loads
+        for (int a = 0; a < 4; ++a)
+            for (int q = 1; q < nl; q += 2) uni = uni && wt[(size_t)a * (nl + 2) + q] == 0.5;
+        Lv.w.uni = uni ? 1 : 0;
+    }
     return SPP_OK;
 }
 
@@ -477,12 +556,13 @@ static spp_status alloc_all(Ctx *c)
     c->G = (size_t)(N + 1) * c->P;
     const size_t G = c->G;
     // kTmaSlack: the sheared TMA boxes of k_wave may read a few dozen elements past the last row
-    CK(c, cudaMalloc(&c->coef_block, sizeof(double) * (8 * G + 2 * (N + 1) + kTmaSlack)));
-    CK(c, cudaMemsetAsync(c->coef_block, 0, sizeof(double) * (8 * G + 2 * (N + 1) + kTmaSlack), c->st));
+    CK(c, cudaMalloc(&c->coef_block, sizeof(double) * (8 * G + 2 * (N + 1) + 2 * (N + 2) + kTmaSlack)));
+    CK(c, cudaMemsetAsync(c->coef_block, 0, sizeof(double) * (8 * G + 2 * (N + 1) + 2 * (N + 2) + kTmaSlack), c->st));
     c->aE = c->coef_block; c->aN = c->aE + G; c->rr = c->aN + G;
     c->ca = c->rr + G; c->cn = c->ca + G; c->cd = c->cn + G;
     c->ya = c->cd + G; c->yn = c->ya + G;
     c->aW = c->yn + G; c->aS = c->aW + (N + 1);
+    c->wxd = c->aS + (N + 1); c->wyd = c->wxd + (N + 2);
     const size_t per = (size_t)(n - 1) * n;
     CK(c, cudaMalloc(&c->fac, sizeof(double) * (8 * per + 4 * (size_t)n)));
     c->tX = c->fac + 8 * per; c->tY = c->tX + n; c->kapX = c->tY + n; c->kapY = c->kapX + n;
@@ -529,7 +609,7 @@ static spp_status alloc_all(Ctx *c)
         Lv.slo = 1; Lv.shi = Lv.n; Lv.shalo = 0; Lv.sdist = false;
         Lv.pitch = round_up(Lv.n + 2, 16);
         Lv.elems = (size_t)(Lv.n + 2) * Lv.pitch;
-        tot += 5 * Lv.elems + 4 * (size_t)(Lv.n + 2) + (l > 0 ? 6 * Lv.elems : 0);
+        tot += 5 * Lv.elems + 10 * (size_t)(Lv.n + 2) + (l > 0 ? 6 * Lv.elems : 0);
     }
     tot += 3 * c->lev[0].elems;   // Zc, Zc2, Bc
     tot += kTmaSlack;
@@ -541,6 +621,11 @@ static spp_status alloc_all(Ctx *c)
         Lv.b = p; p += Lv.elems; Lv.e = p; p += Lv.elems; Lv.q = p; p += Lv.elems; Lv.rho = p; p += Lv.elems;
         Lv.g = p; p += Lv.elems;
         Lv.aW = p; p += Lv.n + 2; Lv.aS = p; p += Lv.n + 2; Lv.hb = p; p += Lv.n + 2; Lv.kb = p; p += Lv.n + 2;
+        Lv.lwx = p; p += Lv.n + 2; Lv.lwy = p; p += Lv.n + 2;
+        {
+            double *w4 = p; p += 4 * (size_t)(Lv.n + 2);
+            Lv.w = Wts{w4, w4 + (Lv.n + 2), w4 + 2 * (Lv.n + 2), w4 + 3 * (Lv.n + 2), 1};
+        }
         if (l > 0) {
             Lv.own = p;
             double *aE = p; p += Lv.elems; double *aN = p; p += Lv.elems; double *rr = p; p += Lv.elems;
@@ -555,7 +640,7 @@ static spp_status alloc_all(Ctx *c)
     c->Zc = p; p += c->lev[0].elems;
     c->Zc2 = p; p += c->lev[0].elems;
     c->Bc = p; p += c->lev[0].elems;
-    return SPP_OK;
+    return set_mesh_arrays(c);
 }
 
 }  // extern "C"
@@ -599,18 +684,18 @@ spp_status setup_2d_ctx(Ctx *c, const double *c1, const double *c2, const double
     }
     int *bad = c->flags + 200;
     CK(c, cudaMemsetAsync(bad, 0, sizeof(int), c->st));
-    k_coef_1d<<<nblk(N + 1), 256, 0, c->st>>>(N, c->eps, c->hx, c->Hx, c->hy, c->Hy, c->aW, c->aS);
-    k_coef_2d<<<nblk((long)mm), 256, 0, c->st>>>(N, c->P, c->eps, c->hx, c->Hx, c->hy, c->Hy, d1, d2, d3, c->aW,
+    k_coef_1d<<<nblk(N + 1), 256, 0, c->st>>>(N, c->eps, c->wxd, c->wyd, c->aW, c->aS);
+    k_coef_2d<<<nblk((long)mm), 256, 0, c->st>>>(N, c->P, c->eps, c->wxd, c->wyd, d1, d2, d3, c->aW,
                                                 c->aS, c->aE, c->aN, c->rr, c->ca, c->cn, c->cd, c->ya, c->yn, bad);
     Level &L0 = c->lev[0];
-    k_level0_1d<<<1, 256, 0, c->st>>>(N, c->hx, c->Hx, c->hy, c->Hy, c->aW, c->aS, L0.aW, L0.aS, L0.hb, L0.kb);
+    k_level0_1d<<<1, 256, 0, c->st>>>(N, c->wxd, c->wyd, c->aW, c->aS, L0.aW, L0.aS, L0.hb, L0.kb);
     c->launches += 3;
     for (int l = 1; l < c->L; ++l) {
         Level &Lv = c->lev[l];
         // (k_coef_level writes aE/D, aN/D into ya, yn; launch_ycoef then replaces them by the
         // y-form couplings aE/D_E, aN/D_N once the whole cd of the level exists)
-        k_coef_level<<<nblk((long)Lv.n * Lv.n), 256, 0, c->st>>>(N, Lv.n, 1 << l, Lv.pitch, c->eps, c->hx, c->Hx,
-            c->hy, c->Hy, d1, d2, d3, Lv.aW, Lv.aS, Lv.hb, Lv.kb, (double *)Lv.aE, (double *)Lv.aN,
+        k_coef_level<<<nblk((long)Lv.n * Lv.n), 256, 0, c->st>>>(N, Lv.n, 1 << l, Lv.pitch, c->eps, Lv.lwx, Lv.lwy,
+            d1, d2, d3, Lv.aW, Lv.aS, Lv.hb, Lv.kb, (double *)Lv.aE, (double *)Lv.aN,
             (double *)Lv.rr, (double *)Lv.ya, (double *)Lv.yn, (double *)Lv.cd);
         c->launches++;
         if (!c->mg_zform) launch_ycoef(c, Lv.n, Lv.pitch, Lv.aE, Lv.aN, Lv.cd, (double *)Lv.ya, (double *)Lv.yn);
@@ -660,8 +745,9 @@ static spp_status ctx_new(const spp_problem *p, const spp_options *o, void *stre
     spp_status s = check_options(&opt, p->dim, nullptr);
     if (s != SPP_OK) return s;
     double tx = 0, ty = 0;
-    if ((s = check_mesh(p->x, N, &tx, nullptr)) != SPP_OK) return s;
-    if (p->dim == 2 && (s = check_mesh(p->y, N, &ty, nullptr)) != SPP_OK) return s;
+    int gx = 0, gy = 0;
+    if ((s = check_mesh(p->x, N, &tx, nullptr, p->dim == 2, &gx)) != SPP_OK) return s;
+    if (p->dim == 2 && (s = check_mesh(p->y, N, &ty, nullptr, true, &gy)) != SPP_OK) return s;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         FAIL((Ctx *)nullptr, SPP_E_CUDA, "spp_create: no CUDA device (this library has no CPU path)");
@@ -683,6 +769,8 @@ static spp_status ctx_new(const spp_problem *p, const spp_options *o, void *stre
     c->hx = tx / c->n; c->Hx = (1.0 - tx) / c->n;
     c->hy = ty / c->n; c->Hy = (1.0 - ty) / c->n;
     c->xh.assign(p->x, p->x + N + 1);
+    if (p->dim == 2) c->yh.assign(p->y, p->y + N + 1);
+    c->gx = gx; c->gy = gy;
     *out = c;
     return SPP_OK;
 }
@@ -1084,7 +1172,7 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
             Level &C = c->lev[l + 1];
             k_pack_level<<<nblk((long)C.n * C.n), 256, 0, c->st>>>(C.n, C.pitch, in, C.e);
             k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, out, e);
-            k_prolong_add<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, e, C.e, C.pitch);
+            k_prolong_add<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, e, C.e, C.pitch, Lv.w);
             k_unpack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, e, out);
         } else if (s == SPP_STAGE_POST_SMOOTH) {
             // the V-cycle's post-smoothing call: b stored as b/D, e, e_c in the level buffers the

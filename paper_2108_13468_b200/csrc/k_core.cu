@@ -10,15 +10,14 @@ namespace spp {
 
 // ===================================================================================== setup
 // 1D coefficients of the 5-point stencil in difference form (R12):
-// aW_i = eps/(hbar_i h_i), aS_j = eps/(kbar_j k_j).  Widths from the piecewise-uniform formula.
-__global__ void k_coef_1d(int N, double eps, double hx, double Hx, double hy, double Hy,
-                          double *aW, double *aS)
+// aW_i = eps/(hbar_i h_i), aS_j = eps/(kbar_j k_j).  wx[i], wy[j] = h_i, k_j (i = 1..N): the
+// piecewise-uniform formula on a Shishkin mesh, coordinate differences on a graded one (R21).
+__global__ void k_coef_1d(int N, double eps, const double *wx, const double *wy, double *aW, double *aS)
 {
-    const int n = N / 2;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= N; i += gridDim.x * blockDim.x) {
         if (i < 1 || i > N - 1) { aW[i] = 0.0; aS[i] = 0.0; continue; }
-        const double h = i <= n ? hx : Hx, h1 = (i + 1) <= n ? hx : Hx, hb = 0.5 * (h + h1);
-        const double k = i <= n ? hy : Hy, k1 = (i + 1) <= n ? hy : Hy, kb = 0.5 * (k + k1);
+        const double h = wx[i], h1 = wx[i + 1], hb = 0.5 * (h + h1);
+        const double k = wy[i], k1 = wy[i + 1], kb = 0.5 * (k + k1);
         aW[i] = eps / (hb * h);
         aS[i] = eps / (kb * k);
     }
@@ -29,55 +28,55 @@ __global__ void k_coef_1d(int N, double eps, double hx, double Hx, double hy, do
 // P:208-212).  c1, c2, r are compact ((N-1)^2, x fastest).  D_E and D_N (the diagonal
 // at the East / North neighbour) are recomputed from the neighbour's samples with the same
 // arithmetic; beyond the last interior node they are absent (the coupling is 0).
-__device__ __forceinline__ void coef_at(int i, int j, int n, double eps, double hx, double Hx, double hy,
-                                        double Hy, double c1, double c2, double r, const double *aW,
+__device__ __forceinline__ void coef_at(int i, int j, double eps, const double *wx, const double *wy,
+                                        double c1, double c2, double r, const double *aW,
                                         const double *aS, double &e, double &no, double &D)
 {
-    const double h = i <= n ? hx : Hx, h1 = (i + 1) <= n ? hx : Hx, hb = 0.5 * (h + h1);
-    const double k = j <= n ? hy : Hy, k1 = (j + 1) <= n ? hy : Hy, kb = 0.5 * (k + k1);
+    const double h = wx[i], h1 = wx[i + 1], hb = 0.5 * (h + h1);
+    const double k = wy[j], k1 = wy[j + 1], kb = 0.5 * (k + k1);
     e = eps / (hb * h1) + c1 / h1;
     no = eps / (kb * k1) + c2 / k1;
     D = ((aW[i] + e) + (aS[j] + no)) + r;
 }
 
-__global__ void __launch_bounds__(256, 6) k_coef_2d(int N, long P, double eps, double hx, double Hx, double hy, double Hy,
+__global__ void __launch_bounds__(256, 6) k_coef_2d(int N, long P, double eps, const double *wx, const double *wy,
                           const double *c1, const double *c2, const double *r, const double *aW,
                           const double *aS, double *aE, double *aN, double *rr, double *ca,
                           double *cn, double *cd, double *ya, double *yn, int *bad)
 {
-    const int n = N / 2, m = N - 1;
+    const int m = N - 1;
     const long tot = (long)m * m;
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
         const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
         const double a = c1[p], b = c2[p], rv = r[p];
         if (!(a > 0.0) || !(b > 0.0) || !(rv >= 0.0) || !isfinite(a) || !isfinite(b) || !isfinite(rv)) atomicOr(bad, 1);
         double e, no, D;
-        coef_at(i, j, n, eps, hx, Hx, hy, Hy, a, b, rv, aW, aS, e, no, D);
+        coef_at(i, j, eps, wx, wy, a, b, rv, aW, aS, e, no, D);
         const long g = (long)j * P + i;
         aE[g] = e; aN[g] = no; rr[g] = rv;
         ca[g] = e / D; cn[g] = no / D; cd[g] = 1.0 / D;
         double cdE = 0.0, cdN = 0.0, t0, t1, DD;
-        if (i < m) { coef_at(i + 1, j, n, eps, hx, Hx, hy, Hy, c1[p + 1], c2[p + 1], r[p + 1], aW, aS, t0, t1, DD); cdE = 1.0 / DD; }
-        if (j < m) { coef_at(i, j + 1, n, eps, hx, Hx, hy, Hy, c1[p + m], c2[p + m], r[p + m], aW, aS, t0, t1, DD); cdN = 1.0 / DD; }
+        if (i < m) { coef_at(i + 1, j, eps, wx, wy, c1[p + 1], c2[p + 1], r[p + 1], aW, aS, t0, t1, DD); cdE = 1.0 / DD; }
+        if (j < m) { coef_at(i, j + 1, eps, wx, wy, c1[p + m], c2[p + m], r[p + m], aW, aS, t0, t1, DD); cdN = 1.0 / DD; }
         ya[g] = e * cdE; yn[g] = no * cdN;
     }
 }
 
 // Corner multigrid level l >= 1 (R8): re-discretisation on the 1D mesh
-// that keeps every 2^l-th corner node plus x_0 and x_{n+1}; coefficients sampled at the
-// coarse nodes.  Widths: 2^l tau/(N/2) inside, (1-tau)/(N/2) for the last interval.
-__global__ void k_coef_level(int N, int nl, int step, long Pl, double eps, double hx, double Hx,
-                             double hy, double Hy, const double *c1, const double *c2,
+// that keeps every 2^l-th corner node plus x_0 and x_{n+1}; coefficients sampled at the coarse
+// nodes.  lwx[q], lwy[q] (q = 1..nl+1) = that mesh's widths: 2^l tau/(N/2) inside and
+// (1-tau)/(N/2) for the last interval on a Shishkin mesh, coordinate differences on a graded one.
+__global__ void k_coef_level(int N, int nl, int step, long Pl, double eps, const double *lwx, const double *lwy,
+                             const double *c1, const double *c2,
                              const double *r, double *aW, double *aS, double *hb, double *kb,
                              double *aE, double *aN, double *rr, double *ca, double *cn, double *cd)
 {
     const int m = N - 1;
     const long tot = (long)nl * nl;
-    const double h = hx * step, k = hy * step;
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
         const int lq = (int)(p / nl) + 1, q = (int)(p % nl) + 1;
-        const double h1 = (q < nl) ? h : Hx, hbar = 0.5 * (h + h1);
-        const double k1 = (lq < nl) ? k : Hy, kbar = 0.5 * (k + k1);
+        const double h = lwx[q], h1 = lwx[q + 1], hbar = 0.5 * (h + h1);
+        const double k = lwy[lq], k1 = lwy[lq + 1], kbar = 0.5 * (k + k1);
         const double aw = eps / (hbar * h), as = eps / (kbar * k);
         if (lq == 1) { aW[q] = aw; hb[q] = hbar; }
         if (q == 1) { aS[lq] = as; kb[lq] = kbar; }
@@ -94,15 +93,14 @@ __global__ void k_coef_level(int N, int nl, int step, long Pl, double eps, doubl
 
 // Level 0 1D arrays (the level-0 operator is A_CC itself; its coefficients are the global
 // ones): copies of aW, aS on 1..n and hbar, kbar for the FE scaling S_0.
-__global__ void k_level0_1d(int N, double hx, double Hx, double hy, double Hy, const double *aW,
+__global__ void k_level0_1d(int N, const double *wx, const double *wy, const double *aW,
                             const double *aS, double *lW, double *lS, double *hb, double *kb)
 {
     const int n = N / 2;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q <= n + 1; q += gridDim.x * blockDim.x) {
         if (q < 1 || q > n) { lW[q] = 0.0; lS[q] = 0.0; hb[q] = 0.0; kb[q] = 0.0; continue; }
-        const double h1 = (q < n) ? hx : Hx, k1 = (q < n) ? hy : Hy;
         lW[q] = aW[q]; lS[q] = aS[q];
-        hb[q] = 0.5 * (hx + h1); kb[q] = 0.5 * (hy + k1);
+        hb[q] = 0.5 * (wx[q] + wx[q + 1]); kb[q] = 0.5 * (wy[q] + wy[q + 1]);
     }
 }
 
@@ -390,26 +388,13 @@ __global__ void __launch_bounds__(kRedThreads) k_mg_resid(int nl, long Pv, long 
     }
 }
 
-// bilinear interpolation of the coarse correction at fine node (i, j)
-__device__ __forceinline__ double interp(const double *ec, long Pc, int i, int j)
-{
-    // coarse index of even fine node 2I is I; odd 2I+1 is between I and I+1 (ghost 0 at I = 0)
-    const int I0 = i >> 1, J0 = j >> 1;
-    const bool oi = i & 1, oj = j & 1;
-    if (!oi && !oj) return ec[(long)J0 * Pc + I0];
-    if (oi && !oj) return 0.5 * (ec[(long)J0 * Pc + I0] + ec[(long)J0 * Pc + I0 + 1]);
-    if (!oi && oj) return 0.5 * (ec[(long)J0 * Pc + I0] + ec[(long)(J0 + 1) * Pc + I0]);
-    return 0.25 * ((ec[(long)J0 * Pc + I0] + ec[(long)J0 * Pc + I0 + 1]) +
-                   (ec[(long)(J0 + 1) * Pc + I0] + ec[(long)(J0 + 1) * Pc + I0 + 1]));
-}
-
-// prolongation and correction e += P e_c
-__global__ void k_prolong_add(int nl, long Pv, double *e, const double *ec, long Pcv)
+// prolongation and correction e += P e_c, geometric weights W (R21)
+__global__ void k_prolong_add(int nl, long Pv, double *e, const double *ec, long Pcv, Wts W)
 {
     const long tot = (long)nl * nl;
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
         const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
-        e[(long)j * Pv + i] += interp(ec, Pcv, i, j);
+        e[(long)j * Pv + i] += W.uni ? interp_w<true>(ec, Pcv, i, j, W) : interp_w<false>(ec, Pcv, i, j, W);
     }
 }
 

@@ -619,21 +619,12 @@ void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform,
 // g = b + aW e'(i-1,j) + aS e'(i,j-1) with e' = e + P e_c (e_c may be null): the right-hand side
 // of the y-form recurrence of a GS sweep from e' (the parallel W/S part), fused with the
 // prolongation and coarse-grid correction; e' itself is never stored.
-__device__ __forceinline__ double interp_c(const double *ec, long Pc, int i, int j)
-{
-    const int I0 = i >> 1, J0 = j >> 1;
-    const bool oi = i & 1, oj = j & 1;
-    if (!oi && !oj) return ec[(long)J0 * Pc + I0];
-    if (oi && !oj) return 0.5 * (ec[(long)J0 * Pc + I0] + ec[(long)J0 * Pc + I0 + 1]);
-    if (!oi && oj) return 0.5 * (ec[(long)J0 * Pc + I0] + ec[(long)(J0 + 1) * Pc + I0]);
-    return 0.25 * ((ec[(long)J0 * Pc + I0] + ec[(long)J0 * Pc + I0 + 1]) +
-                   (ec[(long)(J0 + 1) * Pc + I0] + ec[(long)(J0 + 1) * Pc + I0 + 1]));
-}
 
+template <bool UNI>
 __global__ void __launch_bounds__(256) k_gs_prep(int nl, long pv, const double *__restrict__ e,
     const double *__restrict__ ec, long pcv, const double *__restrict__ b,
     const double *__restrict__ aW, const double *__restrict__ aS, double *g,
-    const double *__restrict__ cd, long pc, int bscaled, int j0, int j1)
+    const double *__restrict__ cd, long pc, int bscaled, int j0, int j1, Wts W)
 {
     const long tot = (long)nl * (j1 - j0 + 1);         // rows j0 .. j1 of the level
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
@@ -641,8 +632,8 @@ __global__ void __launch_bounds__(256) k_gs_prep(int nl, long pv, const double *
         const long v = (long)j * pv + i;
         double ew = e[v - 1], es = e[v - pv];
         if (ec) {
-            ew += (i > 1) ? interp_c(ec, pcv, i - 1, j) : 0.0;
-            es += (j > 1) ? interp_c(ec, pcv, i, j - 1) : 0.0;
+            ew += (i > 1) ? interp_w<UNI>(ec, pcv, i - 1, j, W) : 0.0;
+            es += (j > 1) ? interp_w<UNI>(ec, pcv, i, j - 1, W) : 0.0;
         }
         if (!cd) { g[v] = (b[v] + aW[i] * ew) + aS[j] * es; continue; }
         const double dinv = cd[(long)j * pc + i];      // z-form sweeps take g / D
@@ -683,8 +674,9 @@ void launch_gs_prep(Ctx *c, int l, const double *b, const double *eold, const do
     const bool zf = c->mg_zform;
     const int j0 = L.sdist ? L.slo : 1, j1 = L.sdist ? L.shi : L.n;
     ProfScope ps(c, 5, (double)L.n * (j1 - j0 + 1) * (zf ? 32.0 : 24.0));
-    k_gs_prep<<<gblocks((long)L.n * (j1 - j0 + 1)), 256, 0, c->st>>>(L.n, L.pitch, eold, ec,
-        ec ? c->lev[l + 1].pitch : 0, b, L.aW, L.aS, L.g, zf ? L.cd : nullptr, L.cpitch, bscaled ? 1 : 0, j0, j1);
+    auto kp = L.w.uni ? k_gs_prep<true> : k_gs_prep<false>;
+    kp<<<gblocks((long)L.n * (j1 - j0 + 1)), 256, 0, c->st>>>(L.n, L.pitch, eold, ec,
+        ec ? c->lev[l + 1].pitch : 0, b, L.aW, L.aS, L.g, zf ? L.cd : nullptr, L.cpitch, bscaled ? 1 : 0, j0, j1, L.w);
     c->launches++;
     dbg_sync(c, "k_gs_prep");
 }
@@ -747,6 +739,7 @@ void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, dou
 struct CoarseLev {
     int n; int cpitch;
     const double *aE, *aN, *rr, *cd, *aW, *aS, *hb, *kb;
+    Wts w;                          // interpolation weights from the next coarser level
 };
 struct CoarseArgs {
     int nlev;                       // levels lc .. lc+nlev-1 (the last is the coarsest)
@@ -851,9 +844,10 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
                 if (j < 1 || j > n) continue;
                 const double *r = rho + j * sf + 2 * I;
                 double rs = r[0];
-                if (2 * I - 1 >= 1) rs = 0.5 * r[-1] + rs;
-                if (2 * I + 1 <= n) rs = rs + 0.5 * r[1];
-                acc += (bb == 0 ? 1.0 : 0.5) * rs;
+                const bool u = F.w.uni;
+                if (2 * I - 1 >= 1) rs = (u ? 0.5 : __ldg(F.w.xr + 2 * I - 1)) * r[-1] + rs;   // P^T: I is 2I-1's right parent
+                if (2 * I + 1 <= n) rs = rs + (u ? 0.5 : __ldg(F.w.xl + 2 * I + 1)) * r[1];    //      and 2I+1's left parent
+                acc += (bb == 0 ? 1.0 : (u ? 0.5 : (bb < 0 ? __ldg(F.w.yr + j) : __ldg(F.w.yl + j)))) * rs;
             }
             B[l + 1][J * sc + I] = acc / (__ldg(C.hb + I) * __ldg(C.kb + J));
         }
@@ -867,14 +861,7 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
         const double *ec = E[l + 1];
         for (int k = threadIdx.x; k < n * n; k += blockDim.x) {        // e += P e_c
             const int j = k / n + 1, i = k % n + 1;
-            const int I0 = i >> 1, J0 = j >> 1;
-            const bool oi = i & 1, oj = j & 1;
-            double v;
-            if (!oi && !oj) v = ec[J0 * sc + I0];
-            else if (oi && !oj) v = 0.5 * (ec[J0 * sc + I0] + ec[J0 * sc + I0 + 1]);
-            else if (!oi && oj) v = 0.5 * (ec[J0 * sc + I0] + ec[(J0 + 1) * sc + I0]);
-            else v = 0.25 * ((ec[J0 * sc + I0] + ec[J0 * sc + I0 + 1]) + (ec[(J0 + 1) * sc + I0] + ec[(J0 + 1) * sc + I0 + 1]));
-            E[l][j * sf + i] += v;
+            E[l][j * sf + i] += a.lv[l].w.uni ? interp_w<true>(ec, sc, i, j, a.lv[l].w) : interp_w<false>(ec, sc, i, j, a.lv[l].w);
         }
         __syncthreads();
         cgs_sweep(a.lv[l], B[l], E[l], sf, cring);                     // post-smoothing
@@ -907,7 +894,7 @@ bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs)
     a.nlev = c->L - lc;
     for (int l = lc; l < c->L; ++l) {
         const Level &L = c->lev[l];
-        a.lv[l - lc] = CoarseLev{L.n, (int)L.cpitch, L.aE, L.aN, L.rr, L.cd, L.aW, L.aS, L.hb, L.kb};
+        a.lv[l - lc] = CoarseLev{L.n, (int)L.cpitch, L.aE, L.aN, L.rr, L.cd, L.aW, L.aS, L.hb, L.kb, L.w};
     }
     a.R = R; a.rpitch = c->lev[lc].pitch; a.rs = rs ? 1 : 0;
     a.out = c->lev[lc].q; a.opitch = c->lev[lc].pitch;
@@ -928,13 +915,13 @@ bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs)
 // (2RT+1)^2 fine nodes it needs is formed once into shared memory, then gathered.  rho is never
 // written to HBM.
 // ------------------------------------------------------------------------------------------
-template <int RT>
+template <int RT, bool UNI>
 __global__ void __launch_bounds__(256, 7) k_resid_restrict(int nf, long pv, long pc, const double *__restrict__ e,
     const double *__restrict__ R, const double *__restrict__ aE, const double *__restrict__ aN,
     const double *__restrict__ rr, const double *__restrict__ aW, const double *__restrict__ aS,
     const double *__restrict__ hbf, const double *__restrict__ kbf, int nc, long pvc,
     const double *__restrict__ hbc, const double *__restrict__ kbc, double *bc,
-    const double *__restrict__ cdc, long pcc, int rs_in, int scale_out, int jc0, int jc1)
+    const double *__restrict__ cdc, long pcc, int rs_in, int scale_out, int jc0, int jc1, Wts W)
 {
     constexpr int RFW = 2 * RT + 1;
     __shared__ double s[RFW * RFW];
@@ -963,11 +950,15 @@ __global__ void __launch_bounds__(256, 7) k_resid_restrict(int nf, long pv, long
         if (I > nc || J > jc1) continue;
         const int li = 2 * (I - I0) + 1, lj = 2 * (J - J0) + 1;
         double acc = 0.0;
+        // P^T with the fine level's geometric weights (R21): coarse I is the right parent of fine
+        // 2I-1 and the left parent of 2I+1 (1/2 each on a Shishkin corner)
+        const double wl = UNI ? 0.5 : __ldg(W.xr + 2 * I - 1), wr = UNI ? 0.5 : __ldg(W.xl + 2 * I + 1);
+        const double wd = UNI ? 0.5 : __ldg(W.yr + 2 * J - 1), wu = UNI ? 0.5 : __ldg(W.yl + 2 * J + 1);
 #pragma unroll
         for (int bb = -1; bb <= 1; ++bb) {
             const double *srow = s + (lj + bb) * RFW + li;
-            const double rs = (0.5 * srow[-1] + srow[0]) + 0.5 * srow[1];
-            acc += (bb == 0 ? 1.0 : 0.5) * rs;
+            const double rs = (wl * srow[-1] + srow[0]) + wr * srow[1];
+            acc += (bb == 0 ? 1.0 : (bb < 0 ? wd : wu)) * rs;
         }
         const double bv = acc / (hbc[I] * kbc[J]);
         bc[(long)J * pvc + I] = scale_out ? bv * cdc[(long)J * pcc + I] : bv;   // z-form: stored as b_c / D_c
@@ -984,9 +975,9 @@ void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e, bool
     // coarse rows: this rank's strip of level l+1 when level l runs on strips
     const int jc0 = F.sdist ? C.slo : 1, jc1 = F.sdist ? C.shi : C.n;
     const dim3 grid((C.n + RTn - 1) / RTn, (jc1 - jc0 + RTn) / RTn);
-#define SPP_RR(T) k_resid_restrict<T><<<grid, T >= 32 ? 256 : (T >= 16 ? 256 : 128), 0, c->st>>>(F.n, F.pitch, \
+#define SPP_RR(T) (F.w.uni ? k_resid_restrict<T, true> : k_resid_restrict<T, false>)<<<grid, T >= 32 ? 256 : (T >= 16 ? 256 : 128), 0, c->st>>>(F.n, F.pitch, \
         F.cpitch, e, R, F.aE, F.aN, F.rr, F.aW, F.aS, F.hb, F.kb, C.n, C.pitch, C.hb, C.kb, C.b, C.cd, C.cpitch, \
-        rs_in ? 1 : 0, scale_out ? 1 : 0, jc0, jc1)
+        rs_in ? 1 : 0, scale_out ? 1 : 0, jc0, jc1, F.w)
     if (RTn == 32) SPP_RR(32);
     else if (RTn == 16) SPP_RR(16);
     else SPP_RR(8);

@@ -4,16 +4,16 @@
 
 namespace spp {
 
-__global__ void k_coef_1d(int N, double eps, double hx, double Hx, double hy, double Hy, double *aW, double *aS);
-__global__ void __launch_bounds__(256, 6) k_coef_2d(int N, long P, double eps, double hx, double Hx, double hy, double Hy,
+__global__ void k_coef_1d(int N, double eps, const double *wx, const double *wy, double *aW, double *aS);
+__global__ void __launch_bounds__(256, 6) k_coef_2d(int N, long P, double eps, const double *wx, const double *wy,
                           const double *c1, const double *c2, const double *r, const double *aW,
                           const double *aS, double *aE, double *aN, double *rr, double *ca,
                           double *cn, double *cd, double *ya, double *yn, int *bad);
-__global__ void k_coef_level(int N, int nl, int step, long Pl, double eps, double hx, double Hx,
-                             double hy, double Hy, const double *c1, const double *c2,
+__global__ void k_coef_level(int N, int nl, int step, long Pl, double eps, const double *lwx, const double *lwy,
+                             const double *c1, const double *c2,
                              const double *r, double *aW, double *aS, double *hb, double *kb,
                              double *aE, double *aN, double *rr, double *ca, double *cn, double *cd);
-__global__ void k_level0_1d(int N, double hx, double Hx, double hy, double Hy, const double *aW,
+__global__ void k_level0_1d(int N, const double *wx, const double *wy, const double *aW,
                             const double *aS, double *lW, double *lS, double *hb, double *kb);
 __global__ void k_pack(int m, long P, const double *src, double *dst, int j0, int nrows);
 __global__ void k_unpack(int m, long P, const double *src, double *dst, int j0, int nrows);
@@ -39,7 +39,7 @@ __global__ void k_mg_resid(int nl, long Pv, long Pc, double *z, const double *e,
                            const double *aE, const double *aN, const double *rr, const double *aW,
                            const double *aS, const double *hb, const double *kb, double *rho,
                            double *part);
-__global__ void k_prolong_add(int nl, long Pv, double *e, const double *ec, long Pcv);
+__global__ void k_prolong_add(int nl, long Pv, double *e, const double *ec, long Pcv, Wts W);
 __global__ void k_corner_out(int n, long P0, const double *zc, long P, double *z, const MGState *ms, int j0, int j1);
 __global__ void k_pack_level(int nl, long Pv, const double *src, double *dst);
 __global__ void k_unpack_level(int nl, long Pv, const double *src, double *dst);

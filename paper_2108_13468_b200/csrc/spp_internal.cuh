@@ -54,6 +54,11 @@ struct LineChain {
 };
 struct LineChunk { int chain, first, last, start; };   // lines [first,last] owned, processing from `start`
 
+// Geometric interpolation weights of the odd nodes of a corner level from the next coarser
+// level (R21): node q between the coarser nodes at its left / right (x) and below /
+// above (y); 1/2 on a uniform (Shishkin) corner.  Device arrays indexed 1..n.
+struct Wts { const double *xl, *xr, *yl, *yr; int uni; };   // uni: every weight is 1/2 (no loads)
+
 struct Level {
     int n = 0;                           // unknowns per axis
     long pitch = 0;                      // value pitch
@@ -62,6 +67,8 @@ struct Level {
     const double *ya = nullptr, *yn = nullptr, *cd = nullptr;   // aE/D_E, aN/D_N, 1/D
     long cpitch = 0;
     double *aW = nullptr, *aS = nullptr, *hb = nullptr, *kb = nullptr;   // 1D [n+2]
+    double *lwx = nullptr, *lwy = nullptr;   // the level's 1D mesh widths, index 1..n+1 [n+2]
+    Wts w{};                             // interpolation weights from level l+1 [n+2 each]
     double *own = nullptr;               // owned coefficient block (levels >= 1)
     double *b = nullptr, *e = nullptr, *q = nullptr, *rho = nullptr;     // work (value layout)
     double *g = nullptr;                 // GS right-hand side (k_gs_prep)
@@ -133,6 +140,8 @@ struct Ctx {
     // mesh (widths from the piecewise-uniform formula with tau = x[N/2])
     double tx = 0, ty = 0, hx = 0, Hx = 0, hy = 0, Hy = 0;
     std::vector<double> xh, yh;
+    int gx = 0, gy = 0;                  // graded (not piecewise-uniform) mesh in x / y (R21)
+    double *wxd = nullptr, *wyd = nullptr;   // device widths h_i, k_j (i = 1..N) [N+2]
     // global padded grid
     long P = 0; size_t G = 0;
     double *aE = nullptr, *aN = nullptr, *rr = nullptr;         // coefficients
@@ -231,6 +240,28 @@ cudaError_t setup_mg_tiles(Ctx *c);
 bool plan_tiles(const Ctx *c, int n, int rows, int halo, int halox, bool whole, Level &L);
 void launch_scale_cd(Ctx *c, int l, const double *b, double *q);
 bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs = false);
+
+// linear interpolation of the coarse correction at fine node (i, j): an even node
+// 2I is the coarse node I; an odd node 2I+1 lies between I and I+1 (the ghost 0 at I = 0), with
+// the level's geometric weights (1/2 on a Shishkin corner: then bit for bit the classical
+// 0.5 (a + b) / 0.25 ((a + b) + (c + d)), every product by 1/2 being exact).
+template <bool UNI = false>
+__device__ __forceinline__ double interp_w(const double *ec, long Pc, int i, int j, const Wts &W)
+{
+    const int I0 = i >> 1, J0 = j >> 1;
+    const bool oi = i & 1, oj = j & 1;
+    const double *r0 = ec + (long)J0 * Pc + I0;
+    if (!oi && !oj) return r0[0];
+    if (UNI) {                                   // the classical weights of a uniform corner
+        if (oi && !oj) return 0.5 * (r0[0] + r0[1]);
+        if (!oi && oj) return 0.5 * (r0[0] + r0[Pc]);
+        return 0.25 * ((r0[0] + r0[1]) + (r0[Pc] + r0[Pc + 1]));
+    }
+    const double xl = W.xl[i], xr = W.xr[i], yl = W.yl[j], yr = W.yr[j];
+    if (oi && !oj) return xl * r0[0] + xr * r0[1];
+    if (!oi && oj) return yl * r0[0] + yr * r0[Pc];
+    return yl * (xl * r0[0] + xr * r0[1]) + yr * (xl * r0[Pc] + xr * r0[Pc + 1]);
+}
 
 // profiling helpers
 void prof_collect(Ctx *c);

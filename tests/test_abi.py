@@ -120,3 +120,13 @@ def test_binding_checks_sizes_dtypes_and_residency():
     import torch
     with pytest.raises(ValueError):   # a host tensor and numpy arrays are one residency; sizes still checked
         spp.Solver(2, 16, 1e-3, x, x, torch.ones(224, dtype=torch.float64), ones, ones)
+
+
+def test_bakhvalov_mesh_matches_oracle_bitwise():
+    import oracle
+    import paper_2108_13468_b200 as spp
+    for N, eps, sg, b in [(8, 1e-3, 2, 1), (256, 1e-4, 2, 1), (4096, 1e-8, 2, 1), (512, 1e-6, 2.5, 1.99),
+                          (64, 1e-2, 2, 1), (128, 1.0, 2, 1)]:
+        assert np.array_equal(spp.spp_bakhvalov_mesh(N, eps, sg, b), oracle.mesh_bs(N, eps, sg, b))
+    with pytest.raises(spp.SppError):
+        spp.spp_bakhvalov_mesh(7, 1e-3)
