@@ -84,6 +84,15 @@ def lib():
         L.orc2_set_mg.argtypes = [ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_int]
         L.orc2_cycle_log.argtypes = [ctypes.c_void_p, _ip, ctypes.c_int]
         L.orc2_direct.argtypes = [ctypes.c_void_p, _dp, _dp, ctypes.c_int]
+        for nm in ("orc2_par", "orc2_plevels"):
+            getattr(L, nm).argtypes = [ctypes.c_void_p]
+        L.orc2_plevel_nx.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        L.orc2_plevel_stencil.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp]
+        L.orc2_pgs.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _dp]
+        L.orc2_pvcycle.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _dp]
+        L.orc2_presidual.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _dp, _dp]
+        L.orc2_prestrict.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _dp]
+        L.orc2_pprolong_add.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _dp]
         _lib = L
     return _lib
 
@@ -210,6 +219,53 @@ class Oracle2D:
     @property
     def levels(self):
         return lib().orc2_levels(self.h)
+
+    # --- parabolic-layer corner (c2 = 0): semi-coarsening Galerkin levels, nine-point (NEXT-2)
+    @property
+    def parabolic(self):
+        return bool(lib().orc2_par(self.h))
+
+    @property
+    def plevels(self):
+        return lib().orc2_plevels(self.h)
+
+    def plevel_shape(self, l):
+        return self.n, lib().orc2_plevel_nx(self.h, l)      # (rows ny, columns nx)
+
+    def _pv(self, l, a=None):
+        ny, nx = self.plevel_shape(l)
+        return np.zeros((ny, nx)) if a is None else _f64(a).reshape(ny, nx)
+
+    def plevel_stencil(self, l):
+        ny, nx = self.plevel_shape(l)
+        a = np.zeros((ny, nx, 9))
+        lib().orc2_plevel_stencil(self.h, l, _p(a))
+        return a                                             # [j-1, i-1, (dj+1)*3 + (di+1)]
+
+    def pgs(self, l, b, e):
+        b, e = self._pv(l, b), self._pv(l, e).copy()
+        lib().orc2_pgs(self.h, l, _p(b), _p(e))
+        return e
+
+    def pvcycle(self, l, b):
+        b, e = self._pv(l, b), self._pv(l)
+        lib().orc2_pvcycle(self.h, l, _p(b), _p(e))
+        return e
+
+    def presidual(self, l, b, e):
+        b, e, r = self._pv(l, b), self._pv(l, e), self._pv(l)
+        lib().orc2_presidual(self.h, l, _p(b), _p(e), _p(r))
+        return r
+
+    def prestrict(self, l, r):
+        r, bc = self._pv(l, r), self._pv(l + 1)
+        lib().orc2_prestrict(self.h, l, _p(r), _p(bc))
+        return bc
+
+    def pprolong_add(self, l, ec, e):
+        ec, e = self._pv(l + 1, ec), self._pv(l, e).copy()
+        lib().orc2_pprolong_add(self.h, l, _p(ec), _p(e))
+        return e
 
     def level_n(self, l):
         return lib().orc2_level_n(self.h, l)

@@ -474,9 +474,23 @@ typedef struct {
     double *wxl, *wxr, *wyl, *wyr;
 } orc_level;
 
+/* One level of the semi-coarsening Galerkin multigrid for the corner when the layer along y = 0
+ * is parabolic (c2 = 0). */
+typedef struct {
+    int nx, ny;                 /* unknowns in x (halved per level) and y (n on every level)  */
+    double *a;                  /* [nx*ny*9] stencil: a[p*9 + (dj+1)*3 + (di+1)] is the entry of
+                                   row (i,j) at column (i+di, j+dj); 0 outside the block        */
+    double *wW, *wE;            /* [nx*ny] interpolation weights of an odd-x node from the coarse
+                                   nodes at x_{i-1} and x_{i+1} (operator-induced) */
+    double *e, *rho, *b;        /* work [nx*ny]                                                */
+} orc_plev;
+
 typedef struct {
     int N, n, m;                /* N intervals; n = N/2 (corner size); m = N-1              */
     int gx, gy;                 /* graded (non-Shishkin) mesh in x / y: widths from coordinates */
+    int par;                    /* c2 = 0: one parabolic + one exponential layer */
+    int PL;                     /* parabolic corner: levels of the semi-coarsening hierarchy  */
+    orc_plev pl[24];
     double eps;
     double *aW, *aS;            /* [N+1], index 1..N-1                                      */
     double *aE, *aN, *rr, *D;   /* [m*m], idx (j-1)*m + (i-1)                              */
@@ -724,6 +738,178 @@ static double fe_norm(const orc_level *Lv, const double *v)
     return sqrt(s);
 }
 
+/* ----- corner multigrid, one parabolic and one exponential layer (c2 = 0) -----
+ * Semi-coarsening: factor-2 coarsening in x only, y kept.  The finest operator is A_CC with row
+ * (i,j) multiplied by hbar_i kbar_j (FE scaling); interpolation to fine node (i,j)
+ * (odd i) from the coarse nodes at x_{i-1}, x_{i+1} with the weights of the stencil collapsed in
+ * the North-South direction:
+ *   wW = -(a_{(i,j),(i-1,j-1)} + a_{(i,j),(i-1,j)} + a_{(i,j),(i-1,j+1)}) / (a_{(i,j),(i,j-1)} + a_{(i,j),(i,j)} + a_{(i,j),(i,j+1)})
+ *   wE = the same with the (i+1) column;
+ * an even fine node is a coarse node (weight 1); restriction = interpolation^T;
+ * coarse operators by the Galerkin triple product R A P, nine-point on coarse
+ * grids; downstream point Gauss-Seidel (top-right to bottom-left), V(1,1), four sweeps on the
+ * coarsest grid; the coarsest has <= 4 points in x (reading R7). */
+#define PST(L, p, di, dj) ((L)->a[(size_t)(p) * 9 + ((dj) + 1) * 3 + ((di) + 1)])
+
+static double pl_at(const orc_plev *L, const double *u, int i, int j)
+{
+    return (i < 1 || j < 1 || i > L->nx || j > L->ny) ? 0.0 : u[(size_t)(j - 1) * L->nx + (i - 1)];
+}
+
+/* interpolation weights of level L from its (next coarser) level */
+static void pl_weights(orc_plev *L)
+{
+    for (int j = 1; j <= L->ny; j++)
+        for (int i = 1; i <= L->nx; i++) {
+            size_t p = (size_t)(j - 1) * L->nx + (i - 1);
+            L->wW[p] = L->wE[p] = 0.0;
+            if ((i & 1) == 0) continue;
+            double den = PST(L, p, 0, -1) + PST(L, p, 0, 0) + PST(L, p, 0, 1);
+            L->wW[p] = -(PST(L, p, -1, -1) + PST(L, p, -1, 0) + PST(L, p, -1, 1)) / den;
+            L->wE[p] = -(PST(L, p, 1, -1) + PST(L, p, 1, 0) + PST(L, p, 1, 1)) / den;
+        }
+}
+
+/* interpolation weight P_{(i,j),(I,j)} of fine node i from coarse node I (0 if not a parent) */
+static double pl_P(const orc_plev *F, int i, int j, int I)
+{
+    size_t p = (size_t)(j - 1) * F->nx + (i - 1);
+    if ((i & 1) == 0) return I == i / 2 ? 1.0 : 0.0;
+    if (I == (i - 1) / 2) return I >= 1 ? F->wW[p] : 0.0;
+    if (I == (i + 1) / 2) return F->wE[p];
+    return 0.0;
+}
+
+/* C = P^T F P (Galerkin), row by row of the fine operator */
+static void pl_galerkin(const orc_plev *F, orc_plev *C)
+{
+    memset(C->a, 0, sizeof(double) * (size_t)C->nx * C->ny * 9);
+    for (int j = 1; j <= F->ny; j++)
+        for (int i = 1; i <= F->nx; i++) {
+            size_t p = (size_t)(j - 1) * F->nx + (i - 1);
+            for (int I = (i - 1) / 2; I <= (i + 1) / 2; I++) {
+                if (I < 1 || I > C->nx) continue;
+                double wi = pl_P(F, i, j, I);
+                if (wi == 0.0) continue;
+                for (int dj = -1; dj <= 1; dj++)
+                    for (int di = -1; di <= 1; di++) {
+                        double a = PST(F, p, di, dj);
+                        if (a == 0.0) continue;
+                        int i2 = i + di, j2 = j + dj;
+                        for (int I2 = (i2 - 1) / 2; I2 <= (i2 + 1) / 2; I2++) {
+                            if (I2 < 1 || I2 > C->nx || i2 < 1 || i2 > F->nx) continue;
+                            double w2 = pl_P(F, i2, j2, I2);
+                            if (w2 == 0.0) continue;
+                            size_t q = (size_t)(j - 1) * C->nx + (I - 1);
+                            PST(C, q, I2 - I, dj) += wi * a * w2;
+                        }
+                    }
+            }
+        }
+}
+
+/* downstream point Gauss-Seidel sweep (j descending, i descending), in place */
+static void pl_gs(const orc_plev *L, const double *b, double *e)
+{
+    for (int j = L->ny; j >= 1; j--)
+        for (int i = L->nx; i >= 1; i--) {
+            size_t p = (size_t)(j - 1) * L->nx + (i - 1);
+            double s = b[p];
+            for (int dj = -1; dj <= 1; dj++)
+                for (int di = -1; di <= 1; di++)
+                    if (di || dj) s -= PST(L, p, di, dj) * pl_at(L, e, i + di, j + dj);
+            e[p] = s / PST(L, p, 0, 0);
+        }
+}
+
+static void pl_residual(const orc_plev *L, const double *b, const double *e, double *rho)
+{
+    for (int j = 1; j <= L->ny; j++)
+        for (int i = 1; i <= L->nx; i++) {
+            size_t p = (size_t)(j - 1) * L->nx + (i - 1);
+            double s = 0.0;
+            for (int dj = -1; dj <= 1; dj++)
+                for (int di = -1; di <= 1; di++) s += PST(L, p, di, dj) * pl_at(L, e, i + di, j + dj);
+            rho[p] = b[p] - s;
+        }
+}
+
+static void pl_restrict(const orc_plev *F, const orc_plev *C, const double *r, double *bc)
+{
+    for (int j = 1; j <= C->ny; j++)
+        for (int I = 1; I <= C->nx; I++) {
+            double s = 0.0;
+            for (int i = 2 * I - 1; i <= 2 * I + 1; i++)
+                if (i <= F->nx) s += pl_P(F, i, j, I) * r[(size_t)(j - 1) * F->nx + (i - 1)];
+            bc[(size_t)(j - 1) * C->nx + (I - 1)] = s;
+        }
+}
+
+static void pl_prolong_add(const orc_plev *F, const orc_plev *C, const double *ec, double *e)
+{
+    for (int j = 1; j <= F->ny; j++)
+        for (int i = 1; i <= F->nx; i++) {
+            double s = 0.0;
+            for (int I = (i - 1) / 2; I <= (i + 1) / 2; I++)
+                if (I >= 1 && I <= C->nx) s += pl_P(F, i, j, I) * ec[(size_t)(j - 1) * C->nx + (I - 1)];
+            e[(size_t)(j - 1) * F->nx + (i - 1)] += s;
+        }
+}
+
+static void pl_vcycle(orc2d *P, int l, const double *b)
+{
+    orc_plev *L = &P->pl[l];
+    size_t nn = (size_t)L->nx * L->ny;
+    memset(L->e, 0, nn * sizeof(double));
+    if (l == P->PL - 1) {
+        for (int s = 0; s < 4; s++) pl_gs(L, b, L->e);
+        return;
+    }
+    orc_plev *C = &P->pl[l + 1];
+    pl_gs(L, b, L->e);
+    pl_residual(L, b, L->e, L->rho);
+    pl_restrict(L, C, L->rho, C->b);
+    pl_vcycle(P, l + 1, C->b);
+    pl_prolong_add(L, C, C->e, L->e);
+    pl_gs(L, b, L->e);
+}
+
+/* the hierarchy, from the corner block of the (level-0) coefficients */
+static int pl_build(orc2d *P)
+{
+    const orc_level *L0 = &P->lev[0];
+    int n = P->n, nx = n, l = 0;
+    for (;;) {
+        orc_plev *L = &P->pl[l];
+        L->nx = nx; L->ny = n;
+        size_t nn = (size_t)nx * n;
+        L->a = calloc(nn * 9, sizeof(double));
+        L->wW = calloc(nn, sizeof(double)); L->wE = calloc(nn, sizeof(double));
+        L->e = calloc(nn, sizeof(double)); L->rho = calloc(nn, sizeof(double)); L->b = calloc(nn, sizeof(double));
+        if (!L->a || !L->wW || !L->wE || !L->e || !L->rho || !L->b) { P->PL = l + 1; return ORC_E_NOMEM; }
+        if (l == 0) {
+            for (int j = 1; j <= n; j++)
+                for (int i = 1; i <= n; i++) {
+                    size_t p = IX(i, j, n);
+                    double S = L0->hb[i] * L0->kb[j];                /* FE row scaling */
+                    PST(L, p, 0, 0) = S * L0->D[p];
+                    if (i > 1) PST(L, p, -1, 0) = -S * L0->aW[i];
+                    if (i < n) PST(L, p, 1, 0) = -S * L0->aE[p];
+                    if (j > 1) PST(L, p, 0, -1) = -S * L0->aS[j];
+                    if (j < n) PST(L, p, 0, 1) = -S * L0->aN[p];
+                }
+        } else {
+            pl_galerkin(&P->pl[l - 1], L);
+        }
+        if (nx <= 4) { P->PL = l + 1; break; }
+        pl_weights(L);
+        nx /= 2;
+        l++;
+        if (l >= 24) return ORC_E_ARG;
+    }
+    return ORC_OK;
+}
+
 /* M_CC^{-1}: stationary iteration with the V-cycle until the corner residual, in the
  * FE-rescaled Euclidean norm ||S_0 rho||_2, drops by the relative factor mg_red = 1e-3
  * (reading R6), starting from z = 0; cap mg_cap cycles.  Returns the
@@ -738,6 +924,31 @@ int orc2_corner_solve(orc2d *P, const double *bC, double *zC, int *cap_hit)
     double b0 = fe_norm(L0, bC);
     int cycles = 0;
     *cap_hit = 0;
+    if (P->par) {
+        /* the same iteration on the FE-scaled corner system (S A_CC) z = S b_C: the
+         * scaled residual S b - (S A_CC) z = S (b - A_CC z) has the norm of reading R6 */
+        orc_plev *Q = &P->pl[0];
+        double *sb = malloc(nn * sizeof(double));
+        for (int j = 1; j <= nl; j++)
+            for (int i = 1; i <= nl; i++) sb[IX(i, j, nl)] = (L0->hb[i] * L0->kb[j]) * bC[IX(i, j, nl)];
+
+        for (;;) {
+            pl_residual(Q, sb, zC, rho);
+            double rn = 0.0;
+            for (size_t p = 0; p < nn; p++) rn += rho[p] * rho[p];
+            if (P->mg_fixed > 0) { if (cycles >= P->mg_fixed) break; }
+            else {
+                if (sqrt(rn) <= P->mg_red * b0) break;
+                if (cycles >= P->mg_cap) { *cap_hit = 1; break; }
+            }
+            pl_vcycle(P, 0, rho);
+            for (size_t p = 0; p < nn; p++) zC[p] += Q->e[p];
+            cycles++;
+        }
+        free(sb);
+        free(rho);
+        return cycles;
+    }
     for (;;) {
         for (size_t p = 0; p < nn; p++) rho[p] = 0.0;
         mg_residual(L0, bC, zC, rho);
@@ -877,6 +1088,10 @@ void orc2_destroy(orc2d *P)
         free(Lv->hb); free(Lv->kb); free(Lv->e); free(Lv->rho); free(Lv->b);
         free(Lv->wxl); free(Lv->wxr); free(Lv->wyl); free(Lv->wyr);
     }
+    for (int l = 0; l < P->PL; l++) {
+        orc_plev *L = &P->pl[l];
+        free(L->a); free(L->wW); free(L->wE); free(L->e); free(L->rho); free(L->b);
+    }
     free(P->cycle_log); free(P->bC); free(P->zC);
     free(P);
 }
@@ -905,6 +1120,11 @@ orc2d *orc2_create(int N, double eps, const double *x, const double *y, const do
     P->L = L;
     for (int l = 0; l < L; l++)
         if (build_level(P, l, x, y, c1, c2, r) != ORC_OK) { P->L = l + 1; orc2_destroy(P); return NULL; }
+    /* c2 = 0 everywhere: one parabolic layer along y = 0, semi-coarsening Galerkin
+     * multigrid in the corner */
+    P->par = 1;
+    for (size_t k = 0; k < mm; k++) if (c2[k] != 0.0) { P->par = 0; break; }
+    if (P->par && pl_build(P) != ORC_OK) { orc2_destroy(P); return NULL; }
     P->mg_red = mg_red; P->mg_cap = mg_cap; P->mg_fixed = mg_fixed;
     P->mg_min = 1 << 30;
     return P;
@@ -1049,3 +1269,21 @@ int orc2_direct(const orc2d *P, const double *f, double *u, int refine)
     free(B); free(res); free(cor);
     return ORC_OK;
 }
+
+/* parabolic-corner accessors for the tests (nine-point levels) */
+int orc2_par(const orc2d *P) { return P->par; }
+int orc2_plevels(const orc2d *P) { return P->par ? P->PL : 0; }
+int orc2_plevel_nx(const orc2d *P, int l) { return P->pl[l].nx; }
+void orc2_plevel_stencil(const orc2d *P, int l, double *a)
+{
+    memcpy(a, P->pl[l].a, sizeof(double) * (size_t)P->pl[l].nx * P->pl[l].ny * 9);
+}
+void orc2_pgs(orc2d *P, int l, const double *b, double *e) { pl_gs(&P->pl[l], b, e); }
+void orc2_pvcycle(orc2d *P, int l, const double *b, double *e)
+{
+    pl_vcycle(P, l, b);
+    memcpy(e, P->pl[l].e, sizeof(double) * (size_t)P->pl[l].nx * P->pl[l].ny);
+}
+void orc2_presidual(orc2d *P, int l, const double *b, const double *e, double *rho) { pl_residual(&P->pl[l], b, e, rho); }
+void orc2_prestrict(orc2d *P, int l, const double *r, double *bc) { pl_restrict(&P->pl[l], &P->pl[l + 1], r, bc); }
+void orc2_pprolong_add(orc2d *P, int l, const double *ec, double *e) { pl_prolong_add(&P->pl[l], &P->pl[l + 1], ec, e); }

@@ -18,6 +18,9 @@ Configurations (BASELINE.json ``configs``, B:7-11):
 Paper workloads (pins):
   ex1d  eq:1D example:   c = 2 + sin 5x, r = 1, f = 4 e^{-x}, C_lower = 0.99
   exp2d eq:exponential_MMS: c = (2,3), r = 1, f = L u*
+  par2d eq:parabolic_MMS: c = (1,0), r = 1, f = L u*: one parabolic layer along
+        y = 0 (transition tau_y = sigma sqrt(eps) ln N, eq:tau parabolic: the y mesh is
+        built with eps_y = sqrt(eps), beta_y = 1) and one exponential layer along x = 0
 """
 from __future__ import annotations
 
@@ -54,6 +57,7 @@ class Config:
     beta_x: float = 1.0
     beta_y: float = 1.0
     weighted: int = 1        # Jacobi-weighted residual (reading R11)
+    eps_y: float | None = None   # layer scale of the y mesh (None: eps); sqrt(eps) for par2d
     stop_abs: int = 0
     seed: int = 0
     kind: str = ""
@@ -76,14 +80,18 @@ def config(name: str, N: int | None = None, eps: float | None = None) -> Config:
         "ex1d": Config("ex1d", 1, 128, 1e-8, 1.0, sigma=2.0, beta_x=0.99, kind="ex1d"),
         "exp2d": Config("exp2d", 2, 128, 1e-6, 1.0, sigma=2.5, beta_x=1.99, beta_y=2.99,
                         weighted=0, stop_abs=1, kind="exp2d"),
+        "par2d": Config("par2d", 2, 128, 1e-6, 1.0, sigma=2.5, beta_x=0.99, beta_y=1.0,
+                        weighted=0, stop_abs=1, kind="par2d"),
     }[name]
     if N is not None:
         base.N = N
     if eps is not None:
         base.eps = eps
-    if name == "exp2d":
+    if name in ("exp2d", "par2d"):
         # paper 2D stop ||R||_2 <= 10 N^{-1} ln N: a workload parameter
         base.tol = 10.0 * np.log(base.N) / base.N
+    if name == "par2d":
+        base.eps_y = float(np.sqrt(base.eps))
     if name == "ex1d":
         base.tol = np.log(base.N) / base.N          # K = 1
     return base
@@ -101,8 +109,19 @@ def _g_cfg2(s, eps):
     return s - (-np.expm1(-s / eps)) / Q
 
 
+def _par_factors(X, Y, e):
+    """eq:parabolic_MMS factors: g(x) = cos(pi x/2) - (e^{-x/eps} - e^{-1/eps})/(1 - e^{-1/eps}),
+    h(y) = (1 - e^{-y/sqrt eps})/(1 - e^{-1/sqrt eps}) - y^{5/2}."""
+    Q = -np.expm1(-1.0 / e)
+    s = np.sqrt(e)
+    R = -np.expm1(-1.0 / s)
+    g = np.cos(np.pi * X / 2) - (np.exp(-X / e) - np.exp(-1.0 / e)) / Q
+    h = -np.expm1(-Y / s) / R - Y ** 2.5
+    return g, h, R, s
+
+
 def exact_solution(cfg: Config, x, y=None):
-    """Manufactured solution u* at interior nodes (cfg2, exp2d)."""
+    """Manufactured solution u* at interior nodes (cfg2, exp2d, par2d)."""
     if cfg.kind == "cfg2":
         X, Y = _grid(x, y)
         return _g_cfg2(X, cfg.eps) * _g_cfg2(Y, cfg.eps)
@@ -111,6 +130,10 @@ def exact_solution(cfg: Config, x, y=None):
         e = cfg.eps
         return (np.cos(np.pi * X / 2) * (-np.expm1(-2 * X / e)) * (1 - Y) ** 3
                 * (-np.expm1(-3 * Y / e)))
+    if cfg.kind == "par2d":
+        X, Y = _grid(x, y)
+        g, h, _, _ = _par_factors(X, Y, cfg.eps)
+        return g * h
     raise KeyError(cfg.kind)
 
 
@@ -183,6 +206,15 @@ def sample_2d(cfg: Config, x, y):
         A2 = -e * P2 * F - 6 * P1 * e2 - 3 * P1 * F
         f = gy * A1 + gx * A2 + gx * gy
         return 2.0 * one, 3.0 * one, one.copy(), f
+    if cfg.kind == "par2d":
+        # -eps Lap u - u_x + u with u = g(x) h(y): the layer parts of g satisfy -eps g'' - g' = 0
+        # exactly, so -eps g'' - g' = eps (pi/2)^2 cos(pi x/2) + (pi/2) sin(pi x/2); and
+        # -eps h'' = e^{-y/sqrt eps}/R + (15/4) eps y^{1/2}
+        g, h, R, s = _par_factors(X, Y, e)
+        Ax = e * (np.pi / 2) ** 2 * np.cos(np.pi * X / 2) + (np.pi / 2) * np.sin(np.pi * X / 2)
+        By = np.exp(-Y / s) / R + 3.75 * e * np.sqrt(Y)
+        f = Ax * h + g * By + g * h
+        return one, 0.0 * one, one.copy(), f
     raise KeyError(cfg.kind)
 
 
