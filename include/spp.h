@@ -48,7 +48,7 @@ typedef enum {
     SPP_NOT_CONVERGED = 1,  /* max_iters reached; last iterate + full history returned */
     SPP_E_ARG = -1,         /* bad argument: N odd/too small, eps not in (0,1], NULL pointer ... */
     SPP_E_MESH = -2,        /* coordinates are not a piecewise-uniform mesh broken at N/2     */
-    SPP_E_COEF = -3,        /* c1 <= 0, c2 <= 0 (2D), r < 0, or non-finite  */
+    SPP_E_COEF = -3,        /* c1 <= 0, c2 < 0 or mixed 0/>0 (2D), r < 0, non-finite */
     SPP_E_PIVOT = -4,       /* zero / non-finite Thomas pivot                          */
     SPP_E_MG_CAP = -5,      /* corner MG hit mg_max_cycles in strict mode                      */
     SPP_E_CUDA = -6,        /* CUDA runtime error, or no usable device                         */
@@ -87,7 +87,14 @@ typedef struct {
                                 spp_bakhvalov_mesh); y NULL in 1D.  On a Shishkin mesh the
                                 library uses tau = x[N/2] and the formula widths (R12).      */
     const double *c1, *c2, *r; /* coefficient samples at interior nodes (compact layout);
-                                c2 NULL in 1D.  Residency per `mem`.                        */
+                                c2 NULL in 1D.  Residency per `mem`.  2D: c1 > 0, r >= 0 and
+                                either c2 > 0 everywhere (two exponential layers) or c2 = 0
+                                everywhere (one parabolic layer along y = 0; the
+                                corner then runs the semi-coarsening Galerkin multigrid of
+                                P:1192-1261, whose paper tolerance is mg_reduction = 1e-2, and
+                                the y mesh wants tau_y = sigma sqrt(eps) ln N, eq:tau
+                                parabolic: spp_shishkin_mesh(N, sqrt(eps), sigma, 1)); a
+                                mixture is SPP_E_COEF.  Row strips support c2 > 0 only.     */
     spp_mem mem;
 } spp_problem;
 

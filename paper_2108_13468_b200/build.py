@@ -10,7 +10,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 SRC = PKG / "csrc"
 LIB = PKG / "lib" / "libspp.so"
-SOURCES = ["capi.cu", "k_core.cu", "k_lines.cu", "k_1d.cu", "k_mg.cu", "dist.cu"]
+SOURCES = ["capi.cu", "k_core.cu", "k_lines.cu", "k_1d.cu", "k_mg.cu", "dist.cu", "k_par.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # <nccl.h> (system include path) for the types only: the library resolves NCCL at run time
 # (dlopen), so libspp.so has no link dependency on it

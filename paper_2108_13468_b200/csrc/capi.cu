@@ -300,7 +300,7 @@ static cudaError_t corner_solve_graph(Ctx *c)
     return cudaSuccess;
 }
 
-static bool graph_mode(const Ctx *c) { return c->use_graph && c->prof_on == 0; }
+static bool graph_mode(const Ctx *c) { return c->use_graph && c->prof_on == 0 && !c->par; }
 
 // M_II solve on region I = [n+1, N-1]^2: z = (D - E - N)^{-1} (s v), s = 1/D
 // (scaled, unweighted mode) or 1 (Jacobi mode: the input is already D v, reading R11); the exact
@@ -334,6 +334,15 @@ static int apply_precond(Ctx *c, const double *v, double *z, int *cap_hit, cudaE
                                                             c->aS, L0.hb, L0.kb, c->weighted, c->Bc, part_slot(c, 1),
                                                             L0.rho, c->cd, c->mg_zform, 1, n);
         c->launches++;
+    }
+    if (c->par) {                                       // parabolic variant (NEXT-2): host-driven loop
+        double b0sq = 0;
+        cudaError_t e = fetch_sum(c, part_slot(c, 1), &b0sq);
+        if (e != cudaSuccess) { *err = e; return 0; }
+        const int cyc = par_corner_solve(c, b0sq, cap_hit, err);
+        k_corner_out<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, c->Zc, c->P, z, nullptr, 1, n);
+        c->launches++;
+        return cyc;
     }
     if (gm) {                                           // cycles known after the caller's next sync
         *err = corner_solve_graph(c);
@@ -703,7 +712,24 @@ spp_status setup_2d_ctx(Ctx *c, const double *c1, const double *c2, const double
     int hbad = 0;
     CK(c, cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
     CK(c, cudaStreamSynchronize(c->st));
-    if (hbad) FAIL(c, SPP_E_COEF, "coefficients violate c1 > 0, c2 > 0, r >= 0 or are not finite (P:208-212, P:907)");
+    if (hbad & 1) FAIL(c, SPP_E_COEF, "coefficients violate c1 > 0, c2 >= 0, r >= 0 or are not finite (P:208-212, P:907)");
+    if ((hbad & 6) == 6)
+        FAIL(c, SPP_E_COEF, "c2 must be > 0 everywhere (two exponential layers) or = 0 everywhere (a parabolic layer, "
+                            "P:872-878)");
+    c->par = (hbad & 4) ? 1 : 0;
+    if (c->par && c->dist) FAIL(c, SPP_E_ARG, "row strips: the parabolic-layer corner (c2 = 0) runs on one GPU only");
+    if (c->par) {                                       // NEXT-2: semi-coarsening Galerkin corner MG
+        if (!c->par_block) CK(c, par_alloc(c));
+        CK(c, setup_lines(c));
+        CK(c, par_setup(c));
+        CK(c, cudaEventRecord(e1, c->st));
+        CK(c, cudaEventSynchronize(e1));
+        cudaEventElapsedTime(&c->setup_ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        CK(c, cudaGetLastError());
+        return SPP_OK;
+    }
     CK(c, setup_lines(c));
     CK(c, setup_mg_tiles(c));
     CK(c, cudaEventRecord(e1, c->st));
@@ -815,7 +841,7 @@ static void ctx_free(Ctx *c)
     for (double *p : c->Z) cudaFree(p);
     cudaFree(c->coef_block); cudaFree(c->fac); cudaFree(c->cbuf); cudaFree(c->w);
     cudaFree(c->part); cudaFree(c->dscal); cudaFree(c->flags); cudaFree(c->mg_block);
-    cudaFree(c->chain); cudaFree(c->chain_flags);
+    cudaFree(c->chain); cudaFree(c->chain_flags); cudaFree(c->par_block);
     cudaFree(c->d_chunks); cudaFree(c->d1);
     if (c->hpin) cudaFreeHost(c->hpin);
     corner_graph_destroy(c);
@@ -1129,6 +1155,15 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
                                                           L0.rr, L0.aW, L0.aS, L0.hb, L0.kb, L0.rho, part_slot(c, 1));
         double b0sq = 0;
         CK(c, fetch_sum(c, part_slot(c, 1), &b0sq));
+        if (c->par) {                                   // parabolic variant: the Galerkin corner MG
+            int cap = 0; cudaError_t err = cudaSuccess;
+            const int k = par_corner_solve(c, b0sq, &cap, &err);
+            CK(c, err);
+            if (cyc) *cyc = k;
+            k_unpack_level<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, c->Zc, out);
+            CK(c, cudaStreamSynchronize(c->st));
+            return SPP_OK;
+        }
         // the first cycle's V-cycle input: b_C (/ D in z-form)
         if (c->mg_zform) launch_scale_cd(c, 0, c->Bc, L0.rho);
         else CK(c, cudaMemcpyAsync(L0.rho, c->Bc, sizeof(double) * L0.elems, cudaMemcpyDeviceToDevice, c->st));

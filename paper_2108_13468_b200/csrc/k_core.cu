@@ -49,7 +49,10 @@ __global__ void __launch_bounds__(256, 6) k_coef_2d(int N, long P, double eps, c
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
         const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
         const double a = c1[p], b = c2[p], rv = r[p];
-        if (!(a > 0.0) || !(b > 0.0) || !(rv >= 0.0) || !isfinite(a) || !isfinite(b) || !isfinite(rv)) atomicOr(bad, 1);
+        // bit 0: invalid (c1 > 0, c2 >= 0, r >= 0, finite: P:208-212); bit 1: some c2 > 0;
+        // bit 2: some c2 = 0 (c2 = 0 everywhere is the parabolic-layer variant)
+        if (!(a > 0.0) || !(b >= 0.0) || !(rv >= 0.0) || !isfinite(a) || !isfinite(b) || !isfinite(rv)) atomicOr(bad, 1);
+        atomicOr(bad, b > 0.0 ? 2 : 4);
         double e, no, D;
         coef_at(i, j, eps, wx, wy, a, b, rv, aW, aS, e, no, D);
         const long g = (long)j * P + i;

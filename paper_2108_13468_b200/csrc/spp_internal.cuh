@@ -85,6 +85,14 @@ struct Level {
     bool sdist = false;
 };
 
+// one level of the parabolic-variant corner multigrid (k_par.cu; c2 = 0)
+struct ParLevel {
+    int nx = 0; long pv = 0;             // unknowns in x (ny = n), value pitch
+    double *a = nullptr;                 // nine-point stencil, 9 compact arrays of n*nx
+    double *wW = nullptr, *wE = nullptr; // interpolation weights of the odd-x nodes [n*nx]
+    double *e = nullptr, *rho = nullptr, *b = nullptr;   // padded value layout
+};
+
 // corner GS sweep arguments (k_mg.cu)
 // downstream sweep on [1, nl]^2 (k_mg.cu): y = q + ca y_E + cn y_N, z = cd y (y-form) or z = y
 struct WaveArgs {
@@ -202,6 +210,10 @@ struct Ctx {
     int use_graph = 1;
     int no_lines_tma = 0;                  // SPP_NO_LINES_TMA=1: LSU-loaded line kernel
     int mg_zform = 1;                      // corner GS sweeps in z-form (SPP_MG_YFORM=1: y-form)
+    // parabolic-layer variant (c2 = 0 everywhere; NEXT-2): semi-coarsening Galerkin corner MG
+    int par = 0, PL = 0;
+    ParLevel plev[kMaxLevels];
+    double *par_block = nullptr, *par_sb = nullptr, *par_rho = nullptr;
     // row strips: the decomposition this context is one strip of (nullptr: one
     // GPU), the strip's rank, and the partial-sum segments per reduction slot (one per strip)
     Dist *dist = nullptr;
@@ -237,6 +249,9 @@ void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew,
                          double *part, const MGState *ms = nullptr);
 void launch_lines(Ctx *c, const double *v, double *z);
 cudaError_t setup_mg_tiles(Ctx *c);
+cudaError_t par_alloc(Ctx *c);
+cudaError_t par_setup(Ctx *c);
+int par_corner_solve(Ctx *c, double b0sq, int *cap_hit, cudaError_t *err);
 bool plan_tiles(const Ctx *c, int n, int rows, int halo, int halox, bool whole, Level &L);
 void launch_scale_cd(Ctx *c, int l, const double *b, double *q);
 bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs = false);
