@@ -340,24 +340,30 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
         // step earlier, and the pair shares one 16-byte swizzle unit: one 128-bit load per array).
         // Every shared-memory load of the chunk is issued before the first store: a store ahead
         // of a possibly aliasing load would serialise the load behind it.
-        double2 Q[8], A1[8], A2[8];
-#pragma unroll
-        for (int st = 0; st < 8; ++st) {                        // columns 2st, 2st+1 of the chunk
-            Q[st] = *reinterpret_cast<const double2 *>(sq + xo[st]);     // (2st+1, 2st) as (lo, hi)
-            A1[st] = *reinterpret_cast<const double2 *>(sq + WBOX + xo[st]);
-            A2[st] = *reinterpret_cast<const double2 *>(sq + 2 * WBOX + xo[st]);
-        }
+        // The operands of a step are loaded at that step (volatile asm: the compiler keeps them
+        // there).  Issued as one burst of 24 128-bit loads before the steps, they queued in the
+        // shared-memory pipe ahead of the shuffles of the dependent step chain (measured: cfg4
+        // 21.0 -> 19.3 ms/solve; loading one or two steps ahead, or storing per step, is slower).
+        // The stores below touch only the q slots of this chunk's columns: no load aliases them.
+        auto lds2 = [](const double *pp) {
+            double2 v;
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"((unsigned)__cvta_generic_to_shared(pp)));
+            return v;
+        };
         if (w > 0 && lane == 0) *((volatile int *)&cons[w]) = need;
         auto steps = [&](auto fast_tag) {
             constexpr bool F = decltype(fast_tag)::value;
             double Z[16];
 #pragma unroll
             for (int st = 0; st < 8; ++st) {
+                const double2 Q = lds2(sq + xo[st]);                 // (2st+1, 2st) as (lo, hi)
+                const double2 A1 = lds2(sq + WBOX + xo[st]);
+                const double2 A2 = lds2(sq + 2 * WBOX + xo[st]);
                 double n0 = __shfl_up_sync(0xffffffffu, z2, 1);    // lane t-1's pair of the last step
                 double n1 = __shfl_up_sync(0xffffffffu, z1, 1);
                 if (lane == 0) { n0 = E[st].x; n1 = E[st].y; }
-                double za = fma(A1[st].y, z1, fma(A2[st].y, n0, Q[st].y));   // column 2st   (east one first)
-                double zc = fma(A1[st].x, za, fma(A2[st].x, n1, Q[st].x));   // column 2st+1
+                double za = fma(A1.y, z1, fma(A2.y, n0, Q.y));      // column 2st   (east one first)
+                double zc = fma(A1.x, za, fma(A2.x, n1, Q.x));      // column 2st+1
                 if (!F) {
                     const int idx = c * WCW + 2 * st - WLAG * lane;
                     za = (rvalid && idx >= 0 && idx < ncols) ? za : 0.0;
