@@ -231,53 +231,75 @@ static void corner_graph_destroy(Ctx *c)
     c->cg_exec = nullptr; c->cg = nullptr; c->cg_sig.clear();
 }
 
+// During a capture on c->st into graph g: append a node of type `type` (a conditional with handle
+// h) after the captured work, continue the capture after it; *body = its body graph.
+static cudaError_t capture_add_conditional(Ctx *c, cudaGraph_t g, cudaGraphConditionalHandle h,
+                                           cudaGraphConditionalNodeType type, cudaGraph_t *body)
+{
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    SPP_CUDA_TRY(cudaStreamGetCaptureInfo(c->st, &cs, nullptr, nullptr, &deps, &nd));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = type;
+    cp.conditional.size = 1;
+    cudaGraphNode_t wn = nullptr;
+    SPP_CUDA_TRY(cudaGraphAddNode(&wn, g, deps, nd, &cp));
+    SPP_CUDA_TRY(cudaStreamUpdateCaptureDependencies(c->st, &wn, 1, cudaStreamSetCaptureDependencies));
+    *body = cp.conditional.phGraph_out[0];
+    return cudaSuccess;
+}
+
+// During a capture on c->st into graph g: the corner stationary iteration as k_mg_init + a while
+// node (handle *h, created on g); *body receives the (empty) loop body for corner_body.
+static cudaError_t capture_corner_loop(Ctx *c, cudaGraph_t g, cudaGraphConditionalHandle *h, cudaGraph_t *body)
+{
+    SPP_CUDA_TRY(cudaGraphConditionalHandleCreate(h, g, 0, 0));
+    k_mg_init<<<1, 1, 0, c->st>>>(part_slot(c, 1), c->mgs, c->Zc, c->Zc2, c->opt.mg_reduction, c->opt.mg_max_cycles,
+                                  c->opt.mg_fixed_cycles, *h);
+    c->launches++;
+    return capture_add_conditional(c, g, *h, cudaGraphCondTypeWhile, body);
+}
+
+// the corner loop body (one V-cycle, the update z' = z + e with rho = b_C - A_CC z', the check),
+// captured on c->st (no capture active); sets c->cg_body_launches
+static cudaError_t corner_body(Ctx *c, cudaGraph_t body, cudaGraphConditionalHandle h)
+{
+    Level &L0 = c->lev[0];
+    SPP_CUDA_TRY(cudaStreamBeginCaptureToGraph(c->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    const int64_t b0 = c->launches;
+    const double *ev = vcycle(c, 0, L0.rho, c->mg_zform);
+    launch_cycle_update(c, nullptr, ev, nullptr, c->Bc, L0.rho, part_slot(c, 0), c->mgs);
+    k_mg_check<<<1, 1, 0, c->st>>>(part_slot(c, 0), c->mgs, c->opt.mg_reduction, c->opt.mg_max_cycles,
+                                   c->opt.mg_fixed_cycles, h);
+    c->launches++;
+    c->cg_body_launches = c->launches - b0;
+    cudaGraph_t tmp = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->st, &tmp);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 static cudaError_t corner_graph_build(Ctx *c)
 {
     corner_graph_destroy(c);
     if (!c->cap_st) SPP_CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_st, cudaStreamNonBlocking));
-    Level &L0 = c->lev[0];
-    const double red = c->opt.mg_reduction;
-    const int maxc = c->opt.mg_max_cycles, fixed = c->opt.mg_fixed_cycles;
     cudaGraph_t g = nullptr;
     SPP_CUDA_TRY(cudaGraphCreate(&g, 0));
     cudaGraphConditionalHandle h;
-    SPP_CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
     cudaStream_t user = c->st;
     const int prof = c->prof_on;
     const int64_t l0 = c->launches;
     c->st = c->cap_st; c->prof_on = 0; c->capturing = true;
     cudaError_t e = cudaStreamBeginCaptureToGraph(c->st, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
-        k_mg_init<<<1, 1, 0, c->st>>>(part_slot(c, 1), c->mgs, c->Zc, c->Zc2, red, maxc, fixed, h);
-        cudaStreamCaptureStatus cs;
-        const cudaGraphNode_t *deps = nullptr;
-        size_t nd = 0;
-        e = cudaStreamGetCaptureInfo(c->st, &cs, nullptr, nullptr, &deps, &nd);
-        cudaGraphNodeParams cp = {};
-        cp.type = cudaGraphNodeTypeConditional;
-        cp.conditional.handle = h;
-        cp.conditional.type = cudaGraphCondTypeWhile;
-        cp.conditional.size = 1;
-        cudaGraphNode_t wn = nullptr;
-        if (e == cudaSuccess) e = cudaGraphAddNode(&wn, g, deps, nd, &cp);
-        if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(c->st, &wn, 1, cudaStreamSetCaptureDependencies);
+        cudaGraph_t body = nullptr;
+        e = capture_corner_loop(c, g, &h, &body);
         cudaGraph_t tmp = nullptr;
         const cudaError_t e2 = cudaStreamEndCapture(c->st, &tmp);
         if (e == cudaSuccess) e = e2;
-        if (e == cudaSuccess) {                         // the loop body: one cycle
-            cudaGraph_t body = cp.conditional.phGraph_out[0];
-            e = cudaStreamBeginCaptureToGraph(c->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
-            if (e == cudaSuccess) {
-                const int64_t b0 = c->launches;
-                const double *ev = vcycle(c, 0, L0.rho, c->mg_zform);
-                launch_cycle_update(c, nullptr, ev, nullptr, c->Bc, L0.rho, part_slot(c, 0), c->mgs);
-                k_mg_check<<<1, 1, 0, c->st>>>(part_slot(c, 0), c->mgs, red, maxc, fixed, h);
-                c->launches++;
-                c->cg_body_launches = c->launches - b0;
-                const cudaError_t e3 = cudaStreamEndCapture(c->st, &tmp);
-                e = e3 != cudaSuccess ? e3 : cudaGetLastError();
-            }
-        }
+        if (e == cudaSuccess) e = corner_body(c, body, h);   // the loop body: one cycle
     }
     c->st = user; c->prof_on = prof; c->capturing = false;
     c->launches = l0;
@@ -318,23 +340,30 @@ static void launch_mii(Ctx *c, const double *v, double *z, bool scaled)
 
 // z = M^{-1} v (eq:2D blocks by block back-substitution I -> Y -> X -> C).
 // v, z: padded global grids.  In Jacobi mode the preconditioner input is D v (reading R11).
-static int apply_precond(Ctx *c, const double *v, double *z, int *cap_hit, cudaError_t *err)
+// the blocks of M^{-1} before the corner solve: M_II, then M_YY and M_XX, then the corner's
+// right-hand side b_C (with ||S0 b_C||^2 partials in part slot 1)
+static void precond_head(Ctx *c, const double *v, double *z)
 {
     const int N = c->N, n = c->n;
     // M_II: exact downstream triangular solve on region I
     launch_mii(c, v, z, !c->weighted);
     // M_YY and M_XX (one launch, both chains)
     launch_lines(c, v, z);
+    Level &L0 = c->lev[0];
+    ProfScope ps(c, 9, 40.0 * (double)n * n);
+    k_corner_rhs<<<red_grid((long)n * n), kRedThreads, 0, c->st>>>(N, c->P, L0.pitch, v, z, c->aE, c->aN, c->rr, c->aW,
+                                                        c->aS, L0.hb, L0.kb, c->weighted, c->Bc, part_slot(c, 1),
+                                                        L0.rho, c->cd, c->mg_zform, 1, n);
+    c->launches++;
+}
+
+static int apply_precond(Ctx *c, const double *v, double *z, int *cap_hit, cudaError_t *err)
+{
+    const int n = c->n;
+    precond_head(c, v, z);
     // corner
     Level &L0 = c->lev[0];
     const bool gm = graph_mode(c);
-    {
-        ProfScope ps(c, 9, 40.0 * (double)n * n);
-        k_corner_rhs<<<red_grid((long)n * n), kRedThreads, 0, c->st>>>(N, c->P, L0.pitch, v, z, c->aE, c->aN, c->rr, c->aW,
-                                                            c->aS, L0.hb, L0.kb, c->weighted, c->Bc, part_slot(c, 1),
-                                                            L0.rho, c->cd, c->mg_zform, 1, n);
-        c->launches++;
-    }
     if (c->par) {                                       // parabolic variant (NEXT-2): host-driven loop
         double b0sq = 0;
         cudaError_t e = fetch_sum(c, part_slot(c, 1), &b0sq);
@@ -364,6 +393,205 @@ static int apply_precond(Ctx *c, const double *v, double *z, int *cap_hit, cudaE
     k_corner_out<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, zc, c->P, z, nullptr, 1, n);
     c->launches++;
     return cyc;
+}
+
+// w = W A z_k with <w, v_0>, then modified Gram-Schmidt: h_{j,k} for j = 0..k into
+// dscal[0..k], ||w|| into dscal[k+1], v_{k+1} = w / ||w||
+static void krylov_tail(Ctx *c, int k)
+{
+    const int m = c->m;
+    const long G = (long)c->G;
+    const double mm = (double)m * m;
+    {
+        ProfScope ps(c, 0, 48.0 * mm);
+        k_spmv<<<red_grid((long)m * m), kRedThreads, 0, c->st>>>(m, c->P, c->Z[k], c->aE, c->aN, c->rr, c->aW, c->aS,
+                                                                  c->weighted, c->w, c->V[0], part_slot(c, 0), 1, m);
+        c->launches++;
+    }
+    for (int j = 1; j <= k; ++j) {
+        ProfScope ps(c, 7, 32.0 * G);
+        k_mgs<<<red_grid(G), kRedThreads, 0, c->st>>>(G, c->w, c->V[j - 1], part_slot(c, j - 1), c->dscal + (j - 1),
+                                                     c->V[j], part_slot(c, j), 1);
+        c->launches++;
+    }
+    {
+        ProfScope ps(c, 7, 24.0 * G + 16.0 * G);
+        k_mgs<<<red_grid(G), kRedThreads, 0, c->st>>>(G, c->w, c->V[k], part_slot(c, k), c->dscal + k, c->w,
+                                                     part_slot(c, k + 1), 1);
+        k_normalize<<<red_grid(G), kRedThreads, 0, c->st>>>(G, c->w, part_slot(c, k + 1), c->dscal + k + 1, c->V[k + 1], 1);
+        c->launches += 2;
+    }
+}
+
+// ------------------------------------------------------------------------------------------ Givens
+// The least-squares update of GMRES (Saad 2003, Alg. 6.9 via plane rotations), shared
+// by the host loop and the device-side step of the iteration graphs so both make bit-identical
+// decisions: explicit fma and a scaled sqrt in place of hypot (whose rounding differs between
+// the host and device libraries).
+__host__ __device__ inline double rot_norm(double a, double b)
+{
+    const double m = fmax(fabs(a), fabs(b));
+    if (m == 0.0) return 0.0;
+    const double x = a / m, y = b / m;
+    return m * sqrt(fma(x, x, y * y));
+}
+// rotate column h (h[0..k+1]) by the previous rotations, form rotation k, update g; returns |g_{k+1}|
+__host__ __device__ inline double givens_update(double *h, double *cs, double *sn, double *g, int k, int *brk)
+{
+    for (int i = 0; i < k; ++i) {
+        const double t = fma(cs[i], h[i], sn[i] * h[i + 1]);
+        h[i + 1] = fma(-sn[i], h[i], cs[i] * h[i + 1]);
+        h[i] = t;
+    }
+    const double den = rot_norm(h[k], h[k + 1]);
+    if (den == 0.0) { cs[k] = 1.0; sn[k] = 0.0; }
+    else { cs[k] = h[k] / den; sn[k] = h[k + 1] / den; }
+    *brk = h[k + 1] == 0.0;                            // happy breakdown: w in span(V)
+    h[k] = den; h[k + 1] = 0.0;
+    g[k + 1] = -sn[k] * g[k];
+    g[k] = cs[k] * g[k];
+    return fabs(g[k + 1]);
+}
+// the stop test after iteration k (0-based) with residual res; *converged set when stopping
+__host__ __device__ inline int fg_stop(int k, double res, int brk, double target, int fixed, int maxit, int *converged)
+{
+    if (brk) { *converged = res <= target; return 1; }
+    if (fixed > 0) {
+        if (k + 1 >= fixed) { *converged = res <= target; return 1; }
+    } else if (res <= target) { *converged = 1; return 1; }
+    return k + 1 >= maxit;
+}
+
+// ------------------------------------------------------------------------------------------ iteration graphs
+// Small problems are launch- and synchronisation-bound (cfg2: 52 iterations of ~100 launches).
+// Iteration k of FGMRES becomes one CUDA graph: a gate kernel sets an IF node from the device
+// state (nothing runs once the loop has stopped); its body is the whole iteration (M^{-1} with the
+// corner stationary iteration as a nested while node, W A z_k, MGS) followed by k_fg_step, the
+// Givens update and stop test on the device.  The host launches the graphs in batches (the first
+// as long as the previous solve) and synchronises once per batch.  The kernels and their order
+// are the host loop's, so the iterates are bit for bit the same.
+__global__ void k_fg_init(FGHead *s, double *g, double *hist, double beta, double target)
+{
+    s->target = target;
+    s->k = 0; s->stop = 0; s->converged = 0; s->nonfinite = 0; s->nf_j = 0; s->capfail = 0;
+    s->mg_tot = 0; s->mg_min = 1 << 30; s->mg_max = 0; s->caps = 0;
+    s->res = beta;
+    g[0] = beta; hist[0] = beta;
+}
+__global__ void k_fg_gate(const FGHead *s, cudaGraphConditionalHandle h) { cudaGraphSetConditional(h, s->stop ? 0 : 1); }
+__global__ void k_fg_step(FGHead *s, double *H, double *cs, double *sn, double *g, double *hist, const double *hsrc,
+                          const MGState *ms, int k, int ld, int fixed, int maxit, int strict)
+{
+    s->k = k + 1;
+    if (ms) {
+        const int cyc = ms->cycles, cap = ms->cap;
+        s->mg_tot += cyc; s->mg_min = min(s->mg_min, cyc); s->mg_max = max(s->mg_max, cyc); s->caps += cap;
+        if (cap && strict) { s->capfail = 1; s->stop = 1; return; }
+    }
+    double *h = H + (size_t)k * ld;
+    for (int j = 0; j <= k + 1; ++j) {
+        h[j] = hsrc[j];
+        if (!isfinite(h[j])) { s->nonfinite = 1; s->nf_j = j; s->stop = 1; return; }
+    }
+    int brk = 0, conv = 0;
+    const double res = givens_update(h, cs, sn, g, k, &brk);
+    hist[k + 1] = res;
+    s->res = res;
+    if (fg_stop(k, res, brk, s->target, fixed, maxit, &conv)) { s->stop = 1; s->converged = conv; }
+}
+
+static bool fg_mode(const Ctx *c) { return graph_mode(c) && c->fg_ok && !c->dist; }
+
+static std::vector<long> fg_signature(const Ctx *c)
+{
+    // everything the captured launches take by value besides fixed buffers: the level plans, the
+    // line-chunk plan (it follows the coefficients, so a re-setup may change it), the options
+    std::vector<long> v = corner_signature(c);
+    v.push_back(c->weighted); v.push_back((long)(size_t)c->d_chunks); v.push_back(c->lines_threads);
+    for (const LineChunk &k : c->chunks) { v.push_back(k.chain); v.push_back(k.first); v.push_back(k.last); v.push_back(k.start); }
+    v.push_back((long)(c->opt.tol * 1e15)); v.push_back(c->opt.stop); v.push_back(c->opt.fixed_iters);
+    v.push_back(c->opt.mg_strict); v.push_back(c->opt.max_iters);
+    return v;
+}
+
+static void fg_destroy(Ctx *c)
+{
+    for (auto e : c->itg) if (e) cudaGraphExecDestroy(e);
+    c->itg.clear(); c->itg_launches.clear(); c->itg_sig.clear();
+}
+
+static cudaError_t fg_alloc(Ctx *c)
+{
+    if (c->fgh) return cudaSuccess;
+    const size_t ld = (size_t)c->opt.max_iters + 1;
+    SPP_CUDA_TRY(cudaMalloc(&c->fgh, sizeof(FGHead)));
+    SPP_CUDA_TRY(cudaMallocHost(&c->hfgh, sizeof(FGHead)));
+    SPP_CUDA_TRY(cudaMalloc(&c->fgd, sizeof(double) * (ld * ld + 4 * (ld + 1))));
+    return cudaMemsetAsync(c->fgd, 0, sizeof(double) * (ld * ld + 4 * (ld + 1)), c->st);
+}
+
+// device arrays of the FGMRES state: H (column k at k * ld), cs, sn, g, hist
+static double *fg_H(Ctx *c) { return c->fgd; }
+static double *fg_arr(Ctx *c, int a)
+{
+    const size_t ld = (size_t)c->opt.max_iters + 1;
+    return c->fgd + ld * ld + (size_t)a * (ld + 1);
+}
+
+// capture graph k (V[k+1], Z[k] allocated)
+static cudaError_t fg_build(Ctx *c, int k, cudaGraphExec_t *out)
+{
+    if (!c->cap_st) SPP_CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_st, cudaStreamNonBlocking));
+    const int ld = c->opt.max_iters + 1;
+    cudaGraph_t g = nullptr;
+    SPP_CUDA_TRY(cudaGraphCreate(&g, 0));
+    cudaStream_t user = c->st;
+    const int prof = c->prof_on;
+    const int64_t l0 = c->launches;
+    c->st = c->cap_st; c->prof_on = 0; c->capturing = true;
+    int64_t body_launches = 0;
+    cudaGraph_t ifb = nullptr, wb = nullptr;
+    cudaGraphConditionalHandle hif, hw;
+    cudaError_t e = cudaGraphConditionalHandleCreate(&hif, g, 0, 0);
+    if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(c->st, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        k_fg_gate<<<1, 1, 0, c->st>>>(c->fgh, hif);
+        e = capture_add_conditional(c, g, hif, cudaGraphCondTypeIf, &ifb);
+        cudaGraph_t tmp = nullptr;
+        const cudaError_t e2 = cudaStreamEndCapture(c->st, &tmp);
+        if (e == cudaSuccess) e = e2;
+    }
+    if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(c->st, ifb, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        const int64_t b0 = c->launches;
+        const int n = c->n;
+        Level &L0 = c->lev[0];
+        precond_head(c, c->V[k], c->Z[k]);
+        e = capture_corner_loop(c, ifb, &hw, &wb);
+        if (e == cudaSuccess) {
+            k_corner_out<<<nblk((long)n * n), 256, 0, c->st>>>(n, L0.pitch, nullptr, c->P, c->Z[k], c->mgs, 1, n);
+            c->launches++;
+            krylov_tail(c, k);
+            k_fg_step<<<1, 1, 0, c->st>>>(c->fgh, fg_H(c), fg_arr(c, 0), fg_arr(c, 1), fg_arr(c, 2), fg_arr(c, 3),
+                                          c->dscal, c->mgs, k, ld, c->opt.fixed_iters, c->opt.max_iters,
+                                          c->opt.mg_strict);
+            c->launches++;
+        }
+        body_launches = c->launches - b0;
+        cudaGraph_t tmp = nullptr;
+        const cudaError_t e2 = cudaStreamEndCapture(c->st, &tmp);
+        if (e == cudaSuccess) e = e2;
+    }
+    if (e == cudaSuccess) e = corner_body(c, wb, hw);
+    c->st = user; c->prof_on = prof; c->capturing = false;
+    c->launches = l0;
+    if (e == cudaSuccess && c->sticky != cudaSuccess) { e = c->sticky; c->sticky = cudaSuccess; }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(out, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) { *out = nullptr; return e; }
+    if ((int)c->itg_launches.size() <= k) c->itg_launches.resize(k + 1, 0);
+    c->itg_launches[k] = body_launches;
+    return cudaSuccess;
 }
 
 }  // namespace spp
@@ -594,6 +822,8 @@ static spp_status alloc_all(Ctx *c)
     {
         const char *ng = getenv("SPP_NO_GRAPH");
         c->use_graph = !(ng && ng[0] == '1');
+        const char *nig = getenv("SPP_NO_ITER_GRAPH");
+        c->fg_ok = (nig && nig[0] == '1') ? 0 : 1;
         const char *nl = getenv("SPP_NO_LINES_TMA");
         c->no_lines_tma = (nl && nl[0] == '1') ? 1 : 0;
         const char *yf = getenv("SPP_MG_YFORM");
@@ -845,6 +1075,9 @@ static void ctx_free(Ctx *c)
     cudaFree(c->d_chunks); cudaFree(c->d1);
     if (c->hpin) cudaFreeHost(c->hpin);
     corner_graph_destroy(c);
+    fg_destroy(c);
+    cudaFree(c->fgh); cudaFree(c->fgd);
+    if (c->hfgh) cudaFreeHost(c->hfgh);
     if (c->cap_st) cudaStreamDestroy(c->cap_st);
     cudaFree(c->mgs);
     if (c->hmgs) cudaFreeHost(c->hmgs);
@@ -931,6 +1164,44 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
         k_scale<<<nblk(G / 2), 256, 0, c->st>>>(G, c->V[0], 1.0 / beta);
         c->launches++;
         g[0] = beta;
+        const int ld = maxit + 1;
+        if (fg_mode(c)) {                               // iteration graphs, one sync per batch
+            CK(c, fg_alloc(c));
+            const std::vector<long> sig = fg_signature(c);
+            if (c->itg_sig != sig) { fg_destroy(c); c->itg_sig = sig; }
+            k_fg_init<<<1, 1, 0, c->st>>>(c->fgh, fg_arr(c, 2), fg_arr(c, 3), beta, target);
+            c->launches++;
+            int launched = 0;
+            int batch = std::max(1, std::min(maxit, c->last_iters > 0 ? c->last_iters : 4));
+            for (;;) {
+                for (int b = 0; b < batch && launched < maxit; ++b, ++launched) {
+                    const int k = launched;
+                    CK(c, ensure_vectors(c, k + 1));
+                    if ((int)c->itg.size() <= k) c->itg.resize(k + 1, nullptr);
+                    if (!c->itg[k]) CK(c, fg_build(c, k, &c->itg[k]));
+                    CK(c, cudaGraphLaunch(c->itg[k], c->st));
+                    c->launches++;                      // the gate
+                }
+                CK(c, cudaMemcpyAsync(c->hfgh, c->fgh, sizeof(FGHead), cudaMemcpyDeviceToHost, c->st));
+                CK(c, cudaStreamSynchronize(c->st));
+                if (c->hfgh->stop || launched >= maxit) break;
+                batch = 8;
+            }
+            const FGHead fs = *c->hfgh;
+            if (fs.nonfinite)
+                FAIL(c, SPP_E_NONFINITE, "Hessenberg entry h(%d,%d) is not finite at iteration %d", fs.nf_j, fs.k - 1, fs.k);
+            if (fs.capfail) FAIL(c, SPP_E_MG_CAP, "corner multigrid hit the cycle cap (%d)", c->opt.mg_max_cycles);
+            iters = fs.k; converged = fs.converged; resf = fs.res;
+            mg_tot = fs.mg_tot; mg_min = fs.mg_min; mg_max = fs.mg_max; caps = fs.caps;
+            for (int k = 0; k < iters; ++k) c->launches += c->itg_launches[k];
+            c->launches += (int64_t)mg_tot * c->cg_body_launches;
+            CK(c, cudaMemcpyAsync(H.data(), fg_H(c), sizeof(double) * (size_t)iters * ld, cudaMemcpyDeviceToHost, c->st));
+            CK(c, cudaMemcpyAsync(g.data(), fg_arr(c, 2), sizeof(double) * (iters + 1), cudaMemcpyDeviceToHost, c->st));
+            if (hist && hcap > 1)
+                CK(c, cudaMemcpyAsync(hist + 1, fg_arr(c, 3) + 1, sizeof(double) * std::min(iters, hcap - 1),
+                                      cudaMemcpyDeviceToHost, c->st));
+            CK(c, cudaStreamSynchronize(c->st));
+        } else
         for (int k = 0; k < maxit; ++k) {
             CK(c, ensure_vectors(c, k + 1));
             int cap = 0;
@@ -941,28 +1212,7 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
                 if (cap && c->opt.mg_strict) FAIL(c, SPP_E_MG_CAP, "corner multigrid hit the cycle cap (%d)", c->opt.mg_max_cycles);
                 mg_tot += cyc; mg_min = std::min(mg_min, cyc); mg_max = std::max(mg_max, cyc); caps += cap;
             }
-            // w = W A z_k, with <w, v_0>
-            {
-                ProfScope ps(c, 0, 48.0 * mm);
-                k_spmv<<<red_grid((long)m * m), kRedThreads, 0, c->st>>>(m, c->P, c->Z[k], c->aE, c->aN, c->rr, c->aW, c->aS,
-                                                              weighted, c->w, c->V[0], part_slot(c, 0), 1, m);
-                c->launches++;
-            }
-            // modified Gram-Schmidt: h_{j,k} for j = 0..k, then ||w||
-            for (int j = 1; j <= k; ++j) {
-                ProfScope ps(c, 7, 32.0 * G);
-                k_mgs<<<red_grid(G), kRedThreads, 0, c->st>>>(G, c->w, c->V[j - 1], part_slot(c, j - 1),
-                                                             c->dscal + (j - 1), c->V[j], part_slot(c, j), 1);
-                c->launches++;
-            }
-            {
-                ProfScope ps(c, 7, 24.0 * G + 16.0 * G);
-                k_mgs<<<red_grid(G), kRedThreads, 0, c->st>>>(G, c->w, c->V[k], part_slot(c, k), c->dscal + k,
-                                                             c->w, part_slot(c, k + 1), 1);
-                k_normalize<<<red_grid(G), kRedThreads, 0, c->st>>>(G, c->w, part_slot(c, k + 1), c->dscal + k + 1,
-                                                                   c->V[k + 1], 1);
-                c->launches += 2;
-            }
+            krylov_tail(c, k);
             if (cyc < 0) CK(c, cudaMemcpyAsync(c->hmgs, c->mgs, sizeof(MGState), cudaMemcpyDeviceToHost, c->st));
             CK(c, cudaMemcpyAsync(c->hpin, c->dscal, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, c->st));
             CK(c, cudaStreamSynchronize(c->st));
@@ -972,7 +1222,7 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
                 if (cap && c->opt.mg_strict) FAIL(c, SPP_E_MG_CAP, "corner multigrid hit the cycle cap (%d)", c->opt.mg_max_cycles);
                 mg_tot += cyc; mg_min = std::min(mg_min, cyc); mg_max = std::max(mg_max, cyc); caps += cap;
             }
-            double *h = &H[(size_t)k * (maxit + 1)];
+            double *h = &H[(size_t)k * ld];
             for (int j = 0; j <= k + 1; ++j) {
                 h[j] = c->hpin[j];
                 // SURVEY 5 "NaN/Inf guard on h_{k+1,k}": a non-finite Hessenberg entry is a
@@ -980,28 +1230,14 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
                 if (!std::isfinite(h[j]))
                     FAIL(c, SPP_E_NONFINITE, "Hessenberg entry h(%d,%d) is not finite at iteration %d", j, k, k + 1);
             }
-            // Givens (Saad 2003)
-            for (int i = 0; i < k; ++i) {
-                const double t = cs[i] * h[i] + sn[i] * h[i + 1];
-                h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
-                h[i] = t;
-            }
-            const double den = std::hypot(h[k], h[k + 1]);
-            if (den == 0.0) { cs[k] = 1.0; sn[k] = 0.0; }
-            else { cs[k] = h[k] / den; sn[k] = h[k + 1] / den; }
-            const bool brk = h[k + 1] == 0.0;            // happy breakdown: w in span(V)
-            h[k] = den; h[k + 1] = 0.0;
-            g[k + 1] = -sn[k] * g[k];
-            g[k] = cs[k] * g[k];
-            const double res = std::fabs(g[k + 1]);
+            int brk = 0;
+            const double res = givens_update(h, cs.data(), sn.data(), g.data(), k, &brk);
             iters = k + 1;
             resf = res;
             if (hist && k + 1 < hcap) hist[k + 1] = res;
-            if (brk) { converged = res <= target; break; }
-            if (c->opt.fixed_iters > 0) {
-                if (k + 1 >= c->opt.fixed_iters) { converged = res <= target; break; }
-            } else if (res <= target) { converged = 1; break; }
+            if (fg_stop(k, res, brk, target, c->opt.fixed_iters, maxit, &converged)) break;
         }
+        c->last_iters = iters;
         // y = R^{-1} g;  x = sum_j y_j z_j
         for (int i = iters - 1; i >= 0; --i) {
             double t = g[i];

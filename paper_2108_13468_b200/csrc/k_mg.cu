@@ -95,11 +95,6 @@ constexpr bool EXPF_NOEDGE = false;
 
 struct WaveMaps { CUtensorMap q, a1, a2, cd; };
 
-__device__ __forceinline__ void cp_async8(double *dst, const double *src, bool valid)
-{
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
-}
 
 // chain inflow slots are preset to this NaN (all bits set); the sweep only produces values by
 // fma/select, whose NaNs are canonical (0x7fff...), never this pattern
@@ -732,16 +727,20 @@ void launch_gs(Ctx *c, int l, int mode, const double *b, const double *eold, dou
 }
 
 // ------------------------------------------------------------------------------------------
-// Coarse V-cycle (levels with n <= kCoarseMax): one CTA runs the whole
-// V(1,1) cycle of P:1205-1209 / P:1281-1283 for levels lc..L-1 with every level's b, e and
-// residual in shared memory (zero ghost ring); coefficients come from global memory (L2).
+// Coarse V-cycle (levels with n <= kCoarseMaxN): one CTA runs the
+// whole V(1,1) cycle of P:1205-1209 / P:1281-1283 for levels lc..L-1.  Every level's b, e and
+// coefficients are staged into shared memory once (zero ghost ring), so no step waits on L2.
 //   down: e_l = GS(b_l) from 0; rho = b_l - A_l e_l; b_{l+1} = S^-1 P^T S rho
 //   coarsest: 4 GS sweeps from 0
 //   up:   e_l += P e_{l+1}; e_l = GS(b_l) from e_l
-// GS is the sequential downstream sweep (j desc, i desc; E/N new, W/S old) done in place by
-// anti-diagonals: the nodes of diagonal d = (n-i) + (n-j) need only diagonal d-1 (new E, N) and
-// diagonal d+1 (old W, S), so each diagonal is one parallel step (then __syncthreads).
+// GS is the sequential downstream sweep (j desc, i desc; E/N new, W/S old) done in place as a
+// one-warp wavefront: lane t owns row j = n - t and meets column i = n - (s - t) at step s, so
+// its East neighbour is its own previous step, its North one lane t-1's previous step (through
+// shared memory behind __syncwarp), and West / South are still old.  2n - 1 steps of a few
+// shared-memory loads each; no block barrier inside a sweep.
 // ------------------------------------------------------------------------------------------
+constexpr int kCoarseMaxN = 32;     // one warp: one row per lane
+
 struct CoarseLev {
     int n; int cpitch;
     const double *aE, *aN, *rr, *cd, *aW, *aS, *hb, *kb;
@@ -754,90 +753,96 @@ struct CoarseArgs {
     int rs;                         // R stored as R / D (z-form V-cycle)
     double *out; long opitch;       // result e of level lc (value layout)
 };
+// a level's shared-memory image: offsets into the block's shared array of (n+2)^2 arrays with
+// stride st = n+2 and of 1D arrays of n+2 (offsets, not pointers: the accesses stay LDS/STS and
+// the image copies into registers)
+struct CSm { int b, e, aE, aN, cd, rr, aW, aS, hb, kb, n, st; };
+extern __shared__ double coarse_sm[];
 
-// ring: 4 slots x 4 coefficients x blockDim doubles of shared memory (per-thread prefetch ring)
-__device__ __forceinline__ void cgs_sweep(const CoarseLev &L, const double *b, double *e, int stride, double *ring)
+__device__ __forceinline__ void cgs_sweep(const CSm L)
 {
-    // thread t owns column i = n - t and meets it on diagonals d = t .. t+n-1 at row j = n-(d-t);
-    // its coefficients (column i, rows descending) are staged by cp.async four rows ahead
-    const int n = L.n, t = threadIdx.x, T = blockDim.x;
-    const bool act = t < n;
-    const int i = n - t;
-    const double aw = act ? __ldg(L.aW + i) : 0.0;
-    auto stage = [&](int r) {                          // row j = n - r into slot r & 3
-        const int j = n - r, u = r & 3;
-        const bool ok = act && j >= 1;
-        const int q = ok ? j * L.cpitch + i : 0;
-        double *sl = ring + (size_t)u * 4 * T + t;
-        cp_async8(sl, L.aE + q, ok);
-        cp_async8(sl + T, L.aN + q, ok);
-        cp_async8(sl + 2 * T, L.cd + q, ok);
-        cp_async8(sl + 3 * T, L.aS + (ok ? j : 0), ok);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-#pragma unroll
-    for (int r = 0; r < 4; ++r) stage(r);
-    int r = 0;                                         // rows of this column done
-    for (int d = 0; d <= 2 * (n - 1); ++d) {
-        if (act && d >= t && r < n) {
-            asm volatile("cp.async.wait_group 3;" ::: "memory");
-            const double *sl = ring + (size_t)(r & 3) * 4 * T + t;
-            const int j = n - r, s = j * stride + i;
-            const double v = (((b[s] + aw * e[s - 1]) + sl[3 * T] * e[s - stride]) + sl[0] * e[s + 1]) + sl[T] * e[s + stride];
-            e[s] = v * sl[2 * T];
-            stage(r + 4);                              // slot r&3 refilled with row j-4
-            ++r;
+    double *cs = coarse_sm;
+    if (threadIdx.x < 32) {
+        const int n = L.n, st = L.st, t = threadIdx.x;
+        const bool act = t < n;
+        const int j = n - t;
+        const double as = act ? cs[L.aS + j] : 0.0;
+        const double *b = cs + L.b, *aW = cs + L.aW, *aE = cs + L.aE, *aN = cs + L.aN, *cd = cs + L.cd;
+        double *e = cs + L.e;
+        for (int s = 0; s < 2 * n - 1; ++s) {
+            const int i = n - (s - t);
+            if (act && s >= t && i >= 1) {
+                const int q = j * st + i;
+                const double v = (((b[q] + aW[i] * e[q - 1]) + as * e[q - st]) + aE[q] * e[q + 1]) + aN[q] * e[q + st];
+                e[q] = v * cd[q];
+            }
+            __syncwarp();
         }
-        __syncthreads();
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
 {
-    extern __shared__ double cs[];
-    // layout: per level b_l, e_l of (n_l+2)^2, then one residual scratch of level lc's size
-    double *B[8], *E[8];
-    int st[8];
-    double *p = cs;
+    double *cs = coarse_sm;
+    CSm S[8];
+    int p = 0;
     for (int l = 0; l < a.nlev; ++l) {
-        st[l] = a.lv[l].n + 2;
-        B[l] = p; p += st[l] * st[l];
-        E[l] = p; p += st[l] * st[l];
+        const int n = a.lv[l].n, st = n + 2, A = st * st;
+        S[l] = CSm{p, p + A, p + 2 * A, p + 3 * A, p + 4 * A, p + 5 * A, p + 6 * A, p + 6 * A + st, p + 6 * A + 2 * st,
+                   p + 6 * A + 3 * st, n, st};
+        p += 6 * A + 4 * st;
     }
-    double *rho = p;
-    double *cring = rho + st[0] * st[0];               // cgs_sweep prefetch ring, 16 * blockDim doubles
-    const int tot = (int)(p - cs) + st[0] * st[0];
+    double *rho = cs + p;
+    const int tot = p + S[0].st * S[0].st;
     for (int k = threadIdx.x; k < tot; k += blockDim.x) cs[k] = 0.0;
     __syncthreads();
-    {   // level lc rhs
-        const int n = a.lv[0].n;
-        const CoarseLev &F = a.lv[0];
+    // stage the coefficients and the rhs with asynchronous copies: every load in flight at once
+    auto cp8 = [&](int dst, const double *src) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(cs + dst)), "l"(src)
+                     : "memory");
+    };
+    for (int l = 0; l < a.nlev; ++l) {
+        const CoarseLev &F = a.lv[l];
+        const CSm M = S[l];
+        const int n = F.n;
         for (int k = threadIdx.x; k < n * n; k += blockDim.x) {
-            const int j = k / n + 1, i = k % n + 1;
-            double rv = a.R[(long)j * a.rpitch + i];
-            if (a.rs) {                                 // R / D -> R
-                const int q = j * F.cpitch + i;
-                rv *= ((__ldg(F.aW + i) + __ldg(F.aE + q)) + (__ldg(F.aS + j) + __ldg(F.aN + q))) + __ldg(F.rr + q);
-            }
-            B[0][j * st[0] + i] = rv;
+            const int j = k / n + 1, i = k % n + 1, q = j * F.cpitch + i, s = j * M.st + i;
+            cp8(M.aE + s, F.aE + q); cp8(M.aN + s, F.aN + q); cp8(M.cd + s, F.cd + q); cp8(M.rr + s, F.rr + q);
+            if (l == 0) cp8(M.b + s, a.R + (long)j * a.rpitch + i);
         }
-        __syncthreads();
+        for (int k = threadIdx.x; k < n + 2; k += blockDim.x) {
+            cp8(M.aW + k, F.aW + k); cp8(M.aS + k, F.aS + k); cp8(M.hb + k, F.hb + k); cp8(M.kb + k, F.kb + k);
+        }
     }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    if (a.rs) {                                        // level lc rhs stored as R / D -> R
+        const CSm M = S[0];
+        const int n = M.n;
+        for (int k = threadIdx.x; k < n * n; k += blockDim.x) {
+            const int j = k / n + 1, i = k % n + 1, s = j * M.st + i;
+            cs[M.b + s] *= ((cs[M.aW + i] + cs[M.aE + s]) + (cs[M.aS + j] + cs[M.aN + s])) + cs[M.rr + s];
+        }
+    }
+    __syncthreads();
     const int last = a.nlev - 1;
     // ---- down ----
     for (int l = 0; l < last; ++l) {
-        const CoarseLev &F = a.lv[l], &C = a.lv[l + 1];
-        const int n = F.n, sf = st[l], sc = st[l + 1];
-        cgs_sweep(F, B[l], E[l], sf, cring);                           // pre-smoothing from zero
-        for (int k = threadIdx.x; k < n * n; k += blockDim.x) {        // S-scaled residual
-            const int j = k / n + 1, i = k % n + 1;
-            const int s = j * sf + i, q = j * F.cpitch + i;
-            const double ec = E[l][s];
-            const double Ae = __ldg(F.aW + i) * (ec - E[l][s - 1]) + __ldg(F.aE + q) * (ec - E[l][s + 1]) +
-                              __ldg(F.aS + j) * (ec - E[l][s - sf]) + __ldg(F.aN + q) * (ec - E[l][s + sf]) +
-                              __ldg(F.rr + q) * ec;
-            rho[s] = (__ldg(F.hb + i) * __ldg(F.kb + j)) * (B[l][s] - Ae);
+        const CSm F = S[l], C = S[l + 1];
+        const Wts &W = a.lv[l].w;
+        const int n = F.n, sf = F.st, sc = C.st;
+        cgs_sweep(F);                                                  // pre-smoothing from zero
+        {
+            const double *e = cs + F.e, *b = cs + F.b;
+            for (int k = threadIdx.x; k < n * n; k += blockDim.x) {    // S-scaled residual
+                const int j = k / n + 1, i = k % n + 1;
+                const int s = j * sf + i;
+                const double ec = e[s];
+                const double Ae = cs[F.aW + i] * (ec - e[s - 1]) + cs[F.aE + s] * (ec - e[s + 1]) +
+                                  cs[F.aS + j] * (ec - e[s - sf]) + cs[F.aN + s] * (ec - e[s + sf]) + cs[F.rr + s] * ec;
+                rho[s] = (cs[F.hb + i] * cs[F.kb + j]) * (b[s] - Ae);
+            }
         }
         __syncthreads();
         const int nc = C.n;
@@ -850,33 +855,36 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
                 if (j < 1 || j > n) continue;
                 const double *r = rho + j * sf + 2 * I;
                 double rs = r[0];
-                const bool u = F.w.uni;
-                if (2 * I - 1 >= 1) rs = (u ? 0.5 : __ldg(F.w.xr + 2 * I - 1)) * r[-1] + rs;   // P^T: I is 2I-1's right parent
-                if (2 * I + 1 <= n) rs = rs + (u ? 0.5 : __ldg(F.w.xl + 2 * I + 1)) * r[1];    //      and 2I+1's left parent
-                acc += (bb == 0 ? 1.0 : (u ? 0.5 : (bb < 0 ? __ldg(F.w.yr + j) : __ldg(F.w.yl + j)))) * rs;
+                const bool u = W.uni;
+                if (2 * I - 1 >= 1) rs = (u ? 0.5 : __ldg(W.xr + 2 * I - 1)) * r[-1] + rs;   // P^T: I is 2I-1's right parent
+                if (2 * I + 1 <= n) rs = rs + (u ? 0.5 : __ldg(W.xl + 2 * I + 1)) * r[1];    //      and 2I+1's left parent
+                acc += (bb == 0 ? 1.0 : (u ? 0.5 : (bb < 0 ? __ldg(W.yr + j) : __ldg(W.yl + j)))) * rs;
             }
-            B[l + 1][J * sc + I] = acc / (__ldg(C.hb + I) * __ldg(C.kb + J));
+            cs[C.b + J * sc + I] = acc / (cs[C.hb + I] * cs[C.kb + J]);
         }
         __syncthreads();
     }
     // ---- coarsest: four sweeps from zero ----
-    for (int s4 = 0; s4 < 4; ++s4) cgs_sweep(a.lv[last], B[last], E[last], st[last], cring);
+    for (int s4 = 0; s4 < 4; ++s4) cgs_sweep(S[last]);
     // ---- up ----
     for (int l = last - 1; l >= 0; --l) {
-        const int n = a.lv[l].n, sf = st[l], sc = st[l + 1];
-        const double *ec = E[l + 1];
+        const CSm F = S[l];
+        const int n = F.n, sf = F.st, sc = S[l + 1].st;
+        const double *ec = cs + S[l + 1].e;
+        double *e = cs + F.e;
+        const Wts &W = a.lv[l].w;
         for (int k = threadIdx.x; k < n * n; k += blockDim.x) {        // e += P e_c
             const int j = k / n + 1, i = k % n + 1;
-            E[l][j * sf + i] += a.lv[l].w.uni ? interp_w<true>(ec, sc, i, j, a.lv[l].w) : interp_w<false>(ec, sc, i, j, a.lv[l].w);
+            e[j * sf + i] += W.uni ? interp_w<true>(ec, sc, i, j, W) : interp_w<false>(ec, sc, i, j, W);
         }
         __syncthreads();
-        cgs_sweep(a.lv[l], B[l], E[l], sf, cring);                     // post-smoothing
+        cgs_sweep(F);                                                  // post-smoothing
     }
     {   // result of level lc
-        const int n = a.lv[0].n;
+        const int n = S[0].n;
         for (int k = threadIdx.x; k < n * n; k += blockDim.x) {
             const int j = k / n + 1, i = k % n + 1;
-            a.out[(long)j * a.opitch + i] = E[0][j * st[0] + i];
+            a.out[(long)j * a.opitch + i] = cs[S[0].e + j * S[0].st + i];
         }
     }
 }
@@ -884,8 +892,11 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
 static size_t coarse_smem(const Ctx *c, int lc)
 {
     size_t tot = 0;
-    for (int l = lc; l < c->L; ++l) tot += 2 * (size_t)(c->lev[l].n + 2) * (c->lev[l].n + 2);
-    tot += (size_t)(c->lev[lc].n + 2) * (c->lev[lc].n + 2) + 16 * 256;
+    for (int l = lc; l < c->L; ++l) {
+        const size_t st = (size_t)c->lev[l].n + 2;
+        tot += 6 * st * st + 4 * st;
+    }
+    tot += (size_t)(c->lev[lc].n + 2) * (c->lev[lc].n + 2);
     return tot * sizeof(double);
 }
 
@@ -893,7 +904,7 @@ static size_t coarse_smem(const Ctx *c, int lc)
 // do not fit (the caller then recurses level by level).
 bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs)
 {
-    if (c->L - lc > 8 || c->lev[lc].n > c->tune.coarse_max) return false;
+    if (c->L - lc > 8 || c->lev[lc].n > std::min(c->tune.coarse_max, kCoarseMaxN)) return false;
     const size_t sm = coarse_smem(c, lc);
     if (sm > 200 * 1024) return false;
     CoarseArgs a{};
@@ -907,9 +918,7 @@ bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs)
     double nn = 0;
     for (int l = lc; l < c->L; ++l) nn += (double)c->lev[l].n * c->lev[l].n;
     ProfScope ps(c, 10, nn * 96.0);   // b read; aE, aN, 1/D, r read by two sweeps + residual; e written
-    const int threads = std::max(256, (c->lev[lc].n + 31) / 32 * 32);   // >= n: one column per thread in the sweeps
-    if (threads > 256) return false;
-    k_coarse_vcycle<<<1, threads, sm, c->st>>>(a);
+    k_coarse_vcycle<<<1, 256, sm, c->st>>>(a);
     c->launches++;
     return true;
 }

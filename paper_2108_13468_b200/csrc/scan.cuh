@@ -2,7 +2,8 @@
 // tridiagonal line solves: forward  y_k = al_k y_{k-1} + b_k  (y_{-1} = 0) and backward
 // z_k = be_k z_{k+1} + y_k  (z_len = 0).  Each thread owns K consecutive elements; the
 // recurrence is composed as affine maps through a warp shuffle scan and one shared-memory
-// level (sA[32], sB[64]).  All threads of the block must call these.
+// level (sA[32], sB[64]; skipped for a one-warp block, whose results are bitwise the same).
+// All threads of the block must call these.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -23,6 +24,14 @@ __device__ __forceinline__ void fwd_scan(double (&al)[K], double (&b)[K], double
     for (int d = 1; d < 32; d <<= 1) {
         const double Au = __shfl_up_sync(0xffffffffu, A, d), Bu = __shfl_up_sync(0xffffffffu, B, d);
         if (lane >= d) { B = A * Bu + B; A = A * Au; }
+    }
+    if (nw == 1) {                                     // one warp (short lines): no block level
+        const double Be = __shfl_up_sync(0xffffffffu, B, 1);
+        double yin = lane == 0 ? 0.0 : Be;
+#pragma unroll
+        for (int k = 0; k < K; ++k) { yin = al[k] * yin + b[k]; y[k] = yin; }
+        __syncwarp();                                  // the caller's shared-memory ordering, as the barrier
+        return;
     }
     if (lane == 31) { sA[w] = A; sB[w] = B; }
     __syncthreads();
@@ -58,6 +67,14 @@ __device__ __forceinline__ void bwd_scan(double (&be)[K], double (&y)[K], double
     for (int d = 1; d < 32; d <<= 1) {
         const double Ad = __shfl_down_sync(0xffffffffu, A, d), Bd = __shfl_down_sync(0xffffffffu, B, d);
         if (lane + d < 32) { B = A * Bd + B; A = A * Ad; }
+    }
+    if (nw == 1) {
+        const double Bd = __shfl_down_sync(0xffffffffu, B, 1);
+        double zin = lane == 31 ? 0.0 : Bd;
+#pragma unroll
+        for (int k = K - 1; k >= 0; --k) { zin = be[k] * zin + y[k]; z[k] = zin; }
+        __syncwarp();
+        return;
     }
     if (lane == 0) { sA[w] = A; sB[w] = B; }
     __syncthreads();

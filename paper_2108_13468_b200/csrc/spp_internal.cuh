@@ -138,6 +138,18 @@ struct MGState {
     int cycles, cap;        // cycles run, cycle cap hit
 };
 
+// device-resident FGMRES state of the iteration graphs (capi.cu "iteration graphs"): the
+// Givens/Hessenberg bookkeeping and the stop test run on the device, so a batch of iterations
+// needs no host round trip
+struct FGHead {
+    int k;                  // iterations done
+    int stop;               // the loop has ended (the gates of later graphs skip their iteration)
+    int converged, nonfinite, nf_j, capfail;
+    int mg_tot, mg_min, mg_max, caps;
+    double res;             // |g_k|
+    double target;          // the stop test's threshold (tol, or tol * beta in the relative modes)
+};
+
 struct Ctx {
     int dim = 0, N = 0, n = 0, m = 0;    // N intervals, n = N/2, m = N-1
     double eps = 0;
@@ -208,6 +220,15 @@ struct Ctx {
     int64_t cg_body_launches = 0;          // kernels per loop iteration
     bool capturing = false;
     int use_graph = 1;
+    // iteration graphs: graph k = [gate] -> IF { FGMRES iteration k (the corner loop a nested
+    // while node) }, built on first use and kept while the plan (fg_signature) is unchanged
+    FGHead *fgh = nullptr, *hfgh = nullptr;   // device state / pinned host copy
+    double *fgd = nullptr;                 // device H [(maxit+1)^2], cs, sn, g, hist [maxit+2 each]
+    std::vector<cudaGraphExec_t> itg;
+    std::vector<int64_t> itg_launches;     // kernels of iteration k's body (the corner cycles apart)
+    std::vector<long> itg_sig;
+    int fg_ok = 1;                         // 0: graphs unavailable on this device -> host loop
+    int last_iters = 0;                    // the previous solve's iterations (first batch size)
     int no_lines_tma = 0;                  // SPP_NO_LINES_TMA=1: LSU-loaded line kernel
     int mg_zform = 1;                      // corner GS sweeps in z-form (SPP_MG_YFORM=1: y-form)
     // parabolic-layer variant (c2 = 0 everywhere; NEXT-2): semi-coarsening Galerkin corner MG

@@ -375,6 +375,60 @@ def test_corner_graph_matches_host_loop(name, N, eps, opt):
         assert r_graph.stats["mg_cap_hits"] == r_graph.stats["iters"] > 0
 
 
+@pytest.mark.parametrize("name,N,eps,opt", [("cfg2", 128, None, {}), ("cfg4", 256, 1e-8, {"fixed_iters": 3}),
+                                           ("cfg5", 256, 1e-4, {"max_iters": 5, "tol": 1e-15}),
+                                           ("cfg4", 256, 1e-8, {"mg_fixed_cycles": 2})])
+def test_iteration_graphs_match_host_loop(name, N, eps, opt):
+    """FGMRES iterations as CUDA graphs (capi.cu "iteration graphs": the Givens update and stop
+    test on the device, the corner loop a nested while node, batches of speculative iterations
+    behind a device-side gate) against the host-driven loop: the same statistics, residual
+    history and iterate, bit for bit; repeated solves on one context (batch sizes from the previous
+    solve, graphs reused) too."""
+    cfg = si.config(name, N=N, eps=eps)
+    x = spp.spp_shishkin_mesh(N, cfg.eps, cfg.sigma, cfg.beta_x)
+    y = spp.spp_shishkin_mesh(N, cfg.eps, cfg.sigma, cfg.beta_y)
+    c1, c2, r, f = si.sample_2d(cfg, x, y)
+
+    def run():
+        o = spp.spp_default_options(2)
+        o.tol = cfg.tol
+        for k, v in opt.items():
+            setattr(o, k, v)
+        S = spp.Solver(2, N, cfg.eps, x, y, dev(c1), dev(c2), dev(r), options=o)
+        out = []
+        for k in range(3):                      # the same rhs, a scaled one, a perturbed one
+            fk = f * (1.0 + k) + (k == 2) * si.random_field(500, f.shape)
+            res = S.solve(dev(fk))
+            out.append((res.status, dict(res.stats), np.array(res.hist), host(res.u)))
+        S.close()
+        return out
+
+    g = run()
+    h = _with_env("SPP_NO_GRAPH", run)
+    for (sg, stg, hg, ug), (sh, sth, hh, uh) in zip(g, h):
+        assert sg == sh
+        for k in ("iters", "converged", "mg_cycles_total", "mg_cycles_min", "mg_cycles_max", "mg_cap_hits",
+                  "res_final"):
+            assert stg[k] == sth[k], (k, stg[k], sth[k])
+        assert np.array_equal(hg, hh)
+        assert np.array_equal(ug, uh)
+    if "max_iters" in opt:
+        assert g[0][1]["iters"] == opt["max_iters"] and not g[0][1]["converged"]
+
+
+def test_iteration_graphs_cap_failure():
+    """mg_strict: a corner cycle-cap hit inside the graphs fails the solve with SPP_E_MG_CAP."""
+    cfg = si.config("cfg4", N=256, eps=1e-8)
+    x = spp.spp_shishkin_mesh(256, cfg.eps)
+    c1, c2, r, f = si.sample_2d(cfg, x, x)
+    o = spp.spp_default_options(2)
+    o.mg_max_cycles, o.mg_strict = 1, 1
+    S = spp.Solver(2, 256, cfg.eps, x, x, dev(c1), dev(c2), dev(r), options=o)
+    with pytest.raises(spp.SppError) as ei:
+        S.solve(dev(f))
+    assert ei.value.code == -5                  # SPP_E_MG_CAP
+
+
 @pytest.mark.parametrize("name,N,eps", [("cfg3", 1024, None), ("cfg4", 512, 1e-8)])
 def test_tma_line_kernel_matches_lsu_kernel(name, N, eps):
     """The TMA-staged line-chain kernel (k_lines_tma, line length a multiple of 128) computes the
