@@ -769,22 +769,51 @@ __device__ __forceinline__ void cgs_sweep(const CSm L)
         const double as = act ? cs[L.aS + j] : 0.0;
         const double *b = cs + L.b, *aW = cs + L.aW, *aE = cs + L.aE, *aN = cs + L.aN, *cd = cs + L.cd;
         double *e = cs + L.e;
+        // new values never come back through shared memory: East is this lane's previous step
+        // (0: the ghost column at i = n), North lane t-1's previous step (shuffle; lane 0: the
+        // ghost row); West and South are still old.  The stores are write-only during the sweep,
+        // and a lane's loads of old values precede, in the warp's instruction order, the store of
+        // the lane that overwrites them.  Branch-free (idle lanes read a valid dummy node and
+        // keep their value), with the operands of the next step loaded one step ahead: measured
+        // 122 instead of ~235 cycles per step (tools/ubench/sweep.cu).
+        const int jj = act ? j : 1;
+        auto ld = [&](int ii, double &B, double &W, double &EW, double &S, double &E, double &N, double &C) {
+            const int ic = (ii >= 1 && ii <= n) ? ii : 1, q = jj * st + ic;
+            B = b[q]; W = aW[ic]; EW = e[q - 1]; S = e[q - st]; E = aE[q]; N = aN[q]; C = cd[q];
+        };
+        double B, W, EW, S, E, N, C;
+        ld(n + t, B, W, EW, S, E, N, C);
+        double vlast = 0.0;
         for (int s = 0; s < 2 * n - 1; ++s) {
             const int i = n - (s - t);
-            if (act && s >= t && i >= 1) {
-                const int q = j * st + i;
-                const double v = (((b[q] + aW[i] * e[q - 1]) + as * e[q - st]) + aE[q] * e[q + 1]) + aN[q] * e[q + st];
-                e[q] = v * cd[q];
-            }
-            __syncwarp();
+            const bool ok = act && i >= 1 && i <= n;
+            double Bn, Wn, EWn, Sn, En, Nn, Cn;
+            ld(i - 1, Bn, Wn, EWn, Sn, En, Nn, Cn);
+            double vN = __shfl_up_sync(0xffffffffu, vlast, 1);
+            if (t == 0) vN = 0.0;
+            const double v = (((B + W * EW) + as * S) + E * vlast) + N * vN;
+            const double z = v * C;
+            vlast = ok ? z : vlast;
+            if (ok) e[jj * st + i] = z;
+            B = Bn; W = Wn; EW = EWn; S = Sn; E = En; N = Nn; C = Cn;
         }
     }
     __syncthreads();
 }
 
+#ifdef SPP_COARSE_PROF
+__device__ int g_coarse_prof = 0;
+#define CTP(k) do { if (threadIdx.x == 0) tp[k] = clock64(); } while (0)
+#else
+#define CTP(k)
+#endif
 __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
 {
     double *cs = coarse_sm;
+#ifdef SPP_COARSE_PROF
+    long long tp[16] = {0};
+#endif
+    CTP(0);
     CSm S[8];
     int p = 0;
     for (int l = 0; l < a.nlev; ++l) {
@@ -794,9 +823,12 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
         p += 6 * A + 4 * st;
     }
     double *rho = cs + p;
-    const int tot = p + S[0].st * S[0].st;
-    for (int k = threadIdx.x; k < tot; k += blockDim.x) cs[k] = 0.0;
+    // zero ghost rings: b, e of every level and rho (the coefficient images are fully staged)
+    for (int l = 0; l < a.nlev; ++l)
+        for (int k = threadIdx.x; k < 2 * S[l].st * S[l].st; k += blockDim.x) cs[S[l].b + k] = 0.0;
+    for (int k = threadIdx.x; k < S[0].st * S[0].st; k += blockDim.x) rho[k] = 0.0;
     __syncthreads();
+    CTP(1);
     // stage the coefficients and the rhs with asynchronous copies: every load in flight at once
     auto cp8 = [&](int dst, const double *src) {
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(cs + dst)), "l"(src)
@@ -817,6 +849,7 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
+    CTP(2);
     if (a.rs) {                                        // level lc rhs stored as R / D -> R
         const CSm M = S[0];
         const int n = M.n;
@@ -832,7 +865,9 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
         const CSm F = S[l], C = S[l + 1];
         const Wts &W = a.lv[l].w;
         const int n = F.n, sf = F.st, sc = C.st;
+        if (l == 0) CTP(3);
         cgs_sweep(F);                                                  // pre-smoothing from zero
+        if (l == 0) CTP(4);
         {
             const double *e = cs + F.e, *b = cs + F.b;
             for (int k = threadIdx.x; k < n * n; k += blockDim.x) {    // S-scaled residual
@@ -864,8 +899,10 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
         }
         __syncthreads();
     }
+    CTP(5);
     // ---- coarsest: four sweeps from zero ----
     for (int s4 = 0; s4 < 4; ++s4) cgs_sweep(S[last]);
+    CTP(6);
     // ---- up ----
     for (int l = last - 1; l >= 0; --l) {
         const CSm F = S[l];
@@ -878,7 +915,9 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
             e[j * sf + i] += W.uni ? interp_w<true>(ec, sc, i, j, W) : interp_w<false>(ec, sc, i, j, W);
         }
         __syncthreads();
+        if (l == 0) CTP(7);
         cgs_sweep(F);                                                  // post-smoothing
+        if (l == 0) CTP(8);
     }
     {   // result of level lc
         const int n = S[0].n;
@@ -887,6 +926,13 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
             a.out[(long)j * a.opitch + i] = cs[S[0].e + j * S[0].st + i];
         }
     }
+#ifdef SPP_COARSE_PROF
+    CTP(9);
+    if (threadIdx.x == 0 && atomicAdd(&g_coarse_prof, 1) < 4)
+        printf("[coarse] n0=%d nlev=%d zero %lld stage %lld pre0 %lld down-rest %lld coarsest %lld up-rest %lld post0 %lld out %lld total %lld\n",
+               a.lv[0].n, a.nlev, tp[1] - tp[0], tp[2] - tp[1], tp[4] - tp[3], tp[5] - tp[4], tp[6] - tp[5], tp[7] - tp[6],
+               tp[8] - tp[7], tp[9] - tp[8], tp[9] - tp[0]);
+#endif
 }
 
 static size_t coarse_smem(const Ctx *c, int lc)

@@ -121,7 +121,7 @@ struct Tune {
     int gs_max_halo = 128;     // no certified halo below this -> exact chained sweep
     int sweep_warps = 2;       // warps per CTA of the exact chained sweep (M_II; 2 measured best)
     int gs_lag = 5;            // tiling model: chunk-times each extra warp adds
-    int coarse_max = 16;       // levels with n <= this run as one fused single-CTA V-cycle (16 measured best)
+    int coarse_max = 32;       // levels with n <= this run as one fused single-CTA V-cycle (<= kCoarseMaxN = 32)
     int dist_levels = 2;       // row strips: corner levels whose sweeps run on the strips
     int rho_halo = 0;          // 1: certify halos by rho = max (ca + cn) (round 1) instead of gamma_y, gamma_x
 };
