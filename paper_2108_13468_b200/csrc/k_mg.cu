@@ -123,6 +123,18 @@ __device__ __forceinline__ void st_relaxed2(double *p, double v0, double v1)
                  "l"(__double_as_longlong(v1)));
 }
 
+// predicated forms (the predicate inside the asm: no branch around it)
+__device__ __forceinline__ void st_relaxed_if(bool pr, double *p, double v)
+{
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.relaxed.gpu.global.b64 [%0], %1; }" ::"l"(p),
+                 "l"(__double_as_longlong(v)), "r"((unsigned)pr));
+}
+__device__ __forceinline__ void st_relaxed2_if(bool pr, double *p, double v0, double v1)
+{
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %3, 0; @q st.relaxed.gpu.global.v2.b64 [%0], {%1, %2}; }" ::"l"(p),
+                 "l"(__double_as_longlong(v0)), "l"(__double_as_longlong(v1)), "r"((unsigned)pr));
+}
+
 template <bool YFORM, bool CHAIN>
 __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const __grid_constant__ WaveMaps m)
 {
@@ -359,10 +371,14 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
                 if (lane == 0) { n0 = E[st].x; n1 = E[st].y; }
                 double za = fma(A1.y, z1, fma(A2.y, n0, Q.y));      // column 2st   (east one first)
                 double zc = fma(A1.x, za, fma(A2.x, n1, Q.x));      // column 2st+1
-                if (!F) {
+                if (!F) {                                  // edge chunk: zero outside the block
+                    // one AND per value on the chain (the masks do not depend on it); a ternary
+                    // compiled to three dependent selects
                     const int idx = c * WCW + 2 * st - WLAG * lane;
-                    za = (rvalid && idx >= 0 && idx < ncols) ? za : 0.0;
-                    zc = (rvalid && idx + 1 >= 0 && idx + 1 < ncols) ? zc : 0.0;
+                    const unsigned ua = (unsigned)idx < (unsigned)ncols, uc = (unsigned)(idx + 1) < (unsigned)ncols;
+                    const long long ma = -(long long)(rvalid & ua), mc = -(long long)(rvalid & uc);
+                    za = __longlong_as_double(__double_as_longlong(za) & ma);
+                    zc = __longlong_as_double(__double_as_longlong(zc) & mc);
                 }
                 Z[2 * st] = za; Z[2 * st + 1] = zc;
                 z2 = za; z1 = zc;
@@ -385,16 +401,22 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
                     if (e31) *reinterpret_cast<double2 *>(eo + (idx & (WEB - 1))) = make_double2(Z[2 * st], Z[2 * st + 1]);
                     if (c31) st_relaxed2(co + idx, Z[2 * st], Z[2 * st + 1]);
                 }
-            } else if (lane == 31 && !EXPF_NOEDGE) {
+            } else {
+                // edge chunk: the same stores, predicated (the conditions are warp-uniform but for
+                // lane == 31; a lane-31-only branch around them had the warp reconverge per chunk)
+                const bool e31 = lane == 31 && has_consumer && !EXPF_NOEDGE;
+                const bool c31 = CHAIN && lane == 31 && chain_out && !EXPF_NOEDGE;
 #pragma unroll
                 for (int st = 0; st < 8; ++st) {
                     const int idx = c * WCW + 2 * st - WLAG * 31;
-                    if (idx >= 0 && idx + 1 < ncols) {
-                        if (has_consumer) *reinterpret_cast<double2 *>(eo + (idx & (WEB - 1))) = make_double2(Z[2 * st], Z[2 * st + 1]);
-                        if (CHAIN && chain_out) st_relaxed2(co + idx, Z[2 * st], Z[2 * st + 1]);
-                    } else if (idx >= 0 && idx < ncols) {   // last odd column
-                        if (has_consumer) eo[idx & (WEB - 1)] = Z[2 * st];
-                        if (CHAIN && chain_out) st_relaxed(co + idx, Z[2 * st]);
+                    const bool two = idx >= 0 && idx + 1 < ncols, one = idx >= 0 && idx + 1 == ncols;   // last odd column
+                    const int io = two || one ? idx : 0;
+                    double *ep = eo + (io & (WEB - 1));
+                    if (e31 && two) *reinterpret_cast<double2 *>(ep) = make_double2(Z[2 * st], Z[2 * st + 1]);
+                    if (e31 && one) *ep = Z[2 * st];
+                    if (CHAIN) {
+                        st_relaxed2_if(c31 && two, co + io, Z[2 * st], Z[2 * st + 1]);
+                        st_relaxed_if(c31 && one, co + io, Z[2 * st]);
                     }
                 }
             }
