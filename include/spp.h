@@ -185,14 +185,18 @@ SPP_API spp_status spp_solve(spp_ctx *c, const double *f, double *u_out, spp_mem
  *              of A_l x = b from x0 = e + P e_c (the fused prolongation + right-hand-side kernel
  *              and the sweep of the V-cycle's post-smoothing, with b stored as b/D as there)
  *   RESID_RESTRICT level l: in = [R | e] stacked; out (level l+1) = S^{-1} P^T S (R - A_l e) / D_{l+1},
- *              the fused residual-restriction kernel with the V-cycle's z-form scalings (R read
- *              as R/D, the coarse right-hand side stored divided by its diagonal) */
+ *              the general residual-restriction kernel with the V-cycle's z-form scalings (R read
+ *              as R/D, the coarse right-hand side stored divided by its diagonal)
+ *   PRE_RESTRICT level l: in = R; out (level l+1) = S^{-1} P^T S (R - A_l e) / D_{l+1} with e = one
+ *              downstream GS sweep of A_l e = R from zero: the V-cycle's pre-smoothing followed by
+ *              its residual-restriction, which forms R - A_l e as aW e_W + aS e_S (P:1205-1209,
+ *              P:1276-1280) */
 typedef enum {
     SPP_STAGE_MATVEC = 0, SPP_STAGE_MII = 1, SPP_STAGE_MYY = 2, SPP_STAGE_MXX = 3,
     SPP_STAGE_CORNER_RHS = 4, SPP_STAGE_GS_SWEEP = 5, SPP_STAGE_VCYCLE = 6,
     SPP_STAGE_CORNER_SOLVE = 7, SPP_STAGE_PRECOND = 8, SPP_STAGE_RESTRICT = 9,
     SPP_STAGE_PROLONG_ADD = 10, SPP_STAGE_LEVEL_RESIDUAL = 11, SPP_STAGE_MII_JACOBI = 12,
-    SPP_STAGE_POST_SMOOTH = 13, SPP_STAGE_RESID_RESTRICT = 14
+    SPP_STAGE_POST_SMOOTH = 13, SPP_STAGE_RESID_RESTRICT = 14, SPP_STAGE_PRE_RESTRICT = 15
 } spp_stage;
 SPP_API spp_status spp_apply_stage(spp_ctx *c, spp_stage s, int32_t level, const double *in, double *out,
                            int32_t *cycles_out);

@@ -22,7 +22,7 @@ SPP_STOP_REL_JACOBI, SPP_STOP_REL_L2, SPP_STOP_ABS_L2, SPP_STOP_ABS_MAX = 0, 1, 
 SPP_RIGHT_FLEXIBLE, SPP_LEFT = 0, 1
 STAGES = dict(MATVEC=0, MII=1, MYY=2, MXX=3, CORNER_RHS=4, GS_SWEEP=5, VCYCLE=6, CORNER_SOLVE=7,
               PRECOND=8, RESTRICT=9, PROLONG_ADD=10, LEVEL_RESIDUAL=11, MII_JACOBI=12, POST_SMOOTH=13,
-              RESID_RESTRICT=14)
+              RESID_RESTRICT=14, PRE_RESTRICT=15)
 PROF_CLASSES = 12
 
 

@@ -126,7 +126,8 @@ double *vcycle(Ctx *c, int l, const double *R, bool rs)
     }
     Level &C = c->lev[l + 1];
     launch_gs(c, l, 0, R, nullptr, ea, nullptr, rs);          // pre-smoothing from zero
-    launch_resid_restrict(c, l, R, ea, zf && rs, zf);         // C.b = S^-1 P^T S (R - A_l ea) (/ D_c in z-form)
+    launch_resid_restrict(c, l, nullptr, ea, false, zf);      // C.b = S^-1 P^T S (R - A_l ea) (/ D_c in z-form),
+                                                              // R - A_l ea = aW ea_W + aS ea_S (ea: sweep from 0)
     const double *ec = vcycle(c, l + 1, C.b, zf);
     launch_gs(c, l, 1, R, ea, eb, ec, rs);                    // post-smoothing from ea + P ec
     return eb;
@@ -1470,6 +1471,19 @@ spp_status spp_apply_stage(spp_ctx *cx, spp_stage s, int32_t l, const double *in
             k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in + nn, e);
             launch_scale_cd(c, l, Rq, Rq);
             launch_resid_restrict(c, l, Rq, e, true, true);
+            k_unpack_level<<<nblk((long)C.n * C.n), 256, 0, c->st>>>(C.n, C.pitch, C.b, out);
+        } else if (s == SPP_STAGE_PRE_RESTRICT) {
+            // the V-cycle's pre-smoothing from zero + residual-restriction (z-form, as in vcycle)
+            if (l + 1 >= c->L) FAIL(c, SPP_E_ARG, "no coarser level");
+            if (!c->mg_zform) FAIL(c, SPP_E_STATE, "PRE_RESTRICT drives the z-form path");
+            Level &C = c->lev[l + 1];
+            double *Rq = c->T1;
+            CK(c, cudaMemsetAsync(Rq, 0, sizeof(double) * Lv.elems, c->st));
+            CK(c, cudaMemsetAsync(e, 0, sizeof(double) * Lv.elems, c->st));
+            k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in, Rq);
+            launch_scale_cd(c, l, Rq, Rq);
+            launch_gs(c, l, 0, Rq, nullptr, e, nullptr, true);
+            launch_resid_restrict(c, l, nullptr, e, false, true);
             k_unpack_level<<<nblk((long)C.n * C.n), 256, 0, c->st>>>(C.n, C.pitch, C.b, out);
         } else if (s == SPP_STAGE_LEVEL_RESIDUAL) {
             k_pack_level<<<nblk(nn), 256, 0, c->st>>>(nl, Lv.pitch, in, b);

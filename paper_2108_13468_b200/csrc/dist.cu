@@ -548,7 +548,7 @@ static spp_status vcycle_dist(Dist *d, int l, bool rs)
     for (int r = 0; r < P; ++r)                        // residual + restriction onto the strip's coarse rows
         if (Ctx *c = d->ctx_of(r)) {
             Level &L = c->lev[l];
-            launch_resid_restrict(c, l, l == 0 ? L.rho : L.b, L.e, zf && rs, zf);
+            launch_resid_restrict(c, l, nullptr, L.e, false, zf);   // L.e: the sweep from zero above
         }
     DTRY(vcycle_dist(d, l + 1, zf));
     if (l + 1 < g.D) {

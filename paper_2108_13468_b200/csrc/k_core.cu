@@ -46,8 +46,8 @@ __global__ void __launch_bounds__(256, 6) k_coef_2d(int N, long P, double eps, c
 {
     const int m = N - 1;
     const long tot = (long)m * m;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / m) + 1, i = (int)(p % m) + 1;
+    for (GridWalk gw(tot, m, 1); gw.ok(); gw.next()) {
+        const long p = gw.p; const int j = gw.j, i = gw.i;
         const double a = c1[p], b = c2[p], rv = r[p];
         // bit 0: invalid (c1 > 0, c2 >= 0, r >= 0, finite: P:208-212); bit 1: some c2 > 0;
         // bit 2: some c2 = 0 (c2 = 0 everywhere is the parabolic-layer variant)
@@ -76,8 +76,8 @@ __global__ void k_coef_level(int N, int nl, int step, long Pl, double eps, const
 {
     const int m = N - 1;
     const long tot = (long)nl * nl;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int lq = (int)(p / nl) + 1, q = (int)(p % nl) + 1;
+    for (GridWalk gw(tot, nl, 1); gw.ok(); gw.next()) {
+        const int lq = gw.j, q = gw.i;
         const double h = lwx[q], h1 = lwx[q + 1], hbar = 0.5 * (h + h1);
         const double k = lwy[lq], k1 = lwy[lq + 1], kbar = 0.5 * (k + k1);
         const double aw = eps / (hbar * h), as = eps / (kbar * k);
@@ -112,16 +112,16 @@ __global__ void k_level0_1d(int N, const double *wx, const double *wy, const dou
 __global__ void k_pack(int m, long P, const double *src, double *dst, int j0, int nrows)   // compact -> padded
 {
     const long tot = (long)m * nrows;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / m) + j0, i = (int)(p % m) + 1;
+    for (GridWalk gw(tot, m, j0); gw.ok(); gw.next()) {
+        const long p = gw.p; const int j = gw.j, i = gw.i;
         dst[(long)j * P + i] = src[p];
     }
 }
 __global__ void k_unpack(int m, long P, const double *src, double *dst, int j0, int nrows)  // padded -> compact
 {
     const long tot = (long)m * nrows;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / m) + j0, i = (int)(p % m) + 1;
+    for (GridWalk gw(tot, m, j0); gw.ok(); gw.next()) {
+        const long p = gw.p; const int j = gw.j, i = gw.i;
         dst[p] = src[(long)j * P + i];
     }
 }
@@ -220,8 +220,8 @@ __global__ void __launch_bounds__(kRedThreads) k_resid_stats(int m, long P, cons
     __shared__ double sm[32];
     double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
     const long tot = (long)m * nrows;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / m) + j0, i = (int)(p % m) + 1;
+    for (GridWalk gw(tot, m, j0); gw.ok(); gw.next()) {
+        const int j = gw.j, i = gw.i;
         const long g = (long)j * P + i;
         const double D = ((aW[i] + aE[g]) + (aS[j] + aN[g])) + rr[g];
         const double r = f[g] - Au[g];
@@ -244,8 +244,8 @@ __global__ void __launch_bounds__(kRedThreads) k_rhs(int m, long P, const double
     __shared__ double sm[32];
     double acc = 0.0;
     const long tot = (long)m * nrows;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / m) + j0, i = (int)(p % m) + 1;
+    for (GridWalk gw(tot, m, j0); gw.ok(); gw.next()) {
+        const int j = gw.j, i = gw.i;
         const long g = (long)j * P + i;
         double v = f[g];
         if (weighted) v /= ((aW[i] + aE[g]) + (aS[j] + aN[g])) + rr[g];
@@ -339,8 +339,8 @@ __global__ void __launch_bounds__(kRedThreads) k_corner_rhs(int N, long P, long 
     const int n = N / 2;
     double acc = 0.0;
     const long tot = (long)n * (j1 - j0 + 1);           // corner rows j0 .. j1
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / n) + j0, i = (int)(p % n) + 1;
+    for (GridWalk gw(tot, n, j0); gw.ok(); gw.next()) {
+        const int j = gw.j, i = gw.i;
         const long g = (long)j * P + i;
         double s = 1.0;
         if (weighted) s = ((aW[i] + aE[g]) + (aS[j] + aN[g])) + rr[g];
@@ -366,8 +366,8 @@ __global__ void __launch_bounds__(kRedThreads) k_mg_resid(int nl, long Pv, long 
     __shared__ double sm[32];
     double acc = 0.0;
     const long tot = (long)nl * nl;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
+    for (GridWalk gw(tot, nl, 1); gw.ok(); gw.next()) {
+        const int j = gw.j, i = gw.i;
         const long g = (long)j * Pv + i, c = (long)j * Pc + i;
         double zc, zw, ze, zs, zn;
         if (e) {
@@ -395,8 +395,8 @@ __global__ void __launch_bounds__(kRedThreads) k_mg_resid(int nl, long Pv, long 
 __global__ void k_prolong_add(int nl, long Pv, double *e, const double *ec, long Pcv, Wts W)
 {
     const long tot = (long)nl * nl;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
+    for (GridWalk gw(tot, nl, 1); gw.ok(); gw.next()) {
+        const int j = gw.j, i = gw.i;
         e[(long)j * Pv + i] += W.uni ? interp_w<true>(ec, Pcv, i, j, W) : interp_w<false>(ec, Pcv, i, j, W);
     }
 }
@@ -406,8 +406,8 @@ __global__ void k_corner_out(int n, long P0, const double *zc, long P, double *z
 {
     if (ms) zc = ms->zcur;                          // corner graph: nullptr when no cycle ran (z = 0)
     const long tot = (long)n * (j1 - j0 + 1);
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / n) + j0, i = (int)(p % n) + 1;
+    for (GridWalk gw(tot, n, j0); gw.ok(); gw.next()) {
+        const int j = gw.j, i = gw.i;
         z[(long)j * P + i] = zc ? zc[(long)j * P0 + i] : 0.0;
     }
 }

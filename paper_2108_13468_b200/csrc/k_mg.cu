@@ -650,8 +650,8 @@ __global__ void __launch_bounds__(256) k_gs_prep(int nl, long pv, const double *
     const double *__restrict__ cd, long pc, int bscaled, int j0, int j1, Wts W)
 {
     const long tot = (long)nl * (j1 - j0 + 1);         // rows j0 .. j1 of the level
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / nl) + j0, i = (int)(p % nl) + 1;
+    for (GridWalk gw(tot, nl, j0); gw.ok(); gw.next()) {
+        const int j = gw.j, i = gw.i;
         const long v = (long)j * pv + i;
         double ew = e[v - 1], es = e[v - pv];
         if (ec) {
@@ -668,8 +668,8 @@ __global__ void __launch_bounds__(256) k_gs_prep(int nl, long pv, const double *
 __global__ void k_scale_cd(int nl, long pv, long pc, const double *__restrict__ b, const double *__restrict__ cd, double *q)
 {
     const long tot = (long)nl * nl;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
+    for (GridWalk gw(tot, nl, 1); gw.ok(); gw.next()) {
+        const int j = gw.j, i = gw.i;
         q[(long)j * pv + i] = b[(long)j * pv + i] * cd[(long)j * pc + i];
     }
 }
@@ -997,8 +997,13 @@ bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs)
 // S = diag(hbar_i kbar_j).  One CTA per RT x RT coarse tile: the S-scaled residual of the
 // (2RT+1)^2 fine nodes it needs is formed once into shared memory, then gathered.  rho is never
 // written to HBM.
+// LOW: e is the pre-smoothing sweep from zero on R (the V-cycle's order), so
+// D e = R + aE e_E + aN e_N and the residual is exactly its lower part,
+//   rho = R - A_l e = aW e(i-1,j) + aS e(i,j-1)
+// (the identity holds in exact arithmetic; computed this way it has no cancellation).  The kernel
+// then reads e alone: 8 B per fine node instead of 40 (R, e, aE, aN, r).
 // ------------------------------------------------------------------------------------------
-template <int RT, bool UNI>
+template <int RT, bool UNI, bool LOW>
 __global__ void __launch_bounds__(256, 7) k_resid_restrict(int nf, long pv, long pc, const double *__restrict__ e,
     const double *__restrict__ R, const double *__restrict__ aE, const double *__restrict__ aN,
     const double *__restrict__ rr, const double *__restrict__ aW, const double *__restrict__ aS,
@@ -1016,7 +1021,12 @@ __global__ void __launch_bounds__(256, 7) k_resid_restrict(int nf, long pv, long
         const int di = p % RFW, dj = p / RFW;
         const int i = fi0 + di, j = fj0 + dj;
         double v = 0.0;
-        if (i <= nf && j <= nf) {
+        if (LOW) {
+            if (i <= nf && j <= nf) {
+                const long g = (long)j * pv + i;
+                v = (hbf[i] * kbf[j]) * (aW[i] * e[g - 1] + aS[j] * e[g - pv]);
+            }
+        } else if (i <= nf && j <= nf) {
             const long g = (long)j * pv + i, q = (long)j * pc + i;
             const double ec = e[g];
             const double vW = aW[i], vE = aE[q], vS = aS[j], vN = aN[q], vr = rr[q];
@@ -1048,17 +1058,20 @@ __global__ void __launch_bounds__(256, 7) k_resid_restrict(int nf, long pv, long
     }
 }
 
+// R == nullptr: e is the pre-smoothing sweep from zero (LOW above); R is not read
 void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e, bool rs_in, bool scale_out)
 {
     Level &F = c->lev[l], &C = c->lev[l + 1];
-    ProfScope ps(c, 4, (double)F.n * F.n * 40.0 + 8.0 * C.n * (double)C.n);
+    const bool low = R == nullptr;
+    ProfScope ps(c, 4, (double)F.n * F.n * (low ? 8.0 : 40.0) + 8.0 * C.n * (double)C.n);
     // coarse tile edge: enough CTAs to fill the GPU on the small levels, and several waves of
     // CTAs on the large ones (one wave plus a small remainder leaves most SMs idle in the tail)
     const int RTn = C.n >= 128 ? 16 : 8;
     // coarse rows: this rank's strip of level l+1 when level l runs on strips
     const int jc0 = F.sdist ? C.slo : 1, jc1 = F.sdist ? C.shi : C.n;
     const dim3 grid((C.n + RTn - 1) / RTn, (jc1 - jc0 + RTn) / RTn);
-#define SPP_RR(T) (F.w.uni ? k_resid_restrict<T, true> : k_resid_restrict<T, false>)<<<grid, T >= 32 ? 256 : (T >= 16 ? 256 : 128), 0, c->st>>>(F.n, F.pitch, \
+#define SPP_RR(T) (low ? (F.w.uni ? k_resid_restrict<T, true, true> : k_resid_restrict<T, false, true>) \
+                       : (F.w.uni ? k_resid_restrict<T, true, false> : k_resid_restrict<T, false, false>))<<<grid, T >= 32 ? 256 : (T >= 16 ? 256 : 128), 0, c->st>>>(F.n, F.pitch, \
         F.cpitch, e, R, F.aE, F.aN, F.rr, F.aW, F.aS, F.hb, F.kb, C.n, C.pitch, C.hb, C.kb, C.b, C.cd, C.cpitch, \
         rs_in ? 1 : 0, scale_out ? 1 : 0, jc0, jc1, F.w)
     if (RTn == 32) SPP_RR(32);
@@ -1086,8 +1099,8 @@ __global__ void __launch_bounds__(kRedThreads) k_cycle_update(int nl, long pv, l
     // z' = z + e on rows jz0 .. jz1; rho and the norm on the owned rows j0 .. j1 (a row strip
     // also carries z' on its one-row halos; everything 1 .. nl on one GPU)
     const long tot = (long)nl * (jz1 - jz0 + 1);
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / nl) + jz0, i = (int)(p % nl) + 1;
+    for (GridWalk gw(tot, nl, jz0); gw.ok(); gw.next()) {
+        const int j = gw.j, i = gw.i;
         const long g = (long)j * pv + i, q = (long)j * pc + i;
         const bool own = j >= j0 && j <= j1;
         double zc = e[g];
@@ -1147,8 +1160,8 @@ __global__ void k_level_rho(int nl, long pc, const double *aE, const double *aN,
     __shared__ double sm[3][32];
     double mx = 0.0, gy = 0.0, gx = 0.0;
     const long tot = (long)nl * nl;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
+    for (GridWalk gw(tot, nl, 1); gw.ok(); gw.next()) {
+        const int j = gw.j, i = gw.i;
         const long q = (long)j * pc + i;
         const double ca = (i < nl ? aE[q] : 0.0) * cd[q], cn = (j < nl ? aN[q] : 0.0) * cd[q];
         mx = fmax(mx, ca + cn);
@@ -1179,8 +1192,8 @@ __global__ void k_level_rho(int nl, long pc, const double *aE, const double *aN,
 __global__ void k_ycoef(int nl, long pc, const double *aE, const double *aN, const double *cd, double *ya, double *yn)
 {
     const long tot = (long)nl * nl;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / nl) + 1, i = (int)(p % nl) + 1;
+    for (GridWalk gw(tot, nl, 1); gw.ok(); gw.next()) {
+        const int j = gw.j, i = gw.i;
         const long q = (long)j * pc + i;
         ya[q] = aE[q] * cd[q + 1];
         yn[q] = aN[q] * cd[q + pc];

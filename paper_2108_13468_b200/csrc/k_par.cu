@@ -38,8 +38,8 @@ __global__ void k_par_level0(int n, long P, const double *__restrict__ aE, const
                              const double *__restrict__ hb, const double *__restrict__ kb, double *a)
 {
     const long tot = (long)n * n;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / n) + 1, i = (int)(p % n) + 1;
+    for (GridWalk gw(tot, n, 1); gw.ok(); gw.next()) {
+        const long p = gw.p; const int j = gw.j, i = gw.i;
         const long g = (long)j * P + i;
         const double S = hb[i] * kb[j];
         const double D = ((aW[i] + aE[g]) + (aS[j] + aN[g])) + rr[g];
@@ -58,8 +58,8 @@ __global__ void k_par_level0(int n, long P, const double *__restrict__ aE, const
 __global__ void k_par_weights(ParLev L, double *wW, double *wE)
 {
     const long tot = (long)L.nx * L.ny;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / L.nx) + 1, i = (int)(p % L.nx) + 1;
+    for (GridWalk gw(tot, L.nx, 1); gw.ok(); gw.next()) {
+        const long p = gw.p; const int j = gw.j, i = gw.i;
         double w = 0.0, e = 0.0;
         if (i & 1) {
             const double den = (st9(L, 1, i, j) + st9(L, 4, i, j)) + st9(L, 7, i, j);
@@ -86,8 +86,8 @@ __device__ __forceinline__ double par_P(const ParLev &F, int i, int j, int I)
 __global__ void k_par_galerkin(ParLev F, int ncx, double *ac)
 {
     const long tot = (long)ncx * F.ny;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / ncx) + 1, I = (int)(p % ncx) + 1;
+    for (GridWalk gw(tot, ncx, 1); gw.ok(); gw.next()) {
+        const long p = gw.p; const int j = gw.j, I = gw.i;
         double v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
         for (int i = 2 * I - 1; i <= 2 * I + 1; ++i) {
             if (i > F.nx) continue;
@@ -118,8 +118,8 @@ __global__ void __launch_bounds__(kRedThreads) k_par_resid(ParLev L, const doubl
     __shared__ double sm[32];
     double acc = 0.0;
     const long tot = (long)L.nx * L.ny;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / L.nx) + 1, i = (int)(p % L.nx) + 1;
+    for (GridWalk gw(tot, L.nx, 1); gw.ok(); gw.next()) {
+        const int j = gw.j, i = gw.i;
         const long g = (long)j * L.pv + i;
         double s = 0.0;
 #pragma unroll
@@ -151,8 +151,8 @@ __global__ void k_par_scale(int n, long pv, const double *__restrict__ b, const 
                             const double *__restrict__ kb, double *sb)
 {
     const long tot = (long)n * n;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / n) + 1, i = (int)(p % n) + 1;
+    for (GridWalk gw(tot, n, 1); gw.ok(); gw.next()) {
+        const int j = gw.j, i = gw.i;
         sb[(long)j * pv + i] = (hb[i] * kb[j]) * b[(long)j * pv + i];
     }
 }
@@ -161,8 +161,8 @@ __global__ void k_par_scale(int n, long pv, const double *__restrict__ b, const 
 __global__ void k_par_restrict(ParLev F, int ncx, long pvc, const double *__restrict__ r, double *bc)
 {
     const long tot = (long)ncx * F.ny;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / ncx) + 1, I = (int)(p % ncx) + 1;
+    for (GridWalk gw(tot, ncx, 1); gw.ok(); gw.next()) {
+        const int j = gw.j, I = gw.i;
         double s = 0.0;
         for (int i = 2 * I - 1; i <= 2 * I + 1; ++i)
             if (i <= F.nx) s += par_P(F, i, j, I) * r[(long)j * F.pv + i];
@@ -174,8 +174,8 @@ __global__ void k_par_restrict(ParLev F, int ncx, long pvc, const double *__rest
 __global__ void k_par_prolong(ParLev F, int ncx, long pvc, const double *__restrict__ ec, double *e)
 {
     const long tot = (long)F.nx * F.ny;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < tot; p += (long)gridDim.x * blockDim.x) {
-        const int j = (int)(p / F.nx) + 1, i = (int)(p % F.nx) + 1;
+    for (GridWalk gw(tot, F.nx, 1); gw.ok(); gw.next()) {
+        const int j = gw.j, i = gw.i;
         double s = 0.0;
         for (int I = (i - 1) / 2; I <= (i + 1) / 2; ++I)
             if (I >= 1 && I <= ncx) s += par_P(F, i, j, I) * ec[(long)j * pvc + I];

@@ -38,6 +38,26 @@ __device__ __forceinline__ void zero_tail(double *part)
         for (int b = gridDim.x + threadIdx.x; b < kRedBlocks; b += blockDim.x) part[b] = 0.0;
 }
 constexpr int kRedThreads = 256;
+
+// Grid-stride walk over level nodes (i, j), i = 1..m, j = j0.. in the order p = (j - j0) m + (i - 1):
+// one division at the start, then (i, j) advance incrementally (a 64-bit division per element was
+// a visible share of the memory-bound kernels' issue slots).  Same visiting order as p / m, p % m.
+struct GridWalk {
+    long p, tot, stride;
+    int i, j, m, si, sj;
+    __device__ __forceinline__ GridWalk(long tot_, int m_, int j0)
+        : p(blockIdx.x * (long)blockDim.x + threadIdx.x), tot(tot_), stride((long)gridDim.x * blockDim.x), m(m_)
+    {
+        j = (int)(p / m) + j0; i = (int)(p % m) + 1;
+        sj = (int)(stride / m); si = (int)(stride % m);
+    }
+    __device__ __forceinline__ bool ok() const { return p < tot; }
+    __device__ __forceinline__ void next()
+    {
+        p += stride; i += si; j += sj;
+        if (i > m) { i -= m; ++j; }
+    }
+};
 constexpr long kTmaSlack = 1L << 16;     // doubles appended to grid allocations (TMA over-read)
 
 inline long round_up(long a, long b) { return (a + b - 1) / b * b; }

@@ -99,6 +99,11 @@ def test_bs_transfer_hooks():
         S.apply_stage("RESID_RESTRICT", torch.cat([dev(b), dev(e0)]), out, level=l)
         want = P.restrict(l, P.level_residual(l, b, e0)) / P.level_coef(l + 1)["D"]
         assert relmax(out.cpu().numpy(), want) <= 1e-12, l
+        out = torch.zeros(nc * nc, dtype=torch.float64, device="cuda")
+        S.apply_stage("PRE_RESTRICT", dev(b), out, level=l)
+        e1 = P.gs_sweep(l, b, np.zeros((nl, nl)))
+        want = P.restrict(l, P.level_residual(l, b, e1)) / P.level_coef(l + 1)["D"]
+        assert relmax(out.cpu().numpy(), want) <= 1e-12, l
         out = dev(e0)
         S.apply_stage("PROLONG_ADD", dev(ec), out, level=l)
         assert relmax(out.cpu().numpy(), P.prolong_add(l, ec, e0)) <= 1e-14, l

@@ -146,6 +146,13 @@ def test_product_path_hooks(name, N, eps):
         S.apply_stage("RESID_RESTRICT", torch.cat([dev(b), dev(e0)]), out, level=l)
         want = P.restrict(l, P.level_residual(l, b, e0)) / P.level_coef(l + 1)["D"]
         assert relmax(host(out), want) <= 1e-12, l
+        # the V-cycle's pair: pre-smoothing from zero, then the restriction of its residual
+        # (formed on the GPU as aW e_W + aS e_S; the oracle forms b - A_l e)
+        out = torch.zeros(nc * nc, dtype=torch.float64, device="cuda")
+        S.apply_stage("PRE_RESTRICT", dev(b), out, level=l)
+        e1 = P.gs_sweep(l, b, np.zeros((nl, nl)))
+        want = P.restrict(l, P.level_residual(l, b, e1)) / P.level_coef(l + 1)["D"]
+        assert relmax(host(out), want) <= 1e-12, l
 
 
 @pytest.mark.parametrize("name,N,eps", [("cfg4", 256, 1e-8), ("exp2d", 128, 1e-4), ("cfg2", 128, 1e-2)])
