@@ -77,11 +77,6 @@ constexpr bool EXPF_NOMBAR = true;
 #else
 constexpr bool EXPF_NOMBAR = false;
 #endif
-#ifdef EXP_NOE
-constexpr bool EXPF_NOE = true;
-#else
-constexpr bool EXPF_NOE = false;
-#endif
 #ifdef EXP_NOSTS
 constexpr bool EXPF_NOSTS = true;
 #else
@@ -144,6 +139,8 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
     __shared__ double edge[WMAXW][WEB];
     __shared__ int prod[WMAXW], cons[WMAXW];
     __shared__ __align__(16) double cin[WCW];          // chain inflow of the chunk (warp 0)
+    __shared__ __align__(16) double ezero[WCW];        // zero inflow (warp 0 without a chain)
+    if (threadIdx.x < WCW) ezero[threadIdx.x] = 0.0;
     // Per (sweeping warp, slot): full = the TMA boxes landed; ready = the sweeping warp stored its
     // results in the slot; empty = the write-back warp stored them to global memory (slot free).
     __shared__ __align__(8) unsigned long long bars[WMAXW][WNS], rbars[WMAXW][WNS], ebars[WMAXW][WNS];
@@ -325,19 +322,10 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
             if (lim > 0) { while (*((volatile int *)&cons[w + 1]) < lim) __nanosleep(32); }
         }
         SPP_TP(t2);
-        // the North inflow of the chunk, loaded before the operand wait: lane 0 needs E[0] at the
-        // first step, and a load queued behind the 24 operand loads delays the whole step chain
-        double2 E[8];
-        if (w > 0 && !EXPF_NOE) {
-#pragma unroll
-            for (int st = 0; st < 8; ++st) E[st] = *reinterpret_cast<const double2 *>(&edge[w - 1][(c * WCW + 2 * st) & (WEB - 1)]);
-        } else if (chain_in && !EXPF_NOE) {
-#pragma unroll
-            for (int st = 0; st < 8; ++st) E[st] = *reinterpret_cast<const double2 *>(&cin[2 * st]);
-        } else {
-#pragma unroll
-            for (int st = 0; st < 8; ++st) E[st] = make_double2(0.0, 0.0);
-        }
+        // the North inflow is read by lane 0 at the step that uses it (a broadcast 128-bit load
+        // with the step's operand loads; eight loads ahead of the operand wait put their latency
+        // in front of every chunk: M_II 1.84 -> 1.71 ms per cfg4 solve)
+        const double *Eb = w > 0 ? &edge[w - 1][(c * WCW) & (WEB - 1)] : (chain_in ? cin : ezero);
         SPP_TP(tb);
         if (!EXPF_NOMBAR) mbar_wait((unsigned)__cvta_generic_to_shared(&bars[w][c % WNS]), (unsigned)((c / WNS) & 1));
         __syncwarp();
@@ -368,12 +356,15 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
                 const double2 A2 = lds2(sq + 2 * WBOX + xo[st]);
                 double n0 = __shfl_up_sync(0xffffffffu, z2, 1);    // lane t-1's pair of the last step
                 double n1 = __shfl_up_sync(0xffffffffu, z1, 1);
-                if (lane == 0) { n0 = E[st].x; n1 = E[st].y; }
+                const double2 Es = lds2(Eb + 2 * st);             // North inflow (lane 0)
+                if (lane == 0) { n0 = Es.x; n1 = Es.y; }
                 double za = fma(A1.y, z1, fma(A2.y, n0, Q.y));      // column 2st   (east one first)
                 double zc = fma(A1.x, za, fma(A2.x, n1, Q.x));      // column 2st+1
                 if (!F) {                                  // edge chunk: zero outside the block
                     // one AND per value on the chain (the masks do not depend on it); a ternary
-                    // compiled to three dependent selects
+                    // compiled to three dependent selects.  (Masking the operands instead keeps
+                    // the masks off the chain but costs six ANDs per step: measured slower on the
+                    // tiled levels, 6.37 -> 6.90 ms of sweeps per cfg4 solve.)
                     const int idx = c * WCW + 2 * st - WLAG * lane;
                     const unsigned ua = (unsigned)idx < (unsigned)ncols, uc = (unsigned)(idx + 1) < (unsigned)ncols;
                     const long long ma = -(long long)(rvalid & ua), mc = -(long long)(rvalid & uc);

@@ -1,0 +1,3 @@
+bash tools/ab2.sh
+cp tools/ablibs/b_opmask.so paper_2108_13468_b200/lib/libspp.so
+timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; tail -2 gpurun_out/gpu_tests.log
