@@ -64,6 +64,9 @@ def lib():
         L.orc2_solve.argtypes = [ctypes.c_void_p, _dp, _dp, ctypes.c_int, ctypes.c_int,
                                  ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, ctypes.c_int,
                                  _ip, _dp]
+        L.orc2_solve_r.argtypes = [ctypes.c_void_p, _dp, _dp, ctypes.c_int, ctypes.c_int,
+                                   ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp,
+                                   ctypes.c_int, _ip, _dp]
         L.orc2_levels.argtypes = [ctypes.c_void_p]
         L.orc2_level_n.argtypes = [ctypes.c_void_p, ctypes.c_int]
         L.orc2_get_coef.argtypes = [ctypes.c_void_p, _dp, _dp, _dp, _dp, _dp]
@@ -372,14 +375,15 @@ class Oracle2D:
             raise RuntimeError(rc)
         return u
 
-    def solve(self, f, *, weighted=1, stop_abs=0, tol=1e-8, maxit=200, fixed_iters=0):
+    def solve(self, f, *, weighted=1, stop_abs=0, tol=1e-8, maxit=200, fixed_iters=0, restart=0):
+        """FGMRES (restart = 0, the paper) or FGMRES(restart) (reading R23)"""
         f = self._g(f)
         u = self._g()
         hist = np.zeros(maxit + 2)
         oi = (ctypes.c_int * 8)()
         od = (ctypes.c_double * 4)()
-        rc = lib().orc2_solve(self.h, _p(f), _p(u), weighted, stop_abs, tol, maxit, fixed_iters,
-                              _p(hist), len(hist), oi, od)
+        rc = lib().orc2_solve_r(self.h, _p(f), _p(u), weighted, stop_abs, tol, maxit, fixed_iters,
+                                restart, _p(hist), len(hist), oi, od)
         if rc < 0:
             raise RuntimeError(f"orc2_solve rc={rc}")
         it = oi[0]

@@ -265,28 +265,35 @@ static void apply_givens(double *h, double *cs, double *sn, double *g, int k)
 }
 
 /* Flexible GMRES (Saad 2003, cited P:1306-1308), right-preconditioned, modified
- * Gram-Schmidt, no restart, x0 = 0 ("no restarts" P:831).
+ * Gram-Schmidt, x0 = 0.  restart = 0: no restart (the paper, "no restarts" P:831);
+ * restart = m > 0: FGMRES(m) (SURVEY 8(b) `restart`, reading R23): after m Arnoldi steps without
+ * convergence the iterate is formed, x <- x + sum_j y_j z_j, and the process restarts from the
+ * true residual r = W (f - A x) (Saad 2003, the restarted Algorithm 9.6), the stopping target
+ * staying the one of the initial residual.  With restart >= the steps taken, every operation is
+ * the unrestarted one.
  *   weighted = 1 (BASELINE mode, reading R11): run on (W A) x = W f with W = D^{-1}; the
  *     preconditioner for W A is (W M)^{-1} = M^{-1} D, so z_k = M^{-1}(D v_k).
  *   weighted = 0 (paper mode): plain A x = f, z_k = M^{-1} v_k.
  *   stop_abs = 0: |g_{k+1}| <= tol * beta (relative);  stop_abs = 1: |g_{k+1}| <= tol
  *     (the paper's ||R|| <= 10 N^{-1} ln N, Euclidean).
- *   fixed_iters > 0: run exactly that many Arnoldi steps (parity mode, reading R17).
- * hist[0] = beta, hist[k+1] = |g_{k+1}| (recurrence residual). */
-int orc_fgmres(const orc_sys *s, const double *f, double *x, int weighted, int stop_abs,
-               double tol, int maxit, int fixed_iters, double *hist, int hist_cap,
-               orc_kstats *st)
+ *   fixed_iters > 0: run exactly that many Arnoldi steps in total (parity mode, reading R17).
+ * hist[0] = beta, hist[k+1] = |g_{k+1}| of the k-th step overall (recurrence residual, S:534;
+ * after a restart the recurrence starts from the true residual of the restart). */
+int orc_fgmres_r(const orc_sys *s, const double *f, double *x, int weighted, int stop_abs,
+                 double tol, int maxit, int fixed_iters, int restart, double *hist, int hist_cap,
+                 orc_kstats *st)
 {
     size_t n = s->n;
     memset(st, 0, sizeof(*st));
-    double **V = calloc((size_t)maxit + 1, sizeof(double *));
-    double **Z = calloc((size_t)maxit + 1, sizeof(double *));
-    double *H = calloc((size_t)(maxit + 1) * (maxit + 1), sizeof(double)); /* column k at H + k*(maxit+1) */
-    double *cs = calloc((size_t)maxit + 1, sizeof(double)), *sn = calloc((size_t)maxit + 1, sizeof(double));
-    double *g = calloc((size_t)maxit + 2, sizeof(double)), *y = calloc((size_t)maxit + 1, sizeof(double));
+    const int mr = (restart > 0 && restart < maxit) ? restart : maxit;   /* steps per cycle */
+    double **V = calloc((size_t)mr + 1, sizeof(double *));
+    double **Z = calloc((size_t)mr + 1, sizeof(double *));
+    double *H = calloc((size_t)(mr + 1) * (mr + 1), sizeof(double)); /* column k at H + k*(mr+1) */
+    double *cs = calloc((size_t)mr + 1, sizeof(double)), *sn = calloc((size_t)mr + 1, sizeof(double));
+    double *g = calloc((size_t)mr + 2, sizeof(double)), *y = calloc((size_t)mr + 1, sizeof(double));
     double *q = malloc(sizeof(double) * n), *w = malloc(sizeof(double) * n);
     if (!V || !Z || !H || !cs || !sn || !g || !y || !q || !w) { st->status = ORC_E_NOMEM; goto done; }
-    int ld = maxit + 1;
+    int ld = mr + 1;
 
     V[0] = malloc(sizeof(double) * n);
     if (!V[0]) { st->status = ORC_E_NOMEM; goto done; }
@@ -297,58 +304,77 @@ int orc_fgmres(const orc_sys *s, const double *f, double *x, int weighted, int s
     if (hist_cap > 0) hist[0] = beta;
     memset(x, 0, sizeof(double) * n);
     if (beta == 0.0) { st->converged = 1; st->res_final = 0.0; goto done; }
-    for (size_t i = 0; i < n; i++) V[0][i] /= beta;
-    g[0] = beta;
     double target = stop_abs ? tol : tol * beta;
-    int k;
-    for (k = 0; k < maxit; k++) {
-        /* z_k = M^{-1}(s v_k) */
-        for (size_t i = 0; i < n; i++) q[i] = weighted ? s->D[i] * V[k][i] : V[k][i];
-        Z[k] = malloc(sizeof(double) * n);
-        if (!Z[k]) { st->status = ORC_E_NOMEM; goto done; }
-        int ps = s->Minv(s->ctx, q, Z[k]);
-        if (ps < 0) { st->status = ps; goto done; }
-        /* w = W A z_k */
-        s->A(s->ctx, Z[k], w);
-        if (weighted) for (size_t i = 0; i < n; i++) w[i] /= s->D[i];
-        /* modified Gram-Schmidt ("modified Gram-Schmidt and Arnoldi steps") */
-        double *h = H + (size_t)k * ld;
-        for (int j = 0; j <= k; j++) {
-            h[j] = dot(n, w, V[j]);
-            for (size_t i = 0; i < n; i++) w[i] -= h[j] * V[j][i];
+    int total = 0;                                  /* Arnoldi steps over all cycles */
+    for (;;) {                                      /* restart cycles (one when restart = 0) */
+        for (size_t i = 0; i < n; i++) V[0][i] /= beta;
+        memset(g, 0, sizeof(double) * ((size_t)mr + 2));
+        g[0] = beta;
+        int k, stop = 0;
+        for (k = 0; k < mr && total < maxit; k++) {
+            /* z_k = M^{-1}(s v_k) */
+            for (size_t i = 0; i < n; i++) q[i] = weighted ? s->D[i] * V[k][i] : V[k][i];
+            if (!Z[k]) Z[k] = malloc(sizeof(double) * n);
+            if (!Z[k]) { st->status = ORC_E_NOMEM; goto done; }
+            int ps = s->Minv(s->ctx, q, Z[k]);
+            if (ps < 0) { st->status = ps; goto done; }
+            /* w = W A z_k */
+            s->A(s->ctx, Z[k], w);
+            if (weighted) for (size_t i = 0; i < n; i++) w[i] /= s->D[i];
+            /* modified Gram-Schmidt ("modified Gram-Schmidt and Arnoldi steps") */
+            double *h = H + (size_t)k * ld;
+            for (int j = 0; j <= k; j++) {
+                h[j] = dot(n, w, V[j]);
+                for (size_t i = 0; i < n; i++) w[i] -= h[j] * V[j][i];
+            }
+            h[k + 1] = sqrt(dot(n, w, w));
+            if (!V[k + 1]) V[k + 1] = malloc(sizeof(double) * n);
+            if (!V[k + 1]) { st->status = ORC_E_NOMEM; goto done; }
+            /* SURVEY 5 "NaN/Inf guard on h_{k+1,k}": a non-finite entry is a failure, and only an
+             * exact zero h_{k+1,k} is a (happy) breakdown */
+            for (int j = 0; j <= k + 1; j++) if (!isfinite(h[j])) { st->status = ORC_E_NONFINITE; goto done; }
+            int brk = h[k + 1] == 0.0;
+            for (size_t i = 0; i < n; i++) V[k + 1][i] = brk ? 0.0 : w[i] / h[k + 1];
+            apply_givens(h, cs, sn, g, k);
+            double res = fabs(g[k + 1]);
+            total++;
+            if (total < hist_cap) hist[total] = res;
+            st->iters = total;
+            st->res_final = res;
+            if (brk) { st->breakdown = 1; st->converged = (res <= target); stop = 1; k++; break; }
+            if (fixed_iters > 0) { if (total >= fixed_iters) { st->converged = (res <= target); stop = 1; k++; break; } }
+            else if (res <= target) { st->converged = 1; stop = 1; k++; break; }
         }
-        h[k + 1] = sqrt(dot(n, w, w));
-        V[k + 1] = malloc(sizeof(double) * n);
-        if (!V[k + 1]) { st->status = ORC_E_NOMEM; goto done; }
-        /* SURVEY 5 "NaN/Inf guard on h_{k+1,k}": a non-finite entry is a failure, and only an
-         * exact zero h_{k+1,k} is a (happy) breakdown */
-        for (int j = 0; j <= k + 1; j++) if (!isfinite(h[j])) { st->status = ORC_E_NONFINITE; goto done; }
-        int brk = h[k + 1] == 0.0;
-        for (size_t i = 0; i < n; i++) V[k + 1][i] = brk ? 0.0 : w[i] / h[k + 1];
-        apply_givens(h, cs, sn, g, k);
-        double res = fabs(g[k + 1]);
-        if (k + 1 < hist_cap) hist[k + 1] = res;
-        st->iters = k + 1;
-        st->res_final = res;
-        if (brk) { st->breakdown = 1; st->converged = (res <= target); k++; break; }
-        if (fixed_iters > 0) { if (k + 1 >= fixed_iters) { st->converged = (res <= target); k++; break; } }
-        else if (res <= target) { st->converged = 1; k++; break; }
+        /* solve the k x k upper-triangular system R y = g, then x += sum_j y_j z_j */
+        int kk = k;
+        for (int i = kk - 1; i >= 0; i--) {
+            double t = g[i];
+            for (int j = i + 1; j < kk; j++) t -= H[(size_t)j * ld + i] * y[j];
+            y[i] = t / H[(size_t)i * ld + i];
+        }
+        for (int j = 0; j < kk; j++)
+            for (size_t i = 0; i < n; i++) x[i] += y[j] * Z[j][i];
+        if (stop || total >= maxit) break;
+        /* restart from the true residual v_0 = W (f - A x) */
+        s->A(s->ctx, x, w);
+        for (size_t i = 0; i < n; i++) V[0][i] = weighted ? (f[i] - w[i]) / s->D[i] : f[i] - w[i];
+        beta = sqrt(dot(n, V[0], V[0]));
+        if (!isfinite(beta)) { st->status = ORC_E_NONFINITE; goto done; }
+        if (beta == 0.0) { st->converged = 1; st->res_final = 0.0; break; }
     }
-    /* solve the k x k upper-triangular system R y = g, then x = sum_j y_j z_j */
-    int kk = st->iters;
-    for (int i = kk - 1; i >= 0; i--) {
-        double t = g[i];
-        for (int j = i + 1; j < kk; j++) t -= H[(size_t)j * ld + i] * y[j];
-        y[i] = t / H[(size_t)i * ld + i];
-    }
-    for (int j = 0; j < kk; j++)
-        for (size_t i = 0; i < n; i++) x[i] += y[j] * Z[j][i];
     st->status = st->converged ? ORC_OK : ORC_NOT_CONVERGED;
 done:
-    if (V) for (int j = 0; j <= maxit; j++) free(V[j]);
-    if (Z) for (int j = 0; j <= maxit; j++) free(Z[j]);
+    if (V) for (int j = 0; j <= mr; j++) free(V[j]);
+    if (Z) for (int j = 0; j <= mr; j++) free(Z[j]);
     free(V); free(Z); free(H); free(cs); free(sn); free(g); free(y); free(q); free(w);
     return st->status;
+}
+
+int orc_fgmres(const orc_sys *s, const double *f, double *x, int weighted, int stop_abs,
+               double tol, int maxit, int fixed_iters, double *hist, int hist_cap,
+               orc_kstats *st)
+{
+    return orc_fgmres_r(s, f, x, weighted, stop_abs, tol, maxit, fixed_iters, 0, hist, hist_cap, st);
 }
 
 /* Left-preconditioned GMRES for the 1D paper experiments (MATLAB gmres, "modified
@@ -1135,18 +1161,24 @@ static int cb2_M(void *c, const double *q, double *z) { return orc2_precond((orc
 
 /* FGMRES on the 2D system.  out_i: [0]=iters [1]=converged [2]=mg_cycles_total [3]=mg_min
  * [4]=mg_max [5]=mg_cap_hits [6]=applies;  out_d: [0]=res0 [1]=res_final. */
-int orc2_solve(orc2d *P, const double *f, double *u, int weighted, int stop_abs, double tol,
-               int maxit, int fixed_iters, double *hist, int hist_cap, int *out_i, double *out_d)
+int orc2_solve_r(orc2d *P, const double *f, double *u, int weighted, int stop_abs, double tol,
+                 int maxit, int fixed_iters, int restart, double *hist, int hist_cap, int *out_i, double *out_d)
 {
     P->mg_cycles_total = 0; P->mg_min = 1 << 30; P->mg_max = 0; P->mg_cap_hits = 0; P->applies = 0;
     orc_sys s = {(size_t)P->m * P->m, P, cb2_A, cb2_M, P->D};
     orc_kstats st;
-    int rc = orc_fgmres(&s, f, u, weighted, stop_abs, tol, maxit, fixed_iters, hist, hist_cap, &st);
+    int rc = orc_fgmres_r(&s, f, u, weighted, stop_abs, tol, maxit, fixed_iters, restart, hist, hist_cap, &st);
     out_i[0] = st.iters; out_i[1] = st.converged; out_i[2] = (int)P->mg_cycles_total;
     out_i[3] = P->applies ? P->mg_min : 0; out_i[4] = P->mg_max; out_i[5] = P->mg_cap_hits;
     out_i[6] = P->applies;
     out_d[0] = st.res0; out_d[1] = st.res_final;
     return rc;
+}
+
+int orc2_solve(orc2d *P, const double *f, double *u, int weighted, int stop_abs, double tol,
+               int maxit, int fixed_iters, double *hist, int hist_cap, int *out_i, double *out_d)
+{
+    return orc2_solve_r(P, f, u, weighted, stop_abs, tol, maxit, fixed_iters, 0, hist, hist_cap, out_i, out_d);
 }
 
 /* accessors for tests */
