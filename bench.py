@@ -465,7 +465,7 @@ def run_ours(args, rank, world):
     # warm-up exactly as the timed steps run (this also captures the corner-solve CUDA graph),
     # then one more untimed step with every kernel class profiled, to find the dominant class
     res = None
-    for _ in range(args.warmup):
+    for _ in range(max(1, args.warmup)):      # at least one (its iteration count is the reference)
         res = step(d_c1, d_c2, d_r, d_f, u)
         check(res)
     iters_ref = res.stats["iters"]

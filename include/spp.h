@@ -103,7 +103,10 @@ typedef struct {
     spp_stop stop;
     double tol;
     int32_t max_iters;       /* Arnoldi steps (default 200)                           */
-    int32_t restart;         /* must be 0: no restart (paper); other values SPP_E_ARG  */
+    int32_t restart;         /* 0 = no restart (the paper); m > 0 = FGMRES(m), 2D only:
+                                after m steps x += sum y_j z_j and the next cycle starts from
+                                the true residual, the stop target staying the initial one
+                                (reading R23); max_iters counts all steps          */
     double mg_reduction;     /* corner MG relative reduction of ||S_0 rho||_2 (1e-3) */
     int32_t mg_max_cycles;   /* cycle cap (20)                                        */
     int32_t mg_fixed_cycles; /* 0 = adaptive (paper); > 0 = exactly this many (parity mode)  */
@@ -129,7 +132,8 @@ typedef struct spp_ctx spp_ctx;
 /* Defaults: right/flexible, SPP_STOP_REL_JACOBI, tol 1e-8, 200 iterations, MG 1e-3 / 20 /
  * adaptive / coarsest 4.
  * Option validation (spp_create, spp_create_dist, spp_batch1d_create return SPP_E_ARG):
- * restart != 0; 2D with side = SPP_LEFT or stop = SPP_STOP_ABS_MAX; 1D with exactly one of
+ * restart < 0, restart > 0 in 1D, in row strips or with fixed_iters > 0; 2D with side = SPP_LEFT
+ * or stop = SPP_STOP_ABS_MAX; 1D with exactly one of
  * side = SPP_LEFT / stop = SPP_STOP_ABS_MAX (the left GMRES of P:828-833 always stops on the
  * true max-norm residual, and that stop exists only there); tol <= 0 or not finite. */
 SPP_API void spp_default_options(int32_t dim, spp_options *o);

@@ -17,6 +17,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [*(["-DSPP_WAVE_PROF"] if os.environ.get("SPP_WAVE_PROF") else []),
     *(["-DSPP_LINES_PROF"] if os.environ.get("SPP_LINES_PROF") else []),
     *(["-DSPP_COARSE_PROF"] if os.environ.get("SPP_COARSE_PROF") else []),
+    *(["-DSPP_STRESS"] if os.environ.get("SPP_STRESS") else []),
     *([f"-D{x}" for x in os.environ.get("SPP_EXP", "").split(",") if x]), "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-I", str(ROOT / "include"), "-I", str(SRC)]

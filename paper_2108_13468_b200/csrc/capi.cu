@@ -600,7 +600,11 @@ static cudaError_t fg_build(Ctx *c, int k, cudaGraphExec_t *out)
 // =========================================================================================== ABI
 extern "C" {
 
+#ifdef SPP_STRESS
+const char *spp_version(void) { return "spp-b200 0.1 (sm_100a, fp64) +stress"; }   // race-check build
+#else
 const char *spp_version(void) { return "spp-b200 0.1 (sm_100a, fp64)"; }
+#endif
 
 const char *spp_last_error(const spp_ctx *c)
 {
@@ -677,7 +681,9 @@ static void parse_tune(Ctx *c)
 // silently replaced by other stopping semantics.
 static spp_status check_options(const spp_options *o, int dim, Ctx *c)
 {
-    if (o->restart != 0) FAIL(c, SPP_E_ARG, "restart = %d: only restart = 0 (no restarts, P:831) is implemented", o->restart);
+    if (o->restart < 0) FAIL(c, SPP_E_ARG, "restart = %d must be >= 0", o->restart);
+    if (o->restart > 0 && dim != 2) FAIL(c, SPP_E_ARG, "restart > 0 (FGMRES(m)) is implemented for 2D solves only");
+    if (o->restart > 0 && o->fixed_iters > 0) FAIL(c, SPP_E_ARG, "restart > 0 with fixed_iters > 0 is not implemented");
     if (!(o->tol > 0.0) || !std::isfinite(o->tol)) FAIL(c, SPP_E_ARG, "tol must be finite and > 0");
     if (o->side != SPP_RIGHT_FLEXIBLE && o->side != SPP_LEFT) FAIL(c, SPP_E_ARG, "unknown side %d", (int)o->side);
     if ((int)o->stop < 0 || (int)o->stop > 3) FAIL(c, SPP_E_ARG, "unknown stop %d", (int)o->stop);
@@ -1160,22 +1166,43 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
     double resf = beta;
     const double target = (stop == SPP_STOP_ABS_L2) ? c->opt.tol : c->opt.tol * beta;
     CK(c, cudaMemsetAsync(c->U, 0, sizeof(double) * G, c->st));
+    // FGMRES (restart = 0, the paper) or FGMRES(m) (reading R23): cycles of at most mr Arnoldi
+    // steps; after a cycle without convergence x += sum_j y_j z_j and the next cycle starts from
+    // the true residual W (f - A x), the stopping target staying the initial one
+    const int mr = (c->opt.restart > 0 && c->opt.restart < maxit) ? c->opt.restart : maxit;
+    double bc = beta;                                   // the cycle's initial residual
+    int stopped = 0;
     if (beta == 0.0) converged = 1;
-    else {
-        k_scale<<<nblk(G / 2), 256, 0, c->st>>>(G, c->V[0], 1.0 / beta);
+    for (int cycle = 0; !converged && !stopped && iters < maxit; ++cycle) {
+        if (cycle > 0) {                                // restart vector v0 = W (f - A x) / ||.||
+            k_spmv<<<red_grid((long)m * m), kRedThreads, 0, c->st>>>(m, c->P, c->U, c->aE, c->aN, c->rr, c->aW, c->aS,
+                                                                      0, c->w, nullptr, nullptr, 1, m);
+            k_rhs<<<red_grid((long)m * m), kRedThreads, 0, c->st>>>(m, c->P, c->F, c->aE, c->aN, c->rr, c->aW, c->aS,
+                                                                     weighted, c->V[0], part_slot(c, 0), 1, m, c->w);
+            c->launches += 2;
+            double s2 = 0;
+            CK(c, fetch_sum(c, part_slot(c, 0), &s2));
+            bc = std::sqrt(s2);
+            if (!std::isfinite(bc)) FAIL(c, SPP_E_NONFINITE, "restart residual is not finite after %d iterations", iters);
+            if (bc == 0.0) { converged = 1; break; }
+        }
+        const int steps = std::min(mr, maxit - iters);  // Arnoldi steps of this cycle at most
+        int kk = 0;                                     // steps taken in this cycle
+        k_scale<<<nblk(G / 2), 256, 0, c->st>>>(G, c->V[0], 1.0 / bc);
         c->launches++;
-        g[0] = beta;
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = bc;
         const int ld = maxit + 1;
         if (fg_mode(c)) {                               // iteration graphs, one sync per batch
             CK(c, fg_alloc(c));
             const std::vector<long> sig = fg_signature(c);
             if (c->itg_sig != sig) { fg_destroy(c); c->itg_sig = sig; }
-            k_fg_init<<<1, 1, 0, c->st>>>(c->fgh, fg_arr(c, 2), fg_arr(c, 3), beta, target);
+            k_fg_init<<<1, 1, 0, c->st>>>(c->fgh, fg_arr(c, 2), fg_arr(c, 3), bc, target);
             c->launches++;
             int launched = 0;
-            int batch = std::max(1, std::min(maxit, c->last_iters > 0 ? c->last_iters : 4));
+            int batch = std::max(1, std::min(steps, c->last_iters > 0 ? c->last_iters : 4));
             for (;;) {
-                for (int b = 0; b < batch && launched < maxit; ++b, ++launched) {
+                for (int b = 0; b < batch && launched < steps; ++b, ++launched) {
                     const int k = launched;
                     CK(c, ensure_vectors(c, k + 1));
                     if ((int)c->itg.size() <= k) c->itg.resize(k + 1, nullptr);
@@ -1185,25 +1212,25 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
                 }
                 CK(c, cudaMemcpyAsync(c->hfgh, c->fgh, sizeof(FGHead), cudaMemcpyDeviceToHost, c->st));
                 CK(c, cudaStreamSynchronize(c->st));
-                if (c->hfgh->stop || launched >= maxit) break;
+                if (c->hfgh->stop || launched >= steps) break;
                 batch = 8;
             }
             const FGHead fs = *c->hfgh;
             if (fs.nonfinite)
-                FAIL(c, SPP_E_NONFINITE, "Hessenberg entry h(%d,%d) is not finite at iteration %d", fs.nf_j, fs.k - 1, fs.k);
+                FAIL(c, SPP_E_NONFINITE, "Hessenberg entry h(%d,%d) is not finite at iteration %d", fs.nf_j, fs.k - 1, iters + fs.k);
             if (fs.capfail) FAIL(c, SPP_E_MG_CAP, "corner multigrid hit the cycle cap (%d)", c->opt.mg_max_cycles);
-            iters = fs.k; converged = fs.converged; resf = fs.res;
-            mg_tot = fs.mg_tot; mg_min = fs.mg_min; mg_max = fs.mg_max; caps = fs.caps;
-            for (int k = 0; k < iters; ++k) c->launches += c->itg_launches[k];
-            c->launches += (int64_t)mg_tot * c->cg_body_launches;
-            CK(c, cudaMemcpyAsync(H.data(), fg_H(c), sizeof(double) * (size_t)iters * ld, cudaMemcpyDeviceToHost, c->st));
-            CK(c, cudaMemcpyAsync(g.data(), fg_arr(c, 2), sizeof(double) * (iters + 1), cudaMemcpyDeviceToHost, c->st));
-            if (hist && hcap > 1)
-                CK(c, cudaMemcpyAsync(hist + 1, fg_arr(c, 3) + 1, sizeof(double) * std::min(iters, hcap - 1),
+            kk = fs.k; converged = fs.converged; stopped = fs.stop; resf = fs.res;
+            mg_tot += fs.mg_tot; mg_min = std::min(mg_min, fs.mg_min); mg_max = std::max(mg_max, fs.mg_max); caps += fs.caps;
+            for (int k = 0; k < kk; ++k) c->launches += c->itg_launches[k];
+            c->launches += (int64_t)fs.mg_tot * c->cg_body_launches;
+            CK(c, cudaMemcpyAsync(H.data(), fg_H(c), sizeof(double) * (size_t)kk * ld, cudaMemcpyDeviceToHost, c->st));
+            CK(c, cudaMemcpyAsync(g.data(), fg_arr(c, 2), sizeof(double) * (kk + 1), cudaMemcpyDeviceToHost, c->st));
+            if (hist && hcap > iters + 1)
+                CK(c, cudaMemcpyAsync(hist + iters + 1, fg_arr(c, 3) + 1, sizeof(double) * std::min(kk, hcap - 1 - iters),
                                       cudaMemcpyDeviceToHost, c->st));
             CK(c, cudaStreamSynchronize(c->st));
         } else
-        for (int k = 0; k < maxit; ++k) {
+        for (int k = 0; k < steps; ++k) {
             CK(c, ensure_vectors(c, k + 1));
             int cap = 0;
             cudaError_t err = cudaSuccess;
@@ -1229,36 +1256,41 @@ static spp_status solve_2d(Ctx *c, const double *f, double *u, spp_mem mem, doub
                 // SURVEY 5 "NaN/Inf guard on h_{k+1,k}": a non-finite Hessenberg entry is a
                 // failure (non-finite data or a preconditioner blow-up), never a breakdown
                 if (!std::isfinite(h[j]))
-                    FAIL(c, SPP_E_NONFINITE, "Hessenberg entry h(%d,%d) is not finite at iteration %d", j, k, k + 1);
+                    FAIL(c, SPP_E_NONFINITE, "Hessenberg entry h(%d,%d) is not finite at iteration %d", j, k, iters + k + 1);
             }
             int brk = 0;
             const double res = givens_update(h, cs.data(), sn.data(), g.data(), k, &brk);
-            iters = k + 1;
+            kk = k + 1;
             resf = res;
-            if (hist && k + 1 < hcap) hist[k + 1] = res;
-            if (fg_stop(k, res, brk, target, c->opt.fixed_iters, maxit, &converged)) break;
+            if (hist && iters + k + 1 < hcap) hist[iters + k + 1] = res;
+            // the cycle's last step ends it without a verdict (maxit = steps); a stop before it is final
+            const int fin = fg_stop(k, res, brk, target, c->opt.fixed_iters, steps, &converged);
+            if (fin && (converged || brk || c->opt.fixed_iters > 0 || k + 1 < steps)) stopped = 1;
+            if (fin) break;
         }
-        c->last_iters = iters;
-        // y = R^{-1} g;  x = sum_j y_j z_j
-        for (int i = iters - 1; i >= 0; --i) {
+        // y = R^{-1} g;  x (+)= sum_j y_j z_j
+        for (int i = kk - 1; i >= 0; --i) {
             double t = g[i];
-            for (int j = i + 1; j < iters; ++j) t -= H[(size_t)j * (maxit + 1) + i] * yv[j];
+            for (int j = i + 1; j < kk; ++j) t -= H[(size_t)j * (maxit + 1) + i] * yv[j];
             yv[i] = t / H[(size_t)i * (maxit + 1) + i];
         }
         // device copies of the Z pointers and y (pinned staging, pre-allocated device slots)
         const double **hz = (const double **)(c->hpin + 4 * kRedBlocks);
         double *hy = c->hpin + 4 * kRedBlocks + maxit + 8;
-        for (int j = 0; j < iters; ++j) { hz[j] = c->Z[j]; hy[j] = yv[j]; }
+        if (cycle > 0) CK(c, cudaStreamSynchronize(c->st));   // staging of the last cycle's copies
+        for (int j = 0; j < kk; ++j) { hz[j] = c->Z[j]; hy[j] = yv[j]; }
         const double **dptr = (const double **)(c->dscal + maxit + 8);
         double *dy = c->dscal + 2 * maxit + 16;
-        CK(c, cudaMemcpyAsync(dptr, hz, sizeof(double *) * iters, cudaMemcpyHostToDevice, c->st));
-        CK(c, cudaMemcpyAsync(dy, hy, sizeof(double) * iters, cudaMemcpyHostToDevice, c->st));
+        CK(c, cudaMemcpyAsync(dptr, hz, sizeof(double *) * kk, cudaMemcpyHostToDevice, c->st));
+        CK(c, cudaMemcpyAsync(dy, hy, sizeof(double) * kk, cudaMemcpyHostToDevice, c->st));
         {
-            ProfScope ps(c, 7, 8.0 * G * (iters + 1));
-            k_update_x<<<nblk(G / 2), 256, 0, c->st>>>(G, iters, dptr, dy, c->U);
+            ProfScope ps(c, 7, 8.0 * G * (kk + 1));
+            k_update_x<<<nblk(G / 2), 256, 0, c->st>>>(G, kk, dptr, dy, c->U, cycle > 0 ? 1 : 0);
             c->launches++;
         }
+        iters += kk;
     }
+    c->last_iters = std::min(iters, mr);
     if (c->sticky != cudaSuccess) { const cudaError_t se = c->sticky; c->sticky = cudaSuccess; CK(c, se); }
     CK(c, cudaEventRecord(e1, c->st));
     // output
@@ -1694,6 +1726,7 @@ spp_status spp_create_strips(const spp_problem *p, int32_t nstrips, const spp_op
     if (!p || !out) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_create_strips: NULL argument");
     *out = nullptr;
     if (nstrips == 1) return spp_create(p, o, stream, out);
+    if (o && o->restart != 0) FAIL((Ctx *)nullptr, SPP_E_ARG, "row strips run FGMRES without restarts (restart = 0)");
     std::vector<int> J;
     if (nstrips < 1 || p->dim != 2 || !strip_partition(p->n, nstrips, J))
         FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_create_strips: %d strips of a %s N = %d problem", nstrips,
@@ -1735,6 +1768,7 @@ spp_status spp_create_dist(const spp_problem *local, int32_t j0, int32_t j1, voi
         return spp_create(local, o, stream, out);
     }
     if (!nccl_comm) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_create_dist: NULL NCCL communicator");
+    if (o && o->restart != 0) FAIL((Ctx *)nullptr, SPP_E_ARG, "row strips run FGMRES without restarts (restart = 0)");
     // gather every rank's [j0, j1) through a provisional strip context (its partial-sum buffer)
     std::vector<int> J0(nranks + 1, 0);
     Ctx *c = nullptr;

@@ -822,7 +822,7 @@ spp_status solve_dist(Ctx *c0, const double *f, double *u, spp_mem mem, double *
                 double *dy = c->dscal + 2 * maxit + 16;
                 DCUDA(d, cudaMemcpyAsync(dptr, hz, sizeof(double *) * iters, cudaMemcpyHostToDevice, c->st));
                 DCUDA(d, cudaMemcpyAsync(dy, hy, sizeof(double) * iters, cudaMemcpyHostToDevice, c->st));
-                k_update_x<<<red_grid(cnt / 2), 256, 0, c->st>>>(cnt, iters, dptr, dy, c->U + off);
+                k_update_x<<<red_grid(cnt / 2), 256, 0, c->st>>>(cnt, iters, dptr, dy, c->U + off, 0);
                 c->launches++;
             }
     }

@@ -236,10 +236,11 @@ __global__ void __launch_bounds__(kRedThreads) k_resid_stats(int m, long P, cons
 }
 
 // ===================================================================================== Krylov vectors
-// out = f / D (weighted) or f, partial ||out||^2
+// out = f / D (weighted) or f, partial ||out||^2; with Au != nullptr the residual f - Au in
+// place of f (the restart vector of FGMRES(m), reading R23)
 __global__ void __launch_bounds__(kRedThreads) k_rhs(int m, long P, const double *f, const double *aE,
     const double *aN, const double *rr, const double *aW, const double *aS, int weighted, double *out,
-    double *part, int j0, int nrows)
+    double *part, int j0, int nrows, const double *Au)
 {
     __shared__ double sm[32];
     double acc = 0.0;
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(kRedThreads) k_rhs(int m, long P, const double
     for (GridWalk gw(tot, m, j0); gw.ok(); gw.next()) {
         const int j = gw.j, i = gw.i;
         const long g = (long)j * P + i;
-        double v = f[g];
+        double v = Au ? f[g] - Au[g] : f[g];
         if (weighted) v /= ((aW[i] + aE[g]) + (aS[j] + aN[g])) + rr[g];
         out[g] = v;
         acc += v * v;
@@ -313,11 +314,12 @@ __global__ void __launch_bounds__(kRedThreads) k_normalize(long n2, const double
 }
 
 // x = sum_j y_j Z_j  ("construction of the solution once converged")
-__global__ void k_update_x(long n2, int k, const double *const *Z, const double *y, double *x)
+__global__ void k_update_x(long n2, int k, const double *const *Z, const double *y, double *x, int accumulate)
 {
     const long n = n2 / 2;
     for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < n; p += (long)gridDim.x * blockDim.x) {
-        double2 acc = make_double2(0.0, 0.0);
+        // x = sum_j y_j z_j, or x += ... after a restart (the oracle's order: x, then j = 0, 1, ...)
+        double2 acc = accumulate ? reinterpret_cast<const double2 *>(x)[p] : make_double2(0.0, 0.0);
         for (int j = 0; j < k; ++j) {
             const double2 a = reinterpret_cast<const double2 *>(Z[j])[p];
             acc.x += y[j] * a.x; acc.y += y[j] * a.y;

@@ -130,6 +130,27 @@ __device__ __forceinline__ void st_relaxed2_if(bool pr, double *p, double v0, do
                  "l"(__double_as_longlong(v0)), "l"(__double_as_longlong(v1)), "r"((unsigned)pr));
 }
 
+// Race-detection build (SPP_STRESS, build.py with SPP_STRESS=1): every hand-off point of the
+// sweep -- a sweeping warp's chunk start and its publication to the warp / strip below, the
+// write-back warp's slot reads, the TMA producer's issue -- first sleeps a pseudo-random
+// 0..~4 us (a hash of the launch's start clock, the block, the warp and the chunk), so the
+// producers and consumers of every edge ring, chain buffer and staging slot run in orders the
+// normal build never produces.  The results must stay bit-for-bit those of the normal build
+// (tools/stress_check.py): any missing acquire / release or a consumer reading a slot early
+// shows up as a difference.
+#ifdef SPP_STRESS
+__device__ __forceinline__ void stress_delay(unsigned long long seed, int where, int c)
+{
+    unsigned long long h = seed ^ ((unsigned long long)(blockIdx.x + 977u * blockIdx.y) << 20) ^
+                           ((unsigned long long)(threadIdx.x >> 5) << 40) ^ ((unsigned long long)where << 50) ^ (unsigned)c;
+    h ^= h >> 33; h *= 0xff51afd7ed558ccdull; h ^= h >> 33; h *= 0xc4ceb9fe1a85ec53ull; h ^= h >> 33;
+    if ((h & 3u) == 0u) __nanosleep((unsigned)((h >> 8) & 4095u));
+}
+#define SPP_STRESS_DELAY(where, c) stress_delay(stress_seed, where, c)
+#else
+#define SPP_STRESS_DELAY(where, c) ((void)0)
+#endif
+
 template <bool YFORM, bool CHAIN>
 __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const __grid_constant__ WaveMaps m)
 {
@@ -147,6 +168,11 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
     // warps 0..W-1 sweep 32-row strips; warp W+w writes back the results of warp w; warp 2W is
     // the TMA producer (lane w serves warp w)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = ((blockDim.x >> 5) - 1) / 2;
+#ifdef SPP_STRESS
+    unsigned long long stress_seed;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stress_seed));
+    stress_seed = __shfl_sync(0xffffffffu, stress_seed, 0);   // one seed per warp (warp-uniform sleeps)
+#endif
     if (threadIdx.x < WMAXW) { prod[threadIdx.x] = 0; cons[threadIdx.x] = 0; }
     if (wid < W && lane == 0)
         for (int s = 0; s < WNS; ++s) {
@@ -187,6 +213,7 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
         for (int c = 0; c < nch; ++c) {
             const int sl = c % WNS;
             if (c >= WNS) mbar_wait((unsigned)__cvta_generic_to_shared(&ebars[pw][sl]), (unsigned)(((c / WNS) - 1) & 1));
+            SPP_STRESS_DELAY(1, c);
             const unsigned bar = (unsigned)__cvta_generic_to_shared(&bars[pw][sl]);
             const unsigned dst = ring_s + (unsigned)(sl * WSLOT * 8);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -244,6 +271,7 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
                 const unsigned lo = emin <= 0 ? 0u : ((1u << emin) - 1u);
                 msk = rowmask & hi & ~lo;
             }
+            SPP_STRESS_DELAY(2, c);
             mbar_wait((unsigned)__cvta_generic_to_shared(&rbars[w][c % WNS]), (unsigned)((c / WNS) & 1));
             const double *sl = ring + (size_t)(c % WNS) * WSLOT;
             double *zp = zw - c * WCW;
@@ -291,6 +319,7 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
         // North inflow of lane 0 for the columns of this chunk (all wait loops warp-uniform: a
         // lane-divergent spin sends the shuffles below down the slow emulation path)
         SPP_TP(ta);
+        SPP_STRESS_DELAY(3, c);
         const int need = min(ncols, c * WCW + WCW);
 #ifdef EXP_NOSPIN
         if (false) {
@@ -381,6 +410,7 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
             }
             // hand the bottom row to the next strip (lane 31's pairs): branch-free predicated
             // stores on interior chunks, element-wise checks at the edges
+            SPP_STRESS_DELAY(5, c);                       // delays the hand-off stores below
             double *eo = &edge[w][0];
             double *co = CHAIN ? a.chain_buf + (long)blockIdx.y * a.chain_ld : nullptr;
             if (F) {
@@ -417,6 +447,7 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
         SPP_TP(td);
         const int done = min(ncols, max(0, c * WCW + WCW - WLAG * 31));
         __syncwarp();
+        SPP_STRESS_DELAY(4, c);
         if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(&rbars[w][c % WNS])) : "memory");
         if (lane == 31 && has_consumer)                 // release: the edge values before the count
             asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(&prod[w])), "r"(done) : "memory");

@@ -25,12 +25,12 @@ __global__ void k_resid_stats(int m, long P, const double *f, const double *Au, 
                               double *part4, long pstride, int j0, int nrows);
 __global__ void k_rhs(int m, long P, const double *f, const double *aE, const double *aN,
                       const double *rr, const double *aW, const double *aS, int weighted,
-                      double *out, double *part, int j0, int nrows);
+                      double *out, double *part, int j0, int nrows, const double *Au = nullptr);
 __global__ void k_scale(long n2, double *x, double alpha);
 __global__ void k_mgs(long n2, double *w, const double *x, const double *part_in, double *hslot,
                       const double *y, double *part_out, int nparts);
 __global__ void k_normalize(long n2, const double *w, const double *part_in, double *hslot, double *v, int nparts);
-__global__ void k_update_x(long n2, int k, const double *const *Z, const double *y, double *x);
+__global__ void k_update_x(long n2, int k, const double *const *Z, const double *y, double *x, int accumulate);
 __global__ void k_corner_rhs(int N, long P, long P0, const double *v, const double *z,
                              const double *aE, const double *aN, const double *rr, const double *aW,
                              const double *aS, const double *hb, const double *kb, int weighted,

@@ -89,7 +89,7 @@ def test_options_validated_before_any_device_work():
         for k, v in kw.items():
             setattr(o, k, v)
         return o
-    bad2d = [opts(2, restart=10), opts(2, side=spp.SPP_LEFT), opts(2, stop=spp.SPP_STOP_ABS_MAX), opts(2, tol=0.0),
+    bad2d = [opts(2, restart=-1), opts(2, restart=10, fixed_iters=20), opts(2, side=spp.SPP_LEFT), opts(2, stop=spp.SPP_STOP_ABS_MAX), opts(2, tol=0.0),
              opts(2, tol=float("nan"))]
     for o in bad2d:
         with pytest.raises(spp.SppError) as ei:
