@@ -50,7 +50,10 @@ def _args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg4", help="cfg1..cfg5, or cfg5-sweep (the five eps values as "
                     "independent problems over the ranks)")
-    ap.add_argument("--max-iters", type=int, default=100, help="cfg5-sweep: common FGMRES cap (SURVEY A19)")
+    ap.add_argument("--max-iters", type=int, default=None,
+                    help="FGMRES cap (cfg5-sweep: common cap, default 100, SURVEY A19; else the library default)")
+    ap.add_argument("--restart", type=int, default=0,
+                    help="FGMRES(m) restart length (0 = none, the paper; DESIGN.md reading R23)")
     ap.add_argument("--batch", type=int, default=16384, help="cfg1-batch: problems per GPU")
     ap.add_argument("--n", "--size", dest="n", type=int, default=None, help="override N (diagnostics only)")
     ap.add_argument("--eps", type=float, default=None)
@@ -350,7 +353,7 @@ def run_sweep(args, rank, world):
         d = [torch.from_numpy(np.ascontiguousarray(a).ravel()).to(dev) for a in (c1, c2, r, f)]
         o = spp.spp_default_options(2)
         o.tol = cfg.tol
-        o.max_iters = args.max_iters
+        o.max_iters = args.max_iters if args.max_iters is not None else 100
         jobs.append((cfg, x, y, d, torch.empty_like(d[3]), o))
 
     def step():
@@ -443,6 +446,9 @@ def run_ours(args, rank, world):
     o = spp.spp_default_options(2)
     o.stop = spp.SPP_STOP_REL_JACOBI if cfg.weighted else (spp.SPP_STOP_ABS_L2 if cfg.stop_abs else spp.SPP_STOP_REL_L2)
     o.tol = cfg.tol
+    if args.max_iters is not None:
+        o.max_iters = args.max_iters
+    o.restart = args.restart
     stream = torch.cuda.current_stream(dev)
     comm = None
     if world > 1:
@@ -569,6 +575,7 @@ def run_ours(args, rank, world):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": _workload(cfg), "N": N, "unknowns": cfg.unknowns,
                    "iters_per_solve": res.stats["iters"],
+                   **({"restart": args.restart} if args.restart else {}),
                    "mg_cycles_per_apply": [res.stats["mg_cycles_min"], res.stats["mg_cycles_max"]],
                    "time_to_solution_s": ms * 1e-3, "setup_s": res.stats["setup_s"],
                    "true_res_jacobi_rel": res.stats["true_res_jacobi_rel"],

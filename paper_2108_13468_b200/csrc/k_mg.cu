@@ -1119,23 +1119,45 @@ __global__ void __launch_bounds__(kRedThreads) k_cycle_update(int nl, long pv, l
     if (ms) { z = ms->zcur; znew = ms->znext; }        // corner graph: buffers from the device state
     double acc = 0.0;
     // z' = z + e on rows jz0 .. jz1; rho and the norm on the owned rows j0 .. j1 (a row strip
-    // also carries z' on its one-row halos; everything 1 .. nl on one GPU)
-    const long tot = (long)nl * (jz1 - jz0 + 1);
-    for (GridWalk gw(tot, nl, jz0); gw.ok(); gw.next()) {
-        const int j = gw.j, i = gw.i;
-        const long g = (long)j * pv + i, q = (long)j * pc + i;
-        const bool own = j >= j0 && j <= j1;
-        double zc = e[g];
-        if (z) zc += z[g];
-        znew[g] = zc;
-        if (!own) continue;
-        double zw = e[g - 1], ze = e[g + 1], zs = e[g - pv], zn = e[g + pv];
-        if (z) { zw += z[g - 1]; ze += z[g + 1]; zs += z[g - pv]; zn += z[g + pv]; }
-        const double Az = aW[i] * (zc - zw) + aE[q] * (zc - ze) + aS[j] * (zc - zs) + aN[q] * (zc - zn) + rr[q] * zc;
-        const double r = b[g] - Az;
-        rho[g] = scale_rho ? r * cd[q] : r;             // the next V-cycle's input (rho/D in z-form)
-        const double t = (hb[i] * kb[j]) * r;
-        acc += t * t;
+    // also carries z' on its one-row halos; everything 1 .. nl on one GPU).
+    // One block-iteration = one row segment of 2*blockDim columns starting at the ghost column 0,
+    // each thread a column pair (i0, i0+1), i0 even, with 16-byte loads and stores (the pitches
+    // are multiples of 16 doubles).  Ghost columns (0, nl+1) are written as the zeros they are.
+    auto ld2 = [](const double *p) { return *reinterpret_cast<const double2 *>(p); };
+    const int segw = 2 * blockDim.x;
+    const int nseg = (nl + 2 + segw - 1) / segw;       // columns 0 .. nl+1
+    const long nit = (long)(jz1 - jz0 + 1) * nseg;
+    for (long it = blockIdx.x; it < nit; it += gridDim.x) {
+        const int j = (int)(it / nseg) + jz0;
+        const int i0 = (int)(it % nseg) * segw + 2 * threadIdx.x;
+        if (i0 > nl) continue;
+        const long g = (long)j * pv + i0, q = (long)j * pc + i0;
+        const bool ok0 = i0 >= 1, ok1 = i0 + 1 <= nl;  // valid columns of the pair
+        double2 c = ld2(e + g);
+        if (z) { const double2 t = ld2(z + g); c.x += t.x; c.y += t.y; }
+        *reinterpret_cast<double2 *>(znew + g) = c;
+        if (j < j0 || j > j1) continue;
+        double2 s = ld2(e + g - pv), n = ld2(e + g + pv);
+        double w = e[g - 1], ea = e[g + 2];
+        if (z) {
+            const double2 zs = ld2(z + g - pv), zn = ld2(z + g + pv);
+            s.x += zs.x; s.y += zs.y; n.x += zn.x; n.y += zn.y;
+            w += z[g - 1]; ea += z[g + 2];
+        }
+        const double2 vE = ld2(aE + q), vN = ld2(aN + q), vr = ld2(rr + q), vb = ld2(b + g);
+        const double2 vW = ld2(aW + i0);
+        const double vS = aS[j];
+        const double Az0 = vW.x * (c.x - w) + vE.x * (c.x - c.y) + vS * (c.x - s.x) + vN.x * (c.x - n.x) + vr.x * c.x;
+        const double Az1 = vW.y * (c.y - c.x) + vE.y * (c.y - ea) + vS * (c.y - s.y) + vN.y * (c.y - n.y) + vr.y * c.y;
+        const double r0 = ok0 ? vb.x - Az0 : 0.0, r1 = ok1 ? vb.y - Az1 : 0.0;
+        double2 out = make_double2(r0, r1);
+        if (scale_rho) { const double2 vd = ld2(cd + q); out.x *= vd.x; out.y *= vd.y; }   // rho/D in z-form
+        *reinterpret_cast<double2 *>(rho + g) = out;
+        const double2 vh = ld2(hb + i0);
+        const double kj = kb[j];
+        const double t0 = (vh.x * kj) * r0, t1 = (vh.y * kj) * r1;
+        acc += t0 * t0;
+        acc += t1 * t1;
     }
     double v = acc;
 #pragma unroll
@@ -1144,9 +1166,9 @@ __global__ void __launch_bounds__(kRedThreads) k_cycle_update(int nl, long pv, l
     if (lane == 0) sm[wid] = v;
     __syncthreads();
     if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int k = 0; k < nwp; ++k) s += sm[k];
-        part[blockIdx.x] = s;
+        double s2 = 0.0;
+        for (int k = 0; k < nwp; ++k) s2 += sm[k];
+        part[blockIdx.x] = s2;
     }
     zero_tail(part);
 }
