@@ -352,7 +352,9 @@ static void precond_head(Ctx *c, const double *v, double *z)
     launch_lines(c, v, z);
     Level &L0 = c->lev[0];
     ProfScope ps(c, 9, 40.0 * (double)n * n);
-    k_corner_rhs<<<red_grid((long)n * n), kRedThreads, 0, c->st>>>(N, c->P, L0.pitch, v, z, c->aE, c->aN, c->rr, c->aW,
+    int nb = 0, nt = 0;
+    seg_shape(n, n, &nb, &nt);
+    k_corner_rhs<<<nb, nt, 0, c->st>>>(N, c->P, L0.pitch, v, z, c->aE, c->aN, c->rr, c->aW,
                                                         c->aS, L0.hb, L0.kb, c->weighted, c->Bc, part_slot(c, 1),
                                                         L0.rho, c->cd, c->mg_zform, 1, n);
     c->launches++;

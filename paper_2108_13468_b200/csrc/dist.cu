@@ -605,7 +605,9 @@ static spp_status precond_dist(Dist *d, int k, int *cycles, int *cap)
             continue;
         }
         const int j0 = g.J[r], j1 = g.J[r + 1] - 1;
-        k_corner_rhs<<<red_grid((long)n * (j1 - j0 + 1)), kRedThreads, 0, c->st>>>(c->N, c->P, L0.pitch, c->V[k], c->Z[k],
+        int nb = 0, nt = 0;
+        seg_shape(n, j1 - j0 + 1, &nb, &nt);
+        k_corner_rhs<<<nb, nt, 0, c->st>>>(c->N, c->P, L0.pitch, c->V[k], c->Z[k],
             c->aE, c->aN, c->rr, c->aW, c->aS, L0.hb, L0.kb, c->weighted, c->Bc, pseg(c, 1), L0.rho, c->cd, c->mg_zform,
             j0, j1);
         c->launches++;

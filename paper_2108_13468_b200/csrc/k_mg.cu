@@ -387,18 +387,34 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
                 double n1 = __shfl_up_sync(0xffffffffu, z1, 1);
                 const double2 Es = lds2(Eb + 2 * st);             // North inflow (lane 0)
                 if (lane == 0) { n0 = Es.x; n1 = Es.y; }
-                double za = fma(A1.y, z1, fma(A2.y, n0, Q.y));      // column 2st   (east one first)
-                double zc = fma(A1.x, za, fma(A2.x, n1, Q.x));      // column 2st+1
-                if (!F) {                                  // edge chunk: zero outside the block
-                    // one AND per value on the chain (the masks do not depend on it); a ternary
-                    // compiled to three dependent selects.  (Masking the operands instead keeps
-                    // the masks off the chain but costs six ANDs per step: measured slower on the
-                    // tiled levels, 6.37 -> 6.90 ms of sweeps per cfg4 solve.)
-                    const int idx = c * WCW + 2 * st - WLAG * lane;
-                    const unsigned ua = (unsigned)idx < (unsigned)ncols, uc = (unsigned)(idx + 1) < (unsigned)ncols;
-                    const long long ma = -(long long)(rvalid & ua), mc = -(long long)(rvalid & uc);
-                    za = __longlong_as_double(__double_as_longlong(za) & ma);
-                    zc = __longlong_as_double(__double_as_longlong(zc) & mc);
+                double za, zc;
+                if (CHAIN) {
+                    // exact chain (M_II): edge positions are not zeroed.  Left of the block
+                    // (idx >= ncols) and below it (rows < out_bot) nothing valid depends on them;
+                    // right of it (idx < 0) each lane's values are garbage until it reaches idx = 0,
+                    // where its East input -- the zero inflow at the block's right edge -- is set to
+                    // 0 (a select: no garbage, not even a NaN, passes it).  Write-back and hand-offs
+                    // are masked separately; strips that hand their bottom row on span whole warps.
+                    // One select per step on the chain instead of two masked values: M_II
+                    // 1.70 -> 1.53 ms per cfg4 solve (on the tiled levels it measured slower).
+                    double z1e = z1;
+                    if (!F) z1e = (c * WCW + 2 * st - WLAG * lane == 0) ? 0.0 : z1;
+                    za = fma(A1.y, z1e, fma(A2.y, n0, Q.y));         // column 2st   (east one first)
+                    zc = fma(A1.x, za, fma(A2.x, n1, Q.x));          // column 2st+1
+                } else {
+                    za = fma(A1.y, z1, fma(A2.y, n0, Q.y));
+                    zc = fma(A1.x, za, fma(A2.x, n1, Q.x));
+                    if (!F) {                              // edge chunk: zero outside the block
+                        // one AND per value on the chain (the masks do not depend on it); a ternary
+                        // compiled to three dependent selects.  (Masking the operands instead keeps
+                        // the masks off the chain but costs six ANDs per step: measured slower on the
+                        // tiled levels, 6.37 -> 6.90 ms of sweeps per cfg4 solve.)
+                        const int idx = c * WCW + 2 * st - WLAG * lane;
+                        const unsigned ua = (unsigned)idx < (unsigned)ncols, uc = (unsigned)(idx + 1) < (unsigned)ncols;
+                        const long long ma = -(long long)(rvalid & ua), mc = -(long long)(rvalid & uc);
+                        za = __longlong_as_double(__double_as_longlong(za) & ma);
+                        zc = __longlong_as_double(__double_as_longlong(zc) & mc);
+                    }
                 }
                 Z[2 * st] = za; Z[2 * st + 1] = zc;
                 z2 = za; z1 = zc;
@@ -1182,7 +1198,9 @@ void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew,
     // a row strip updates z on its one-row halos too (their e came from the neighbours)
     const int j0 = L.sdist ? L.slo : 1, j1 = L.sdist ? L.shi : L.n;
     const int jz0 = std::max(1, j0 - (L.sdist ? 1 : 0)), jz1 = std::min(L.n, j1 + (L.sdist ? 1 : 0));
-    k_cycle_update<<<red_grid((long)L.n * (jz1 - jz0 + 1)), kRedThreads, 0, c->st>>>(L.n, L.pitch, L.cpitch, z, e, znew, b,
+    int nb = 0, nt = 0;
+    seg_shape(L.n, jz1 - jz0 + 1, &nb, &nt);
+    k_cycle_update<<<nb, nt, 0, c->st>>>(L.n, L.pitch, L.cpitch, z, e, znew, b,
                                                           L.aE, L.aN, L.rr, L.aW, L.aS, L.hb, L.kb, rho, part, ms, L.cd,
                                                           c->mg_zform ? 1 : 0, jz0, jz1, j0, j1);
     c->launches++;

@@ -38,6 +38,18 @@ __device__ __forceinline__ void zero_tail(double *part)
         for (int b = gridDim.x + threadIdx.x; b < kRedBlocks; b += blockDim.x) part[b] = 0.0;
 }
 constexpr int kRedThreads = 256;
+// Launch shape of the row-segment reduction kernels (k_cycle_update, k_corner_rhs): a thread per
+// column pair of a row of n + 2 columns (ghosts included), at most kRedThreads threads per block,
+// a warp multiple; one block-iteration per row segment, at most kRedBlocks blocks.
+inline void seg_shape(int n, long rows, int *blocks, int *threads)
+{
+    int t = ((n + 2) / 2 + 31) / 32 * 32;
+    t = t < 32 ? 32 : (t > kRedThreads ? kRedThreads : t);
+    const long nseg = (n + 2 + 2L * t - 1) / (2L * t);
+    const long b = rows * nseg;
+    *threads = t;
+    *blocks = (int)(b < 1 ? 1 : (b > kRedBlocks ? kRedBlocks : b));
+}
 
 // Grid-stride walk over level nodes (i, j), i = 1..m, j = j0.. in the order p = (j - j0) m + (i - 1):
 // one division at the start, then (i, j) advance incrementally (a 64-bit division per element was

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+bash tools/ab2.sh
+cp tools/ablibs/c_reset_crhs.so paper_2108_13468_b200/lib/libspp.so
+timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/gpu_tests_c.log 2>&1; tail -2 gpurun_out/gpu_tests_c.log
