@@ -547,6 +547,59 @@ std::vector<LineChunk> plan_chain_chunks(int chain, const std::vector<double> &k
     return out;
 }
 
+// warm-up starts of chunks beginning at every line (as in plan_chain_chunks)
+static std::vector<int> warm_starts(const std::vector<double> &k)
+{
+    const int nl = (int)k.size();
+    const double target = std::log(1e-17);
+    std::vector<double> lg(nl + 1, 0.0);
+    for (int l = 0; l < nl; ++l) lg[l + 1] = lg[l] + std::log(std::max(k[l], 1e-300));
+    std::vector<int> wst(nl + 1, 0);
+    for (int f = 0, st = 0; f <= nl; ++f) {
+        while (st < f && lg[f] - lg[st + 1] <= target) ++st;
+        wst[f] = (lg[f] - lg[st] <= target) ? st : 0;
+    }
+    return wst;
+}
+// greedy chunks of lines l0..l1 whose span (warm-up + owned lines) is at most T (at least one
+// owned line each); returns their number, appends them to *out when given
+static int greedy_chunks(int chain, const std::vector<int> &wst, int l0, int l1, int T, std::vector<LineChunk> *out)
+{
+    int cnt = 0;
+    for (int f = l0; f <= l1;) {
+        const int last = std::min(l1, std::max(f, wst[f] + T - 1));
+        if (out) out->push_back({chain, f, last, wst[f]});
+        ++cnt;
+        f = last + 1;
+    }
+    return cnt;
+}
+// One GPU, both chains in one launch of `budget` CTAs (one per SM): the CTAs are split between
+// the chains so that the longest chunk, in time, is as short as possible.  A chunk's time is its
+// span in lines times the chain's per-line cost; a Y line costs ~1.2 X lines (its operand column
+// is repacked through shared memory; SPP_LINES_PROF: ~6.1k vs ~5.1k cycles per line at cfg4).
+// With the same number of CTAs per chain, the Y chunks (warm-up ~22 lines at cfg4) ran 50 lines
+// against the X chunks' 28.
+void plan_chunks_balanced(Ctx *c, const std::vector<double> &kx, const std::vector<double> &ky, int nl, int budget)
+{
+    const std::vector<int> wx = warm_starts(kx), wy = warm_starts(ky);
+    const double ycost = 1.2;
+    auto need = [&](int tau) {
+        return greedy_chunks(0, wx, 0, nl - 1, tau, nullptr) + greedy_chunks(1, wy, 0, nl - 1, std::max(1, (int)(tau / ycost)), nullptr);
+    };
+    int lo = 1, hi = (int)(2 * ycost * nl) + 2;         // need(hi) = 2 <= budget
+    while (lo < hi) {                                   // smallest tau with need(tau) <= budget
+        const int mid = (lo + hi) / 2;
+        if (need(mid) <= std::max(2, budget)) hi = mid; else lo = mid + 1;
+    }
+    c->chunks.clear();
+    greedy_chunks(0, wx, 0, nl - 1, lo, &c->chunks);
+    greedy_chunks(1, wy, 0, nl - 1, std::max(1, (int)(lo / ycost)), &c->chunks);
+    if (getenv("SPP_DEBUG_LINES"))
+        fprintf(stderr, "[spp] line chains (balanced): %zu chunks, X span <= %d, Y span <= %d lines\n", c->chunks.size(), lo,
+                std::max(1, (int)(lo / ycost)));
+}
+
 void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double> &ky, const int lo[2],
                  const int hi[2], int budget)
 {
@@ -585,8 +638,7 @@ cudaError_t setup_lines(Ctx *c)
     SPP_CUDA_TRY(cudaMemcpyAsync(c->ky.data(), c->kapY, sizeof(double) * nl, cudaMemcpyDeviceToHost, c->st));
     SPP_CUDA_TRY(cudaStreamSynchronize(c->st));
     if (c->line_lo[0] < 0) {                            // one GPU: every line, the GPU shared by both chains
-        const int lo[2] = {0, 0}, hi[2] = {nl - 1, nl - 1};
-        plan_chunks(c, c->kx, c->ky, lo, hi, c->sm_count / 2);
+        plan_chunks_balanced(c, c->kx, c->ky, nl, c->sm_count);
     } else {
         plan_chunks(c, c->kx, c->ky, c->line_lo, c->line_hi, c->sm_count);
     }
