@@ -1,7 +1,7 @@
 # Round-2 measurement: parity tests, smoke, the default bench line (cfg4, with e2e and the CPU
 # baseline), the reference arm (the oracle), the other BASELINE configs, the ncu launch list, the
 # DRAM bytes of every k_wave launch, and ncu --set full captures of the top kernels.
-O=gpurun_out/final
+O=gpurun_out/final2
 mkdir -p $O/configs
 nvidia-smi > $O/smi.txt 2>&1
 timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/gpu_tests.log 2>&1; tail -1 $O/gpu_tests.log
