@@ -816,46 +816,52 @@ struct CoarseArgs {
 // a level's shared-memory image: offsets into the block's shared array of (n+2)^2 arrays with
 // stride st = n+2 and of 1D arrays of n+2 (offsets, not pointers: the accesses stay LDS/STS and
 // the image copies into registers)
-struct CSm { int b, e, aE, aN, cd, rr, aW, aS, hb, kb, n, st; };
+struct CSm { int b, e, aE, aN, cd, rr, aW, aS, hb, kb, n, st, ca, cn; };
 extern __shared__ double coarse_sm[];
 
-__device__ __forceinline__ void cgs_sweep(const CSm L)
+__device__ __forceinline__ void cgs_sweep(const CSm L, double *q)
 {
     double *cs = coarse_sm;
+    const int n = L.n, st = L.st;
+    // the parallel part first (all threads): q = (b + aW e_W + aS e_S) / D from the old e, then
+    // the z-form recurrence z = q + ca z_E + cn z_N (ca = aE/D, cn = aN/D) by one warp
+    {
+        const double *b = cs + L.b, *e = cs + L.e, *cd = cs + L.cd;
+        for (int k = threadIdx.x; k < n * n; k += blockDim.x) {
+            const int j = k / n + 1, i = k % n + 1, s = j * st + i;
+            q[s] = ((b[s] + cs[L.aW + i] * e[s - 1]) + cs[L.aS + j] * e[s - st]) * cd[s];
+        }
+    }
+    __syncthreads();
     if (threadIdx.x < 32) {
-        const int n = L.n, st = L.st, t = threadIdx.x;
+        const int t = threadIdx.x;
         const bool act = t < n;
         const int j = n - t;
-        const double as = act ? cs[L.aS + j] : 0.0;
-        const double *b = cs + L.b, *aW = cs + L.aW, *aE = cs + L.aE, *aN = cs + L.aN, *cd = cs + L.cd;
+        const double *ca = cs + L.ca, *cn = cs + L.cn;
         double *e = cs + L.e;
-        // new values never come back through shared memory: East is this lane's previous step
-        // (0: the ghost column at i = n), North lane t-1's previous step (shuffle; lane 0: the
-        // ghost row); West and South are still old.  The stores are write-only during the sweep,
-        // and a lane's loads of old values precede, in the warp's instruction order, the store of
-        // the lane that overwrites them.  Branch-free (idle lanes read a valid dummy node and
-        // keep their value), with the operands of the next step loaded one step ahead: measured
-        // 122 instead of ~235 cycles per step (tools/ubench/sweep.cu).
+        // one warp, lane t owns row j = n - t and meets column i = n - (s - t) at step s: East is
+        // the lane's previous step (0 at the block edge), North lane t-1's previous step (shuffle;
+        // lane 0: the ghost row).  Branch-free (idle lanes read a valid dummy node and keep their
+        // value), the operands of the next step loaded after the step's shuffle.
         const int jj = act ? j : 1;
-        auto ld = [&](int ii, double &B, double &W, double &EW, double &S, double &E, double &N, double &C) {
-            const int ic = (ii >= 1 && ii <= n) ? ii : 1, q = jj * st + ic;
-            B = b[q]; W = aW[ic]; EW = e[q - 1]; S = e[q - st]; E = aE[q]; N = aN[q]; C = cd[q];
+        auto ld = [&](int ii, double &Q, double &A, double &Nc) {
+            const int ic = (ii >= 1 && ii <= n) ? ii : 1, o = jj * st + ic;
+            Q = q[o]; A = ca[o]; Nc = cn[o];
         };
-        double B, W, EW, S, E, N, C;
-        ld(n + t, B, W, EW, S, E, N, C);
+        double Q, A, Nc;
+        ld(n + t, Q, A, Nc);
         double vlast = 0.0;
         for (int s = 0; s < 2 * n - 1; ++s) {
             const int i = n - (s - t);
             const bool ok = act && i >= 1 && i <= n;
-            double Bn, Wn, EWn, Sn, En, Nn, Cn;
-            ld(i - 1, Bn, Wn, EWn, Sn, En, Nn, Cn);
             double vN = __shfl_up_sync(0xffffffffu, vlast, 1);
             if (t == 0) vN = 0.0;
-            const double v = (((B + W * EW) + as * S) + E * vlast) + N * vN;
-            const double z = v * C;
+            double Qn, An, Nn;
+            ld(i - 1, Qn, An, Nn);
+            const double z = fma(A, vlast, fma(Nc, vN, Q));
             vlast = ok ? z : vlast;
             if (ok) e[jj * st + i] = z;
-            B = Bn; W = Wn; EW = EWn; S = Sn; E = En; N = Nn; C = Cn;
+            Q = Qn; A = An; Nc = Nn;
         }
     }
     __syncthreads();
@@ -879,8 +885,8 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
     for (int l = 0; l < a.nlev; ++l) {
         const int n = a.lv[l].n, st = n + 2, A = st * st;
         S[l] = CSm{p, p + A, p + 2 * A, p + 3 * A, p + 4 * A, p + 5 * A, p + 6 * A, p + 6 * A + st, p + 6 * A + 2 * st,
-                   p + 6 * A + 3 * st, n, st};
-        p += 6 * A + 4 * st;
+                   p + 6 * A + 3 * st, n, st, p + 6 * A + 4 * st, p + 7 * A + 4 * st};
+        p += 8 * A + 4 * st;
     }
     double *rho = cs + p;
     // zero ghost rings: b, e of every level and rho (the coefficient images are fully staged)
@@ -918,6 +924,15 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
             cs[M.b + s] *= ((cs[M.aW + i] + cs[M.aE + s]) + (cs[M.aS + j] + cs[M.aN + s])) + cs[M.rr + s];
         }
     }
+    for (int l = 0; l < a.nlev; ++l) {                  // z-form couplings ca = aE/D, cn = aN/D
+        const CSm M = S[l];
+        for (int k = threadIdx.x; k < M.st * M.st; k += blockDim.x) {
+            const int j = k / M.st, i = k % M.st;
+            const bool in = i >= 1 && i <= M.n && j >= 1 && j <= M.n;
+            cs[M.ca + k] = in ? cs[M.aE + k] * cs[M.cd + k] : 0.0;
+            cs[M.cn + k] = in ? cs[M.aN + k] * cs[M.cd + k] : 0.0;
+        }
+    }
     __syncthreads();
     const int last = a.nlev - 1;
     // ---- down ----
@@ -926,7 +941,7 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
         const Wts &W = a.lv[l].w;
         const int n = F.n, sf = F.st, sc = C.st;
         if (l == 0) CTP(3);
-        cgs_sweep(F);                                                  // pre-smoothing from zero
+        cgs_sweep(F, rho);                                             // pre-smoothing from zero
         if (l == 0) CTP(4);
         {
             const double *e = cs + F.e, *b = cs + F.b;
@@ -961,7 +976,7 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
     }
     CTP(5);
     // ---- coarsest: four sweeps from zero ----
-    for (int s4 = 0; s4 < 4; ++s4) cgs_sweep(S[last]);
+    for (int s4 = 0; s4 < 4; ++s4) cgs_sweep(S[last], rho);
     CTP(6);
     // ---- up ----
     for (int l = last - 1; l >= 0; --l) {
@@ -976,7 +991,7 @@ __global__ void __launch_bounds__(256) k_coarse_vcycle(CoarseArgs a)
         }
         __syncthreads();
         if (l == 0) CTP(7);
-        cgs_sweep(F);                                                  // post-smoothing
+        cgs_sweep(F, rho);                                             // post-smoothing
         if (l == 0) CTP(8);
     }
     {   // result of level lc
@@ -1000,7 +1015,7 @@ static size_t coarse_smem(const Ctx *c, int lc)
     size_t tot = 0;
     for (int l = lc; l < c->L; ++l) {
         const size_t st = (size_t)c->lev[l].n + 2;
-        tot += 6 * st * st + 4 * st;
+        tot += 8 * st * st + 4 * st;
     }
     tot += (size_t)(c->lev[lc].n + 2) * (c->lev[lc].n + 2);
     return tot * sizeof(double);
