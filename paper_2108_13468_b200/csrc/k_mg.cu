@@ -1050,13 +1050,9 @@ bool launch_coarse_vcycle(Ctx *c, int lc, const double *R, bool rs)
 // S = diag(hbar_i kbar_j).  One CTA per RT x RT coarse tile: the S-scaled residual of the
 // (2RT+1)^2 fine nodes it needs is formed once into shared memory, then gathered.  rho is never
 // written to HBM.
-// LOW: e is the pre-smoothing sweep from zero on R (the V-cycle's order), so
-// D e = R + aE e_E + aN e_N and the residual is exactly its lower part,
-//   rho = R - A_l e = aW e(i-1,j) + aS e(i,j-1)
-// (the identity holds in exact arithmetic; computed this way it has no cancellation).  The kernel
-// then reads e alone: 8 B per fine node instead of 40 (R, e, aE, aN, r).
+// (The V-cycle itself restricts the residual of its pre-smoothing through k_restrict_low below.)
 // ------------------------------------------------------------------------------------------
-template <int RT, bool UNI, bool LOW>
+template <int RT, bool UNI>
 __global__ void __launch_bounds__(256, 7) k_resid_restrict(int nf, long pv, long pc, const double *__restrict__ e,
     const double *__restrict__ R, const double *__restrict__ aE, const double *__restrict__ aN,
     const double *__restrict__ rr, const double *__restrict__ aW, const double *__restrict__ aS,
@@ -1074,12 +1070,7 @@ __global__ void __launch_bounds__(256, 7) k_resid_restrict(int nf, long pv, long
         const int di = p % RFW, dj = p / RFW;
         const int i = fi0 + di, j = fj0 + dj;
         double v = 0.0;
-        if (LOW) {
-            if (i <= nf && j <= nf) {
-                const long g = (long)j * pv + i;
-                v = (hbf[i] * kbf[j]) * (aW[i] * e[g - 1] + aS[j] * e[g - pv]);
-            }
-        } else if (i <= nf && j <= nf) {
+        if (i <= nf && j <= nf) {
             const long g = (long)j * pv + i, q = (long)j * pc + i;
             const double ec = e[g];
             const double vW = aW[i], vE = aE[q], vS = aS[j], vN = aN[q], vr = rr[q];
@@ -1111,7 +1102,53 @@ __global__ void __launch_bounds__(256, 7) k_resid_restrict(int nf, long pv, long
     }
 }
 
-// R == nullptr: e is the pre-smoothing sweep from zero (LOW above); R is not read
+// The V-cycle's restriction of the residual of its pre-smoothing.  e is the sweep from zero on R
+// (P:1205-1209), so D e = R + aE e_E + aN e_N and the residual is exactly its lower part,
+//   rho = R - A_l e = aW e(i-1,j) + aS e(i,j-1)
+// (the identity holds in exact arithmetic; computed this way it has no cancellation): the kernel
+// reads e alone, 8 B per fine node instead of 40 (R, e, aE, aN, r).  One thread per
+// coarse node: the 4 x 4 block of e it needs (fine rows 2J-2 .. 2J+1, columns 2I-2 .. 2I+1) by
+// eight 16-byte loads -- neighbouring threads read neighbouring 32 bytes -- instead of a shared-
+// memory tile of 33 x 33 fine residuals per 16 x 16 coarse nodes with a barrier between.  The
+// arithmetic is the tile kernel's, expression for expression.
+template <bool UNI>
+__global__ void __launch_bounds__(256) k_restrict_low(int nf, long pv, const double *__restrict__ e,
+    const double *__restrict__ aW, const double *__restrict__ aS, const double *__restrict__ hbf,
+    const double *__restrict__ kbf, int nc, long pvc, const double *__restrict__ hbc, const double *__restrict__ kbc,
+    double *bc, const double *__restrict__ cdc, long pcc, int scale_out, int jc0, Wts W)
+{
+    const int I = (int)(blockIdx.x * blockDim.x + threadIdx.x) + 1, J = (int)blockIdx.y + jc0;
+    if (I > nc) return;
+    const int i0 = 2 * I - 2;
+    double ev[4][4];                                   // e(i0 + c, 2J - 2 + r)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const double *p = e + (long)(2 * J - 2 + r) * pv + i0;
+        const double2 a = *reinterpret_cast<const double2 *>(p), b = *reinterpret_cast<const double2 *>(p + 2);
+        ev[r][0] = a.x; ev[r][1] = a.y; ev[r][2] = b.x; ev[r][3] = b.y;
+    }
+    double sres[3][3];                                 // S-scaled residual at fine (i0+1+di, 2J-1+dj)
+#pragma unroll
+    for (int dj = 0; dj < 3; ++dj)
+#pragma unroll
+        for (int di = 0; di < 3; ++di) {
+            const int i = i0 + 1 + di, j = 2 * J - 1 + dj;
+            sres[dj][di] = (i <= nf && j <= nf) ? (hbf[i] * kbf[j]) * (aW[i] * ev[dj + 1][di] + aS[j] * ev[dj][di + 1]) : 0.0;
+        }
+    const double wl = UNI ? 0.5 : __ldg(W.xr + 2 * I - 1), wr = UNI ? 0.5 : __ldg(W.xl + 2 * I + 1);
+    const double wd = UNI ? 0.5 : __ldg(W.yr + 2 * J - 1), wu = UNI ? 0.5 : __ldg(W.yl + 2 * J + 1);
+    double acc = 0.0;
+#pragma unroll
+    for (int bb = -1; bb <= 1; ++bb) {
+        const double *srow = sres[bb + 1];
+        const double rs = (wl * srow[0] + srow[1]) + wr * srow[2];
+        acc += (bb == 0 ? 1.0 : (bb < 0 ? wd : wu)) * rs;
+    }
+    const double bv = acc / (hbc[I] * kbc[J]);
+    bc[(long)J * pvc + I] = scale_out ? bv * cdc[(long)J * pcc + I] : bv;   // z-form: stored as b_c / D_c
+}
+
+// R == nullptr: e is the pre-smoothing sweep from zero (k_restrict_low); R is not read
 void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e, bool rs_in, bool scale_out)
 {
     Level &F = c->lev[l], &C = c->lev[l + 1];
@@ -1122,9 +1159,17 @@ void launch_resid_restrict(Ctx *c, int l, const double *R, const double *e, bool
     const int RTn = C.n >= 128 ? 16 : 8;
     // coarse rows: this rank's strip of level l+1 when level l runs on strips
     const int jc0 = F.sdist ? C.slo : 1, jc1 = F.sdist ? C.shi : C.n;
+    if (low) {                                          // thread per coarse node, rows jc0 .. jc1
+        const int t = std::min(256, (C.n + 31) / 32 * 32);
+        const dim3 g2((C.n + t - 1) / t, jc1 - jc0 + 1);
+        auto kr = F.w.uni ? k_restrict_low<true> : k_restrict_low<false>;
+        kr<<<g2, t, 0, c->st>>>(F.n, F.pitch, e, F.aW, F.aS, F.hb, F.kb, C.n, C.pitch, C.hb, C.kb, C.b, C.cd, C.cpitch,
+                                scale_out ? 1 : 0, jc0, F.w);
+        c->launches++;
+        return;
+    }
     const dim3 grid((C.n + RTn - 1) / RTn, (jc1 - jc0 + RTn) / RTn);
-#define SPP_RR(T) (low ? (F.w.uni ? k_resid_restrict<T, true, true> : k_resid_restrict<T, false, true>) \
-                       : (F.w.uni ? k_resid_restrict<T, true, false> : k_resid_restrict<T, false, false>))<<<grid, T >= 32 ? 256 : (T >= 16 ? 256 : 128), 0, c->st>>>(F.n, F.pitch, \
+#define SPP_RR(T) (F.w.uni ? k_resid_restrict<T, true> : k_resid_restrict<T, false>)<<<grid, T >= 32 ? 256 : (T >= 16 ? 256 : 128), 0, c->st>>>(F.n, F.pitch, \
         F.cpitch, e, R, F.aE, F.aN, F.rr, F.aW, F.aS, F.hb, F.kb, C.n, C.pitch, C.hb, C.kb, C.b, C.cd, C.cpitch, \
         rs_in ? 1 : 0, scale_out ? 1 : 0, jc0, jc1, F.w)
     if (RTn == 32) SPP_RR(32);
