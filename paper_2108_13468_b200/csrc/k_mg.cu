@@ -273,15 +273,19 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
             }
             SPP_STRESS_DELAY(2, c);
             mbar_wait((unsigned)__cvta_generic_to_shared(&rbars[w][c % WNS]), (unsigned)((c / WNS) & 1));
-            const double *sl = ring + (size_t)(c % WNS) * WSLOT;
-            double *zp = zw - c * WCW;
-            double v[16];
+            // chunks with nothing to store (halo warps, the staircase ends of a tile) skip the slot
+            // reads: 16 shared-memory loads per lane and chunk that only compete with the sweeps
+            if (__any_sync(0xffffffffu, msk != 0u)) {
+                const double *sl = ring + (size_t)(c % WNS) * WSLOT;
+                double *zp = zw - c * WCW;
+                double v[16];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = YFORM ? sl[3 * WBOX + offs[e]] * sl[offs[e]] : sl[offs[e]];
+                for (int e = 0; e < 16; ++e) v[e] = YFORM ? sl[3 * WBOX + offs[e]] * sl[offs[e]] : sl[offs[e]];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                if (msk & (1u << e)) *zp = v[e];
-                zp += dwv;
+                for (int e = 0; e < 16; ++e) {
+                    if (msk & (1u << e)) *zp = v[e];
+                    zp += dwv;
+                }
             }
             __syncwarp();                               // every lane's loads of the slot consumed
             if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(&ebars[w][c % WNS])) : "memory");
