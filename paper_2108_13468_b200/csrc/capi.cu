@@ -333,7 +333,7 @@ static void launch_mii(Ctx *c, const double *v, double *z, bool scaled)
     WaveArgs a{};
     a.nl = c->n - 1; a.pv = c->P; a.pc = c->P; a.ioff = c->n; a.joff = c->n;
     a.q = v; a.z = z; a.cd = c->cd;
-    if (scaled) { a.ca = c->ya; a.cn = c->yn; }   // D z = v + aE z_E + aN z_N (y-form)
+    if (scaled) { ensure_y0(c); a.ca = c->ya; a.cn = c->yn; }   // D z = v + aE z_E + aN z_N (y-form)
     else { a.ca = c->ca; a.cn = c->cn; }          // z = (D v)/D + ca z_E + cn z_N (z-form)
     const double nn = (double)a.nl * a.nl;
     launch_wave_chain(c, a, c->N + 1, c->N + 1, scaled, 1, nn * (scaled ? 40.0 : 32.0));
@@ -933,8 +933,10 @@ spp_status setup_2d_ctx(Ctx *c, const double *c1, const double *c2, const double
     int *bad = c->flags + 200;
     CK(c, cudaMemsetAsync(bad, 0, sizeof(int), c->st));
     k_coef_1d<<<nblk(N + 1), 256, 0, c->st>>>(N, c->eps, c->wxd, c->wyd, c->aW, c->aS);
+    const int want_y = (!c->mg_zform || !c->weighted) ? 1 : 0;
+    c->y0_ok = want_y;
     k_coef_2d<<<nblk((long)mm), 256, 0, c->st>>>(N, c->P, c->eps, c->wxd, c->wyd, d1, d2, d3, c->aW,
-                                                c->aS, c->aE, c->aN, c->rr, c->ca, c->cn, c->cd, c->ya, c->yn, bad);
+                                                c->aS, c->aE, c->aN, c->rr, c->ca, c->cn, c->cd, c->ya, c->yn, want_y, bad);
     Level &L0 = c->lev[0];
     k_level0_1d<<<1, 256, 0, c->st>>>(N, c->wxd, c->wyd, c->aW, c->aS, L0.aW, L0.aS, L0.hb, L0.kb);
     c->launches += 3;

@@ -512,7 +512,7 @@ static void launch_mii_dist(Ctx *c, const Geom &g, int t, const double *v, doubl
     a.nr = a.nr_out = g.J[t + 1] - g.J[t];
     a.q = v; a.z = z; a.cd = c->cd;
     const bool scaled = !c->weighted;
-    if (scaled) { a.ca = c->ya; a.cn = c->yn; }    // D z = v + aE z_E + aN z_N (y-form)
+    if (scaled) { ensure_y0(c); a.ca = c->ya; a.cn = c->yn; }    // D z = v + aE z_E + aN z_N (y-form)
     else { a.ca = c->ca; a.cn = c->cn; }           // z = (D v)/D + ca z_E + cn z_N (z-form)
     a.ext_in = t < g.P - 1 ? c->chain + (long)g.ext_slot * c->chain_ld : nullptr;
     a.chain_last = t > g.Pb ? 1 : 0;

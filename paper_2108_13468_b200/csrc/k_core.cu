@@ -42,7 +42,7 @@ __device__ __forceinline__ void coef_at(int i, int j, double eps, const double *
 __global__ void __launch_bounds__(256, 6) k_coef_2d(int N, long P, double eps, const double *wx, const double *wy,
                           const double *c1, const double *c2, const double *r, const double *aW,
                           const double *aS, double *aE, double *aN, double *rr, double *ca,
-                          double *cn, double *cd, double *ya, double *yn, int *bad)
+                          double *cn, double *cd, double *ya, double *yn, int want_y, int *bad)
 {
     const int m = N - 1;
     const long tot = (long)m * m;
@@ -59,6 +59,9 @@ __global__ void __launch_bounds__(256, 6) k_coef_2d(int N, long P, double eps, c
         const long g = (long)j * P + i;
         aE[g] = e; aN[g] = no; rr[g] = rv;
         ca[g] = e / D; cn[g] = no / D; cd[g] = 1.0 / D;
+        // the y-form couplings (unweighted M_II, SPP_MG_YFORM) only when the mode uses them;
+        // otherwise ensure_y0 forms them on demand (the Jacobi-mode solve never does)
+        if (!want_y) continue;
         double cdE = 0.0, cdN = 0.0, t0, t1, DD;
         if (i < m) { coef_at(i + 1, j, eps, wx, wy, c1[p + 1], c2[p + 1], r[p + 1], aW, aS, t0, t1, DD); cdE = 1.0 / DD; }
         if (j < m) { coef_at(i, j + 1, eps, wx, wy, c1[p + m], c2[p + m], r[p + m], aW, aS, t0, t1, DD); cdN = 1.0 / DD; }

@@ -756,7 +756,7 @@ void launch_gs_sweep(Ctx *c, int l, const double *q, double *enew)
     WaveArgs a{};
     a.nl = L.n; a.pv = L.pitch; a.pc = L.cpitch;
     if (zf) { a.ca = l == 0 ? c->ca : L.ya; a.cn = l == 0 ? c->cn : L.yn; }   // levels >= 1 keep aE/D, aN/D in ya, yn
-    else { a.ca = L.ya; a.cn = L.yn; }
+    else { if (l == 0) ensure_y0(c); a.ca = L.ya; a.cn = L.yn; }
     a.cd = L.cd; a.z = enew; a.q = q;
     if (L.sdist) {                                  // row strip: own rows + halo rows above
         a.joff = L.slo - 1;
@@ -1330,6 +1330,16 @@ void launch_ycoef(Ctx *c, int nl, long pc, const double *aE, const double *aN, c
 {
     k_ycoef<<<gblocks((long)nl * nl), 256, 0, c->st>>>(nl, pc, aE, aN, cd, ya, yn);
     c->launches++;
+}
+
+// The global grid's y-form couplings, formed on first use when the setup skipped them (the
+// Jacobi-mode z-form solve never reads them).  Bit for bit k_coef_2d's: aE (1/D_E) with 1/D_E
+// from the same formula, and the zero ghost ring of cd at the block edges.
+void ensure_y0(Ctx *c)
+{
+    if (c->y0_ok) return;
+    launch_ycoef(c, c->N - 1, c->P, c->aE, c->aN, c->cd, c->ya, c->yn);
+    c->y0_ok = 1;
 }
 
 // Tile plan of a sweep over `rows` output rows x n columns of a level with certified halo

@@ -8,7 +8,7 @@ __global__ void k_coef_1d(int N, double eps, const double *wx, const double *wy,
 __global__ void __launch_bounds__(256, 6) k_coef_2d(int N, long P, double eps, const double *wx, const double *wy,
                           const double *c1, const double *c2, const double *r, const double *aW,
                           const double *aS, double *aE, double *aN, double *rr, double *ca,
-                          double *cn, double *cd, double *ya, double *yn, int *bad);
+                          double *cn, double *cd, double *ya, double *yn, int want_y, int *bad);
 __global__ void k_coef_level(int N, int nl, int step, long Pl, double eps, const double *lwx, const double *lwy,
                              const double *c1, const double *c2,
                              const double *r, double *aW, double *aS, double *hb, double *kb,

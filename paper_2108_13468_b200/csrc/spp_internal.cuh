@@ -263,6 +263,7 @@ struct Ctx {
     int last_iters = 0;                    // the previous solve's iterations (first batch size)
     int no_lines_tma = 0;                  // SPP_NO_LINES_TMA=1: LSU-loaded line kernel
     int mg_zform = 1;                      // corner GS sweeps in z-form (SPP_MG_YFORM=1: y-form)
+    int y0_ok = 0;                         // ya, yn of the global grid are current (ensure_y0)
     // parabolic-layer variant (c2 = 0 everywhere; NEXT-2): semi-coarsening Galerkin corner MG
     int par = 0, PL = 0;
     ParLevel plev[kMaxLevels];
@@ -293,6 +294,7 @@ double *vcycle(Ctx *c, int l, const double *R, bool rs);
 void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform, int cls, double bytes);
 long wave_chain_ctas(const Ctx *c, long rows);
 void launch_ycoef(Ctx *c, int nl, long pc, const double *aE, const double *aN, const double *cd, double *ya, double *yn);
+void ensure_y0(Ctx *c);
 cudaError_t wave_init();
 cudaError_t lines_init();
 const CUtensorMap *tmap2d(Ctx *c, const void *base, unsigned long long d0, unsigned long long d1,
