@@ -952,6 +952,11 @@ spp_status setup_2d_ctx(Ctx *c, const double *c1, const double *c2, const double
     }
     int hbad = 0;
     CK(c, cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    // one host synchronisation for the validation flags, the line chains' contraction factors and
+    // the MG levels' (their kernels run on whatever coefficients arrived; a rejected set is
+    // reported before anything is planned from them)
+    CK(c, setup_lines_launch(c));
+    CK(c, setup_mg_tiles_launch(c));
     CK(c, cudaStreamSynchronize(c->st));
     if (hbad & 1) FAIL(c, SPP_E_COEF, "coefficients violate c1 > 0, c2 >= 0, r >= 0 or are not finite (P:208-212, P:907)");
     if ((hbad & 6) == 6)
@@ -961,7 +966,7 @@ spp_status setup_2d_ctx(Ctx *c, const double *c1, const double *c2, const double
     if (c->par && c->dist) FAIL(c, SPP_E_ARG, "row strips: the parabolic-layer corner (c2 = 0) runs on one GPU only");
     if (c->par) {                                       // NEXT-2: semi-coarsening Galerkin corner MG
         if (!c->par_block) CK(c, par_alloc(c));
-        CK(c, setup_lines(c));
+        CK(c, setup_lines_plan(c));
         CK(c, par_setup(c));
         CK(c, cudaEventRecord(e1, c->st));
         CK(c, cudaEventSynchronize(e1));
@@ -971,8 +976,8 @@ spp_status setup_2d_ctx(Ctx *c, const double *c1, const double *c2, const double
         CK(c, cudaGetLastError());
         return SPP_OK;
     }
-    CK(c, setup_lines(c));
-    CK(c, setup_mg_tiles(c));
+    CK(c, setup_lines_plan(c));
+    CK(c, setup_mg_tiles_plan(c));
     CK(c, cudaEventRecord(e1, c->st));
     CK(c, cudaEventSynchronize(e1));
     cudaEventElapsedTime(&c->setup_ms, e0, e1);

@@ -610,7 +610,10 @@ void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double
     }
 }
 
-cudaError_t setup_lines(Ctx *c)
+// Setup of the line chains in two halves around one host synchronisation (setup_2d_ctx batches
+// it with the MG levels' contraction factors): the factor scans and the kappa read-back, then
+// the chunk plan.
+cudaError_t setup_lines_launch(Ctx *c)
 {
     const int n = c->n, nl = n - 1, N = c->N;
     const long per = (long)nl * n;
@@ -636,7 +639,17 @@ cudaError_t setup_lines(Ctx *c)
     c->kx.assign(nl, 0.0); c->ky.assign(nl, 0.0);
     SPP_CUDA_TRY(cudaMemcpyAsync(c->kx.data(), c->kapX, sizeof(double) * nl, cudaMemcpyDeviceToHost, c->st));
     SPP_CUDA_TRY(cudaMemcpyAsync(c->ky.data(), c->kapY, sizeof(double) * nl, cudaMemcpyDeviceToHost, c->st));
-    SPP_CUDA_TRY(cudaStreamSynchronize(c->st));
+    return cudaSuccess;
+}
+
+// after the stream has synchronised (kappa on the host)
+cudaError_t setup_lines_plan(Ctx *c)
+{
+    const int n = c->n, nl = n - 1, N = c->N;
+    const long per = (long)nl * n;
+    double *base = c->fac;
+    double *xp = base, *xe = base + per, *xa = base + 2 * per, *xb = base + 3 * per;
+    double *yp = base + 4 * per, *ye = base + 5 * per, *ya = base + 6 * per, *yb = base + 7 * per;
     if (c->line_lo[0] < 0) {                            // one GPU: every line, the GPU shared by both chains
         plan_chunks_balanced(c, c->kx, c->ky, nl, c->sm_count);
     } else {
@@ -658,6 +671,15 @@ cudaError_t setup_lines(Ctx *c)
     if (T < 32) T = 32;
     if (T > 256) T = 256;
     c->lines_threads = T;
+    return cudaSuccess;   // the chunk table's upload is stream-ordered before every use; c->chunks
+                          // changes only in the next setup, after its own synchronisation
+}
+
+cudaError_t setup_lines(Ctx *c)
+{
+    SPP_CUDA_TRY(setup_lines_launch(c));
+    SPP_CUDA_TRY(cudaStreamSynchronize(c->st));
+    SPP_CUDA_TRY(setup_lines_plan(c));
     return cudaStreamSynchronize(c->st);
 }
 

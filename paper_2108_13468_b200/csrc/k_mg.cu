@@ -318,8 +318,14 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
 #define SPP_TP(v)
 #endif
     for (int c = 0; c < nch; ++c) {
-        // interior chunks (warp-uniform test): every lane's element valid
-        const bool fast = rows_all && c * WCW - WLAG * 31 >= 0 && c * WCW + WCW - 1 < ncols;
+        // chunks without edge handling (warp-uniform test).  Tiled sweeps: every lane's element
+        // valid.  Exact chain: no chunk with columns right of the block (sweep index < 0: the first
+        // four), which must come out exactly 0 -- the zero inflow at the block's right edge; values
+        // left of it (index >= ncols) and below its rows feed only positions outside it (the
+        // write-back, the published counts and the polled chain inflow stop at ncols; the chain
+        // buffer rows have n + 32 > ncols + 15 slots), so they need nothing.
+        const bool fast = CHAIN ? c * WCW - WLAG * 31 >= 0
+                                : rows_all && c * WCW - WLAG * 31 >= 0 && c * WCW + WCW - 1 < ncols;
         // North inflow of lane 0 for the columns of this chunk (all wait loops warp-uniform: a
         // lane-divergent spin sends the shuffles below down the slow emulation path)
         SPP_TP(ta);
@@ -393,18 +399,21 @@ __global__ void __launch_bounds__((2 * WMAXW + 1) * 32) k_wave(WaveArgs a, const
                 if (lane == 0) { n0 = Es.x; n1 = Es.y; }
                 double za, zc;
                 if (CHAIN) {
-                    // exact chain (M_II): edge positions are not zeroed.  Left of the block
-                    // (idx >= ncols) and below it (rows < out_bot) nothing valid depends on them;
-                    // right of it (idx < 0) each lane's values are garbage until it reaches idx = 0,
-                    // where its East input -- the zero inflow at the block's right edge -- is set to
-                    // 0 (a select: no garbage, not even a NaN, passes it).  Write-back and hand-offs
-                    // are masked separately; strips that hand their bottom row on span whole warps.
-                    // One select per step on the chain instead of two masked values: M_II
-                    // 1.70 -> 1.53 ms per cfg4 solve (on the tiled levels it measured slower).
-                    double z1e = z1;
-                    if (!F) z1e = (c * WCW + 2 * st - WLAG * lane == 0) ? 0.0 : z1;
-                    za = fma(A1.y, z1e, fma(A2.y, n0, Q.y));         // column 2st   (east one first)
-                    zc = fma(A1.x, za, fma(A2.x, n1, Q.x));          // column 2st+1
+                    // exact chain (M_II), right of the block (first four chunks only): q = 0 there,
+                    // and with the zero initial East value and lane 0's inflow (index >= 0 always)
+                    // every value there is exactly +0 -- the block edge's zero inflow -- with
+                    // neither a mask nor a select on the step chain (the pair (idx, idx+1) has idx
+                    // even: both columns on the same side).  M_II 1.54 -> 1.50 ms per cfg4 solve
+                    // against a select of the East input at idx = 0 (and that one against per-value
+                    // masks: 1.70 -> 1.53).  On the tiled levels the same change measured slower
+                    // (mg_sweep 6.26 -> 6.51 ms per solve), so they keep the masks below.
+                    double qy = Q.y, qx = Q.x;
+                    if (!F) {
+                        const bool in = c * WCW + 2 * st - WLAG * lane >= 0;
+                        qy = in ? qy : 0.0; qx = in ? qx : 0.0;
+                    }
+                    za = fma(A1.y, z1, fma(A2.y, n0, qy));           // column 2st   (east one first)
+                    zc = fma(A1.x, za, fma(A2.x, n1, qx));           // column 2st+1
                 } else {
                     za = fma(A1.y, z1, fma(A2.y, n0, Q.y));
                     zc = fma(A1.x, za, fma(A2.x, n1, Q.x));
@@ -1392,10 +1401,11 @@ bool plan_tiles(const Ctx *c, int n, int rows, int halo, int halox, bool whole, 
     return true;
 }
 
-cudaError_t setup_mg_tiles(Ctx *c)
+// Tile plans in two halves around one host synchronisation (batched with the line chains' by
+// setup_2d_ctx): the contraction factors of every level and their read-back into c->rho_h, then
+// the certified halos and tiles.
+cudaError_t setup_mg_tiles_launch(Ctx *c)
 {
-    const Tune &T = c->tune;
-    const int Wt = std::max(1, std::min(T.gs_warps, c->mg_zform ? WMAXW : 4));   // 5 warps only fit in z-form
     const size_t S = (size_t)c->L * kRedBlocks;
     for (int l = 0; l < c->L; ++l) {
         double *p = c->part + (size_t)l * kRedBlocks;
@@ -1403,9 +1413,17 @@ cudaError_t setup_mg_tiles(Ctx *c)
                                                            c->lev[l].aN, c->lev[l].cd, p, p + S, p + 2 * S);
         c->launches++;
     }
-    std::vector<double> h(3 * S);
-    SPP_CUDA_TRY(cudaMemcpyAsync(h.data(), c->part, sizeof(double) * 3 * S, cudaMemcpyDeviceToHost, c->st));
-    SPP_CUDA_TRY(cudaStreamSynchronize(c->st));
+    c->rho_h.assign(3 * S, 0.0);
+    SPP_CUDA_TRY(cudaMemcpyAsync(c->rho_h.data(), c->part, sizeof(double) * 3 * S, cudaMemcpyDeviceToHost, c->st));
+    return cudaSuccess;
+}
+
+cudaError_t setup_mg_tiles_plan(Ctx *c)
+{
+    const Tune &T = c->tune;
+    const int Wt = std::max(1, std::min(T.gs_warps, c->mg_zform ? WMAXW : 4));   // 5 warps only fit in z-form
+    const size_t S = (size_t)c->L * kRedBlocks;
+    const std::vector<double> &h = c->rho_h;
     for (int l = 0; l < c->L; ++l) {
         Level &L = c->lev[l];
         double rho = 0.0, gy = 0.0, gx = 0.0;
@@ -1443,6 +1461,13 @@ cudaError_t setup_mg_tiles(Ctx *c)
         if (!plan_tiles(c, n, n, hy, hx, true, L)) L.tile_warps = 0;   // no tiling: exact chain
     }
     return cudaSuccess;
+}
+
+cudaError_t setup_mg_tiles(Ctx *c)
+{
+    SPP_CUDA_TRY(setup_mg_tiles_launch(c));
+    SPP_CUDA_TRY(cudaStreamSynchronize(c->st));
+    return setup_mg_tiles_plan(c);
 }
 
 }  // namespace spp

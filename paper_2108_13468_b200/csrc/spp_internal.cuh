@@ -264,6 +264,7 @@ struct Ctx {
     int no_lines_tma = 0;                  // SPP_NO_LINES_TMA=1: LSU-loaded line kernel
     int mg_zform = 1;                      // corner GS sweeps in z-form (SPP_MG_YFORM=1: y-form)
     int y0_ok = 0;                         // ya, yn of the global grid are current (ensure_y0)
+    std::vector<double> rho_h;             // setup: the levels' contraction partials (host copy)
     // parabolic-layer variant (c2 = 0 everywhere; NEXT-2): semi-coarsening Galerkin corner MG
     int par = 0, PL = 0;
     ParLevel plev[kMaxLevels];
@@ -282,6 +283,8 @@ bool strip_partition(int N, int P, std::vector<int> &J);
 bool check_partition(int N, const std::vector<int> &J, int *Pb, std::string *why);
 cudaError_t setup_levels(Ctx *c, const double *c1, const double *c2, const double *r);
 cudaError_t setup_lines(Ctx *c);
+cudaError_t setup_lines_launch(Ctx *c);
+cudaError_t setup_lines_plan(Ctx *c);
 void plan_chunks(Ctx *c, const std::vector<double> &kx, const std::vector<double> &ky, const int lo[2],
                  const int hi[2], int budget);
 std::vector<LineChunk> plan_chain_chunks(int chain, const std::vector<double> &k, int l0, int l1, int budget);
@@ -304,6 +307,8 @@ void launch_cycle_update(Ctx *c, const double *z, const double *e, double *znew,
                          double *part, const MGState *ms = nullptr);
 void launch_lines(Ctx *c, const double *v, double *z);
 cudaError_t setup_mg_tiles(Ctx *c);
+cudaError_t setup_mg_tiles_launch(Ctx *c);
+cudaError_t setup_mg_tiles_plan(Ctx *c);
 cudaError_t par_alloc(Ctx *c);
 cudaError_t par_setup(Ctx *c);
 int par_corner_solve(Ctx *c, double b0sq, int *cap_hit, cudaError_t *err);
