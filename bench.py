@@ -32,6 +32,10 @@ import spp_inputs as si  # noqa: E402
 BASELINE = json.loads((ROOT / "BASELINE.json").read_text())
 METRIC = BASELINE["metric"]
 UNIT = "unknowns/s"
+# Test hook (tests/test_gpu_dist_proc.py): every rank of a torchrun job on cuda:0 with gloo as the
+# process group, so the row-strip branch of this file runs on a one-GPU box (with SPP_NCCL_LIB
+# pointing at the tests' mock transport).  A functional check, never a measurement.
+SHARED_GPU = os.environ.get("SPP_BENCH_SHARED_GPU", "") == "1"
 
 
 def _peaks():
@@ -303,6 +307,8 @@ def max_over_ranks(ms, world, device):
     if world <= 1:
         return ms
     import torch
+    if torch.distributed.get_backend() == "gloo":
+        device = "cpu"
     t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     return float(t.item())
@@ -430,7 +436,7 @@ def run_ours(args, rank, world):
     import torch
     import paper_2108_13468_b200 as spp
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    dev = torch.device("cuda", 0 if SHARED_GPU else int(os.environ.get("LOCAL_RANK", "0")))
     torch.cuda.set_device(dev)
     cfg = si.config(args.config, N=args.n, eps=args.eps)
     N, m = cfg.N, cfg.N - 1
@@ -581,7 +587,9 @@ def run_ours(args, rank, world):
                    "true_res_jacobi_rel": res.stats["true_res_jacobi_rel"],
                    "l2": "inputs larger than L2 (each grid function 134 MB > 126 MB L2)",
                    "parallelism": (f"row strips over {world} GPUs (NCCL; rows [{j0},{j1}) on rank 0; "
-                                   f"{info['strip_levels']} corner levels on strips)") if world > 1 else "single GPU"},
+                                   f"{info['strip_levels']} corner levels on strips)"
+                                   + ("; SHARED-GPU FUNCTIONAL CHECK, NOT A MEASUREMENT" if SHARED_GPU else ""))
+                                  if world > 1 else "single GPU"},
         "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "traffic_source": "profiles/traffic.json (ncu --set full capture of this kernel class)"
@@ -610,7 +618,7 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        backend = "nccl" if torch.cuda.is_available() and not SHARED_GPU else "gloo"
         if backend == "nccl":
             torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         dist.init_process_group(backend)
