@@ -75,3 +75,23 @@ def test_bench_row_strips_under_torchrun(mock_env):
     assert d["exchange"]["blocks_per_solve"] > 0
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
     assert d["config"]["true_res_jacobi_rel"] <= 1e-8
+
+
+def test_real_nccl_resolves_and_creates_a_communicator():
+    """The real libnccl (torch's, found by the binding) through the library's run-time loader:
+    every entry point dist.cu needs resolves, and a one-rank communicator is created and
+    destroyed.  (In a subprocess: the loader caches one NCCL per process, and the tests above
+    run with the mock.)"""
+    code = ("import torch, paper_2108_13468_b200 as spp\n"
+            "torch.cuda.set_device(0)\n"
+            "spp._nccl_env()\n"
+            "import os; print('lib', os.environ.get('SPP_NCCL_LIB'))\n"
+            "uid = spp.nccl_unique_id()\n"
+            "comm = spp.nccl_comm_create(uid, 1, 0)\n"
+            "assert comm\n"
+            "spp.nccl_comm_destroy(comm)\n"
+            "print('REAL NCCL OK')\n")
+    env = {k: v for k, v in os.environ.items() if k not in ("SPP_NCCL_LIB", "SPP_BENCH_SHARED_GPU")}
+    p = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0 and "REAL NCCL OK" in p.stdout, (p.stdout[-1000:], p.stderr[-2000:])
+    assert "mock" not in p.stdout
