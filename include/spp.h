@@ -52,7 +52,9 @@ typedef enum {
     SPP_E_PIVOT = -4,       /* zero / non-finite Thomas pivot                          */
     SPP_E_MG_CAP = -5,      /* corner MG hit mg_max_cycles in strict mode                      */
     SPP_E_CUDA = -6,        /* CUDA runtime error, or no usable device                         */
-    SPP_E_NCCL = -7,
+    SPP_E_NCCL = -7,        /* NCCL cannot be loaded, a call or the communicator failed, or an
+                               exchange did not complete within SPP_NCCL_TIMEOUT_S seconds
+                               (default 600): a peer is gone or out of step         */
     SPP_E_NOMEM = -8,       /* device or host allocation failed                                */
     SPP_E_STATE = -9,       /* call not valid in this context state                            */
     SPP_E_NONFINITE = -10   /* NaN/Inf in the Krylov recurrence (beta or a Hessenberg entry):

@@ -17,6 +17,8 @@ _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "lib" / "libspp.so"
 
 SPP_OK, SPP_NOT_CONVERGED = 0, 1
+(SPP_E_ARG, SPP_E_MESH, SPP_E_COEF, SPP_E_PIVOT, SPP_E_MG_CAP, SPP_E_CUDA, SPP_E_NCCL, SPP_E_NOMEM, SPP_E_STATE,
+ SPP_E_NONFINITE) = range(-1, -11, -1)
 SPP_HOST, SPP_DEVICE = 0, 1
 SPP_STOP_REL_JACOBI, SPP_STOP_REL_L2, SPP_STOP_ABS_L2, SPP_STOP_ABS_MAX = 0, 1, 2, 3
 SPP_RIGHT_FLEXIBLE, SPP_LEFT = 0, 1

@@ -19,6 +19,8 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -229,6 +231,7 @@ struct NcclApi {
     ncclResult_t (*destroy)(ncclComm_t);
     ncclResult_t (*count)(const ncclComm_t, int *);
     ncclResult_t (*urank)(const ncclComm_t, int *);
+    ncclResult_t (*asyncerr)(ncclComm_t, ncclResult_t *);     // optional (failure detection)
 };
 
 // NCCL is resolved at run time: SPP_NCCL_LIB if set (the binding points it at torch's libnccl),
@@ -255,6 +258,7 @@ static const NcclApi *nccl_api(std::string *why)
         SPP_SYM(init, "ncclCommInitRank") SPP_SYM(destroy, "ncclCommDestroy") SPP_SYM(count, "ncclCommCount")
         SPP_SYM(urank, "ncclCommUserRank")
 #undef SPP_SYM
+        if (ok) *(void **)&api.asyncerr = dlsym(h, "ncclCommGetAsyncError");
         if (!h) err = std::string("cannot load libnccl.so.2: ") + (dlerror() ? dlerror() : "?");
         state = ok ? 1 : -1;
     }
@@ -355,6 +359,11 @@ spp_status exchange_rows(Dist *d, const std::vector<Xfer> &xs)
     const ncclResult_t rc2 = api->gend();
     if (rc == ncclSuccess) rc = rc2;
     if (rc != ncclSuccess) return dfail(d, SPP_E_NCCL, std::string("NCCL exchange: ") + api->errstr(rc));
+    if (api->asyncerr) {                               // a failure NCCL has already seen (dead peer, network)
+        ncclResult_t ar = ncclSuccess;
+        if (api->asyncerr((ncclComm_t)d->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress)
+            return dfail(d, SPP_E_NCCL, std::string("NCCL asynchronous error: ") + api->errstr(ar));
+    }
     for (size_t k = 0; k < xs.size(); ++k) {
         const Xfer &x = xs[k];
         if (x.dst != me || contig(x)) continue;
@@ -383,17 +392,41 @@ spp_status exchange_rows(Dist *d, const std::vector<Xfer> &xs)
 static inline double *pslot(Ctx *c, int k) { return c->part + (size_t)k * c->nparts * kRedBlocks; }
 static inline double *pseg(Ctx *c, int k) { return pslot(c, k) + (size_t)c->rank * kRedBlocks; }
 
-static cudaError_t fetch_sum_all(Ctx *c, int k, double *out)
+// Wait for a stream on the host.  Loopback: a plain synchronise.  NCCL: the stream holds
+// sends / receives that never complete when a peer has died or left the collective order, so
+// poll it, ask NCCL for an asynchronous error now and then, and give up after
+// SPP_NCCL_TIMEOUT_S seconds (default 600) with SPP_E_NCCL instead of hanging (SURVEY 5,
+// failure detection; no recovery: the caller destroys the context).
+static spp_status dist_wait(Dist *d, cudaStream_t st)
+{
+    if (d->me < 0) { DCUDA(d, cudaStreamSynchronize(st)); return SPP_OK; }
+    const NcclApi *api = nccl_api(nullptr);
+    static const double limit = [] { const char *e = getenv("SPP_NCCL_TIMEOUT_S"); const double v = e ? atof(e) : 0.0; return v > 0.0 ? v : 600.0; }();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned long spins = 1;; ++spins) {
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e == cudaSuccess) return SPP_OK;
+        if (e != cudaErrorNotReady) return dfail(d, SPP_E_CUDA, std::string("stream wait: ") + cudaGetErrorString(e));
+        if ((spins & 0xfff) != 0) continue;
+        if (api && api->asyncerr) {
+            ncclResult_t ar = ncclSuccess;
+            if (api->asyncerr((ncclComm_t)d->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress)
+                return dfail(d, SPP_E_NCCL, std::string("NCCL asynchronous error: ") + api->errstr(ar));
+        }
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit)
+            return dfail(d, SPP_E_NCCL, "timeout waiting for an exchange (SPP_NCCL_TIMEOUT_S): a peer is gone or out of step");
+    }
+}
+
+static spp_status fetch_sum_all(Dist *d, Ctx *c, int k, double *out)
 {
     const int cnt = c->nparts * kRedBlocks;
-    cudaError_t e = cudaMemcpyAsync(c->hpin, pslot(c, k), sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->st);
-    if (e != cudaSuccess) return e;
-    e = cudaStreamSynchronize(c->st);
-    if (e != cudaSuccess) return e;
+    DCUDA(d, cudaMemcpyAsync(c->hpin, pslot(c, k), sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->st));
+    DTRY(dist_wait(d, c->st));
     double s = 0.0;
     for (int i = 0; i < cnt; ++i) s += c->hpin[i];
     *out = s;
-    return cudaSuccess;
+    return SPP_OK;
 }
 
 // Geometry + the strips' level plans, after the (replicated) setup.  Identical on every rank:
@@ -618,7 +651,7 @@ static spp_status precond_dist(Dist *d, int k, int *cycles, int *cap)
     DTRY(exchange_rows(d, xs));
     Ctx *lead = d->cx[0];
     double b0sq = 0.0;
-    DCUDA(d, fetch_sum_all(lead, 1, &b0sq));
+    DTRY(fetch_sum_all(d, lead, 1, &b0sq));
     // stationary V-cycle iteration (reading R6): exactly corner_solve's decisions
     const double b0 = std::sqrt(b0sq);
     double res = b0;
@@ -647,7 +680,7 @@ static spp_status precond_dist(Dist *d, int k, int *cycles, int *cap)
         ++cyc;
         if (fixed <= 0) {
             double s = 0.0;
-            DCUDA(d, fetch_sum_all(lead, 0, &s));
+            DTRY(fetch_sum_all(d, lead, 0, &s));
             res = std::sqrt(s);
         }
     }
@@ -707,7 +740,7 @@ spp_status solve_dist(Ctx *c0, const double *f, double *u, spp_mem mem, double *
     xf_partials(g, xs, 0, 1);
     DTRY(exchange_rows(d, xs));
     double bsq = 0.0;
-    DCUDA(d, fetch_sum_all(lead, 0, &bsq));
+    DTRY(fetch_sum_all(d, lead, 0, &bsq));
     const double beta = std::sqrt(bsq);
     if (!std::isfinite(beta)) return dfail(d, SPP_E_NONFINITE, "||W f|| is not finite (NaN/Inf in the right-hand side)");
     std::vector<double> H((size_t)(maxit + 1) * (maxit + 1), 0.0), cs(maxit + 1), sn(maxit + 1), gg(maxit + 2, 0.0),
@@ -780,7 +813,7 @@ spp_status solve_dist(Ctx *c0, const double *f, double *u, spp_mem mem, double *
                     c->launches++;
                 }
             DCUDA(d, cudaMemcpyAsync(lead->hpin, lead->dscal, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, lead->st));
-            DCUDA(d, cudaStreamSynchronize(lead->st));
+            DTRY(dist_wait(d, lead->st));
             double *h = &H[(size_t)k * (maxit + 1)];
             for (int j = 0; j <= k + 1; ++j) {
                 h[j] = lead->hpin[j];
@@ -869,7 +902,7 @@ spp_status solve_dist(Ctx *c0, const double *f, double *u, spp_mem mem, double *
         xf_partials(g, xs, 0, 4);
         DTRY(exchange_rows(d, xs));
         double s4[4];
-        for (int a = 0; a < 4; ++a) DCUDA(d, fetch_sum_all(lead, a, &s4[a]));
+        for (int a = 0; a < 4; ++a) DTRY(fetch_sum_all(d, lead, a, &s4[a]));
         st->true_res_l2_rel = s4[2] > 0 ? std::sqrt(s4[0] / s4[2]) : 0.0;
         st->true_res_jacobi_rel = s4[3] > 0 ? std::sqrt(s4[1] / s4[3]) : 0.0;
         st->iters = iters; st->converged = converged;

@@ -1,4 +1,4 @@
-// TEST INFRASTRUCTURE ONLY: a stand-in for the ten NCCL entry points spp_create_dist uses
+// TEST INFRASTRUCTURE ONLY: a stand-in for the NCCL entry points spp_create_dist uses
 // (csrc/dist.cu nccl_api), so that the one-strip-per-PROCESS path can be exercised on a box with a
 // single GPU, where the real NCCL refuses two ranks on one device.  The library loads it only when
 // SPP_NCCL_LIB points at it (tests/test_gpu_dist_proc.py); nothing in the product links it.
@@ -78,6 +78,8 @@ static ncclResult_t run_ops(MockComm *c, std::vector<Op> &ops)
         if (cudaStreamSynchronize(o.st) != cudaSuccess) return 2;
     const int P = c->nranks;
     auto t_last = std::chrono::steady_clock::now();
+    const char *te = getenv("SPP_MOCK_NCCL_TIMEOUT_S");
+    const double limit = te && atof(te) > 0.0 ? atof(te) : 120.0;
     for (;;) {
         bool all = true, moved = false;
         std::vector<char> busy_s(P, 0), busy_r(P, 0);   // an earlier unfinished op of the same pair goes first
@@ -110,8 +112,8 @@ static ncclResult_t run_ops(MockComm *c, std::vector<Op> &ops)
         const auto now = std::chrono::steady_clock::now();
         if (moved) t_last = now;
         else {
-            if (std::chrono::duration<double>(now - t_last).count() > 120.0) {
-                fprintf(stderr, "[mock_nccl] rank %d: no progress for 120 s (unmatched send/recv?)\n", c->rank);
+            if (std::chrono::duration<double>(now - t_last).count() > limit) {
+                fprintf(stderr, "[mock_nccl] rank %d: no progress for %.0f s (unmatched send/recv?)\n", c->rank, limit);
                 return 2;
             }
             std::this_thread::sleep_for(std::chrono::microseconds(50));
@@ -178,6 +180,8 @@ ncclResult_t ncclCommDestroy(ncclComm_t c)
 
 ncclResult_t ncclCommCount(const ncclComm_t c, int *n) { if (!c || !n) return 4; *n = c->nranks; return 0; }
 ncclResult_t ncclCommUserRank(const ncclComm_t c, int *r) { if (!c || !r) return 4; *r = c->rank; return 0; }
+
+ncclResult_t ncclCommGetAsyncError(ncclComm_t c, ncclResult_t *e) { if (!c || !e) return 4; *e = 0; return 0; }
 
 const char *ncclGetErrorString(ncclResult_t r)
 {

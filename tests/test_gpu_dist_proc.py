@@ -95,3 +95,13 @@ def test_real_nccl_resolves_and_creates_a_communicator():
     p = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
     assert p.returncode == 0 and "REAL NCCL OK" in p.stdout, (p.stdout[-1000:], p.stderr[-2000:])
     assert "mock" not in p.stdout
+
+
+def test_lost_peer_is_an_error_not_a_hang(mock_env):
+    """Failure detection: a rank that leaves before the solve makes the other's solve
+    return SPP_E_NCCL (the transport's timeout here; over the real NCCL the library's own
+    stream-wait timeout SPP_NCCL_TIMEOUT_S and ncclCommGetAsyncError polling) instead of hanging."""
+    env = dict(mock_env, SPP_MOCK_NCCL_TIMEOUT_S="5", SPP_NCCL_TIMEOUT_S="20")
+    p = _torchrun(2, ["tests/dist_fail_worker.py"], env, timeout=240)
+    assert "LOST PEER DETECTED" in p.stdout, (p.stdout[-2000:], p.stderr[-3000:])
+    assert "UNEXPECTED" not in p.stdout
