@@ -10,6 +10,8 @@
 #include <cstring>
 #include <new>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "dist.cuh"
 #include "kernels.cuh"
 
@@ -40,8 +42,21 @@ static const char *kProfNames[SPP_PROF_CLASSES] = {"spmv", "sweep_I", "lines_XY"
                                                    "mg_resid_restrict", "mg_prolong", "mg_update",
                                                    "krylov_vec", "setup", "other", "mg_coarse", "exchange"};
 
+// NVTX ranges (tracing): SPP_NVTX=1 names every launch class and the setup / solve
+// calls on the host timeline of a tracing tool (nvtx3 is header-only and does nothing unless a
+// tool is attached).  With the iteration graphs the ranges bracket the capture, not the replay:
+// trace with SPP_NO_GRAPH=1 for per-launch ranges.
+static bool nvtx_on()
+{
+    static const bool on = [] { const char *e = getenv("SPP_NVTX"); return e && *e && *e != '0'; }();
+    return on;
+}
+NvtxScope::NvtxScope(const char *name) : on(nvtx_on()) { if (on) nvtxRangePushA(name); }
+NvtxScope::~NvtxScope() { if (on) nvtxRangePop(); }
+
 ProfScope::ProfScope(Ctx *c_, int cls_, double bytes_) : c(c_), cls(cls_), bytes(bytes_)
 {
+    if (nvtx_on() && cls >= 0 && cls < SPP_PROF_CLASSES) { nvtxRangePushA(kProfNames[cls]); nv = true; }
     if (!c || !(c->prof_on & (1 << cls))) { c = nullptr; return; }
     if (c->ev_used + 2 > c->ev_pool.size()) {
         for (int k = 0; k < 64; ++k) {
@@ -55,6 +70,7 @@ ProfScope::ProfScope(Ctx *c_, int cls_, double bytes_) : c(c_), cls(cls_), bytes
 }
 ProfScope::~ProfScope()
 {
+    if (nv) nvtxRangePop();
     if (!c) return;
     cudaEvent_t b = c->ev_pool[c->ev_used++];
     cudaEventRecord(b, c->st);
@@ -993,6 +1009,7 @@ extern "C" {
 spp_status spp_setup(spp_ctx *cx, const double *c1, const double *c2, const double *r, spp_mem mem)
 {
     Ctx *c = (Ctx *)cx;
+    NvtxScope nvs("spp_setup");
     if (!c) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_setup: NULL context");
     if (!c1 || !r || (c->dim == 2 && !c2)) FAIL(c, SPP_E_ARG, "spp_setup: NULL coefficient array");
     if (c->dim == 1) return (spp_status)setup_1d(c, c1, r, mem);
@@ -1346,6 +1363,7 @@ spp_status spp_solve(spp_ctx *cx, const double *f, double *u, spp_mem mem, doubl
                      spp_stats *st)
 {
     Ctx *c = (Ctx *)cx;
+    NvtxScope nvs("spp_solve");
     if (!c) FAIL((Ctx *)nullptr, SPP_E_ARG, "spp_solve: NULL context");
     if (!f) FAIL(c, SPP_E_ARG, "spp_solve: NULL rhs");
     if (c->dim == 1) return (spp_status)solve_1d_abi(c, f, u, mem, hist, hcap, st);

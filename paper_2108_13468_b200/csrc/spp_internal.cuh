@@ -341,9 +341,16 @@ __device__ __forceinline__ double interp_w(const double *ec, long Pc, int i, int
 // profiling helpers
 void prof_collect(Ctx *c);
 struct ProfScope {
-    Ctx *c; int cls; double bytes; cudaEvent_t a = nullptr;
+    Ctx *c; int cls; double bytes; cudaEvent_t a = nullptr; bool nv = false;
     ProfScope(Ctx *c_, int cls_, double bytes_);
     ~ProfScope();
+};
+// NVTX range for a host-side phase (SPP_NVTX=1; no cost otherwise): spp_setup, spp_solve, and one
+// range per launch class from ProfScope (tracing)
+struct NvtxScope {
+    bool on;
+    explicit NvtxScope(const char *name);
+    ~NvtxScope();
 };
 
 }  // namespace spp
