@@ -694,24 +694,50 @@ void launch_wave_chain(Ctx *c, WaveArgs a, long rows_v, long rows_c, bool yform,
 // of the y-form recurrence of a GS sweep from e' (the parallel W/S part), fused with the
 // prolongation and coarse-grid correction; e' itself is never stored.
 
+// One block-iteration = one row segment of 2*blockDim columns starting at the ghost column 0; each
+// thread owns a column pair (i0, i0+1), i0 even: 16-byte loads of b, 1/D, aW and of the South
+// row of e, one 16-byte store, and the interpolation's branch on the parity of i resolved at
+// compile time (one node per thread had the lanes of a warp alternate between its branches).
+// The arithmetic per node is unchanged.
 template <bool UNI>
 __global__ void __launch_bounds__(256) k_gs_prep(int nl, long pv, const double *__restrict__ e,
     const double *__restrict__ ec, long pcv, const double *__restrict__ b,
     const double *__restrict__ aW, const double *__restrict__ aS, double *g,
     const double *__restrict__ cd, long pc, int bscaled, int j0, int j1, Wts W)
 {
-    const long tot = (long)nl * (j1 - j0 + 1);         // rows j0 .. j1 of the level
-    for (GridWalk gw(tot, nl, j0); gw.ok(); gw.next()) {
-        const int j = gw.j, i = gw.i;
-        const long v = (long)j * pv + i;
-        double ew = e[v - 1], es = e[v - pv];
+    auto ld2 = [](const double *p) { return *reinterpret_cast<const double2 *>(p); };
+    const int segw = 2 * blockDim.x;
+    const int nseg = (nl + 1 + segw - 1) / segw;        // columns 0 .. nl
+    const long nit = (long)(j1 - j0 + 1) * nseg;        // rows j0 .. j1 of the level
+    for (long it = blockIdx.x; it < nit; it += gridDim.x) {
+        const int j = (int)(it / nseg) + j0;
+        const int i0 = (int)(it % nseg) * segw + 2 * threadIdx.x;
+        if (i0 > nl) continue;
+        const bool ok0 = i0 >= 1, ok1 = i0 + 1 <= nl;   // valid columns of the pair
+        const long v = (long)j * pv + i0;
+        const double2 es2 = ld2(e + v - pv);            // e(i0, j-1), e(i0+1, j-1)
+        double ew0 = ok0 ? e[v - 1] : 0.0, ew1 = e[v];  // e(i0-1, j), e(i0, j)
+        double es0 = es2.x, es1 = es2.y;
         if (ec) {
-            ew += (i > 1) ? interp_w<UNI>(ec, pcv, i - 1, j, W) : 0.0;
-            es += (j > 1) ? interp_w<UNI>(ec, pcv, i, j - 1, W) : 0.0;
+            ew0 += (i0 > 1) ? interp_p<UNI, true>(ec, pcv, i0 - 1, j, W) : 0.0;
+            es0 += (j > 1) ? interp_p<UNI, false>(ec, pcv, i0, j - 1, W) : 0.0;
+            ew1 += (i0 > 0) ? interp_p<UNI, false>(ec, pcv, i0, j, W) : 0.0;
+            es1 += (j > 1) ? interp_p<UNI, true>(ec, pcv, i0 + 1, j - 1, W) : 0.0;
         }
-        if (!cd) { g[v] = (b[v] + aW[i] * ew) + aS[j] * es; continue; }
-        const double dinv = cd[(long)j * pc + i];      // z-form sweeps take g / D
-        g[v] = bscaled ? b[v] + (aW[i] * ew + aS[j] * es) * dinv : ((b[v] + aW[i] * ew) + aS[j] * es) * dinv;
+        const double2 vb = ld2(b + v), vW = ld2(aW + i0);
+        const double vS = aS[j];
+        double2 out;
+        if (!cd) {
+            out.x = (vb.x + vW.x * ew0) + vS * es0;
+            out.y = (vb.y + vW.y * ew1) + vS * es1;
+        } else {
+            const double2 dinv = ld2(cd + (long)j * pc + i0);   // z-form sweeps take g / D
+            out.x = bscaled ? vb.x + (vW.x * ew0 + vS * es0) * dinv.x : ((vb.x + vW.x * ew0) + vS * es0) * dinv.x;
+            out.y = bscaled ? vb.y + (vW.y * ew1 + vS * es1) * dinv.y : ((vb.y + vW.y * ew1) + vS * es1) * dinv.y;
+        }
+        if (ok0 && ok1) *reinterpret_cast<double2 *>(g + v) = out;
+        else if (ok0) g[v] = out.x;
+        else if (ok1) g[v + 1] = out.y;
     }
 }
 
@@ -749,7 +775,10 @@ void launch_gs_prep(Ctx *c, int l, const double *b, const double *eold, const do
     const int j0 = L.sdist ? L.slo : 1, j1 = L.sdist ? L.shi : L.n;
     ProfScope ps(c, 5, (double)L.n * (j1 - j0 + 1) * (zf ? 32.0 : 24.0));
     auto kp = L.w.uni ? k_gs_prep<true> : k_gs_prep<false>;
-    kp<<<gblocks((long)L.n * (j1 - j0 + 1)), 256, 0, c->st>>>(L.n, L.pitch, eold, ec,
+    // a thread per column pair; a block no wider than a row needs (the small levels)
+    const int nt = std::max(32, std::min(256, ((L.n + 2) / 2 + 31) / 32 * 32));
+    const long pairs = (long)(j1 - j0 + 1) * (((L.n + 1 + 2 * nt - 1) / (2 * nt)) * (long)nt);
+    kp<<<(int)std::max(1L, std::min((pairs + nt - 1) / nt, 148L * 16)), nt, 0, c->st>>>(L.n, L.pitch, eold, ec,
         ec ? c->lev[l + 1].pitch : 0, b, L.aW, L.aS, L.g, zf ? L.cd : nullptr, L.cpitch, bscaled ? 1 : 0, j0, j1, L.w);
     c->launches++;
     dbg_sync(c, "k_gs_prep");

@@ -338,6 +338,27 @@ __device__ __forceinline__ double interp_w(const double *ec, long Pc, int i, int
     return yl * (xl * r0[0] + xr * r0[1]) + yr * (xl * r0[Pc] + xr * r0[Pc + 1]);
 }
 
+// interp_w with the parity of i known at compile time (a thread that owns a column pair (i0,
+// i0+1), i0 even, knows it; the parity of j is uniform over a row): the same expressions, so the
+// same bits, without the lane-alternating branch on i.
+template <bool UNI, bool OI>
+__device__ __forceinline__ double interp_p(const double *ec, long Pc, int i, int j, const Wts &W)
+{
+    const int I0 = i >> 1, J0 = j >> 1;
+    const bool oj = j & 1;
+    const double *r0 = ec + (long)J0 * Pc + I0;
+    if (!OI && !oj) return r0[0];
+    if (UNI) {
+        if (OI && !oj) return 0.5 * (r0[0] + r0[1]);
+        if (!OI && oj) return 0.5 * (r0[0] + r0[Pc]);
+        return 0.25 * ((r0[0] + r0[1]) + (r0[Pc] + r0[Pc + 1]));
+    }
+    const double xl = W.xl[i], xr = W.xr[i], yl = W.yl[j], yr = W.yr[j];
+    if (OI && !oj) return xl * r0[0] + xr * r0[1];
+    if (!OI && oj) return yl * r0[0] + yr * r0[Pc];
+    return yl * (xl * r0[0] + xr * r0[1]) + yr * (xl * r0[Pc] + xr * r0[Pc + 1]);
+}
+
 // profiling helpers
 void prof_collect(Ctx *c);
 struct ProfScope {
