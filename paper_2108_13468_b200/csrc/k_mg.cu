@@ -776,7 +776,9 @@ void launch_gs_prep(Ctx *c, int l, const double *b, const double *eold, const do
     ProfScope ps(c, 5, (double)L.n * (j1 - j0 + 1) * (zf ? 32.0 : 24.0));
     auto kp = L.w.uni ? k_gs_prep<true> : k_gs_prep<false>;
     // a thread per column pair; a block no wider than a row needs (the small levels)
-    const int nt = std::max(32, std::min(256, ((L.n + 2) / 2 + 31) / 32 * 32));
+    // (the row's pairs spread evenly over its segments, as seg_shape does)
+    const int prs = (L.n + 2) / 2, nsg = (prs + 255) / 256;
+    const int nt = std::max(32, std::min(256, ((prs + nsg - 1) / nsg + 31) / 32 * 32));
     const long pairs = (long)(j1 - j0 + 1) * (((L.n + 1 + 2 * nt - 1) / (2 * nt)) * (long)nt);
     kp<<<(int)std::max(1L, std::min((pairs + nt - 1) / nt, 148L * 16)), nt, 0, c->st>>>(L.n, L.pitch, eold, ec,
         ec ? c->lev[l + 1].pitch : 0, b, L.aW, L.aS, L.g, zf ? L.cd : nullptr, L.cpitch, bscaled ? 1 : 0, j0, j1, L.w);

@@ -43,7 +43,11 @@ constexpr int kRedThreads = 256;
 // a warp multiple; one block-iteration per row segment, at most kRedBlocks blocks.
 inline void seg_shape(int n, long rows, int *blocks, int *threads)
 {
-    int t = ((n + 2) / 2 + 31) / 32 * 32;
+    // the row's column pairs spread evenly over its segments (n = 2048: 1025 pairs = 5 segments of
+    // 224 threads; 256-thread blocks would leave the fifth segment with one pair)
+    const int pairs = (n + 3) / 2;
+    const int ns = (pairs + kRedThreads - 1) / kRedThreads;
+    int t = ((pairs + ns - 1) / ns + 31) / 32 * 32;
     t = t < 32 ? 32 : (t > kRedThreads ? kRedThreads : t);
     const long nseg = (n + 2 + 2L * t - 1) / (2L * t);
     const long b = rows * nseg;
